@@ -1,0 +1,112 @@
+/*
+ * rangefit_b200.h -- C ABI of the sm_100a per-pixel windowed plane-fit path.
+ *
+ * This is the drop-in boundary for the reference package `rangefit`
+ * (arxiv/paper_2103_06644, /root/reference/pkg/src/rangefit).  The reference is
+ * pure Python/numpy and has no FFI; its plugin point is the `backend` string of
+ * `fit_rect` (fitting.py:757-786) and its per-window pipeline is
+ *   compute_tan_maps (camera.py:124-135)
+ *   -> build_{rgbd,standard}_implicit_channels (integral.py:217-263)
+ *   -> scatter_from_integrals (fitting.py:420-533)
+ *   -> fit_implicit_{rgbd,standard} (fitting.py:546-579)
+ *   -> canonicalize_implicit (fitting.py:76-94).
+ * Each entry point below names the reference interface it replaces.  The
+ * Python host layer (paper_2103_06644_b200/) binds these with ctypes; see
+ * INTEGRATION.md for the binding a maintainer adds on the reference side.
+ *
+ * Conventions: no C++ exceptions cross this boundary; every call returns an
+ * rf_status; rf_last_error() returns a thread-local message.  All device
+ * buffers are caller-owned.  Calls are stream-ordered and asynchronous.
+ */
+#ifndef RANGEFIT_B200_H
+#define RANGEFIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RF_ABI_VERSION 1
+
+typedef enum rf_status {
+  RF_OK = 0,
+  RF_ERR_ARGUMENT = 1,    /* bad argument (reference: ValueError)              */
+  RF_ERR_SHAPE = 2,       /* shape / dtype mismatch (reference: ValueError)    */
+  RF_ERR_CUDA = 3,        /* CUDA runtime error                                */
+  RF_ERR_UNSUPPORTED = 4  /* valid reference input this path does not support  */
+} rf_status;
+
+/* depth element types (reference DepthImage, synth.py:69-114) */
+typedef enum rf_depth_dtype {
+  RF_DEPTH_F32_M = 0,   /* float32 metres; valid = isfinite & > 0 (synth.py:84)     */
+  RF_DEPTH_U16_MM = 1   /* uint16 millimetres; Z = mm / 1000.0, valid = mm > 0
+                           (DepthImage.from_millimeters, synth.py:111-114)         */
+} rf_depth_dtype;
+
+/* formulation bits (reference FORMULATIONS, fitting.py:45-49) */
+#define RF_IMPLICIT_STANDARD 1 /* "implicit-standard": monomials [X, Y, Z, 1]       */
+#define RF_IMPLICIT_RGBD 2     /* "implicit-rgbd" (disparity form): [tx, ty, 1, 1/Z] */
+
+/* status bits of the per-pixel status byte */
+#define RF_PIX_INPUT_VALID 1u  /* centre pixel valid (DepthImage.valid)               */
+#define RF_PIX_FIT 2u          /* centre valid and window holds >= MIN_SAMPLES (4)   */
+#define RF_PIX_DEGENERATE 4u   /* FitResult.degenerate (fitting.py:553-554)           */
+
+/* Pinhole intrinsics (reference CameraIntrinsics, camera.py:35-75). */
+typedef struct rf_intrinsics {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} rf_intrinsics;
+
+/* Per-camera device tables (reference TanAngleMaps, camera.py:78-96): the
+ * separable tan lattices tan_x[x] = (x - cx)/fx, tan_y[y] = (y - cy)/fy. */
+typedef struct rf_tables rf_tables;
+
+/* Caller-owned device output planes for one formulation, each [batch, H, W]
+ * (normal is [batch, H, W, 3], xyz interleaved).  Pixels whose status lacks
+ * RF_PIX_FIT hold NaN in every float plane. */
+typedef struct rf_pixel_out {
+  float* normal;     /* unit normal (a,b,c)/|(a,b,c)|, canonical sign (fitting.py:76-94) */
+  float* offset;     /* d/|(a,b,c)|: n.X + offset = 0                                    */
+  float* residual;   /* FitResult.rms_residual = sqrt(max(lambda,0)/n) (fitting.py:556)  */
+  float* curvature;  /* lambda_min(C3)/trace(C3) of the centred monomial scatter         */
+  uint8_t* status;   /* RF_PIX_* bits                                                    */
+} rf_pixel_out;
+
+/* Replaces compute_tan_maps (camera.py:124-135) + the camera-constant channel
+ * stack build_constant_channels (integral.py:193-199), once per camera.
+ * delta_x / delta_y (H*W float64 host arrays, CameraIntrinsics.delta_*) must be
+ * NULL or all-zero: non-separable distortion lattices return
+ * RF_ERR_UNSUPPORTED.  Validation mirrors CameraIntrinsics.__post_init__. */
+rf_status rf_tables_create(const rf_intrinsics* intrinsics, const double* delta_x,
+                           const double* delta_y, int device, rf_tables** out);
+rf_status rf_tables_destroy(rf_tables* tables);
+
+/* Replaces, for every pixel of a batch of frames, the reference pipeline
+ *   fit_rect(depth, maps, Rect(max(x-r,0), max(y-r,0), min(x+r+1,W), min(y+r+1,H)),
+ *            formulation, backend)            (fitting.py:757-786)
+ * with window = 2r+1.  depth: device pointer to batch frames of H rows, each
+ * row_pitch elements apart (frame stride = H*row_pitch).  mask: optional device
+ * uint8 [batch,H,W] (DepthImage(values, valid=mask), synth.py:88-94) or NULL.
+ * formulation_mask: RF_IMPLICIT_* bits; out_std / out_rgbd may be NULL when the
+ * matching bit is clear.  stream: a cudaStream_t (NULL = legacy default). */
+rf_status rf_fit_pixels(const rf_tables* tables, const void* depth, int dtype, int64_t batch,
+                        int32_t height, int32_t width, int64_t row_pitch, const uint8_t* mask,
+                        int32_t window, int32_t formulation_mask, const rf_pixel_out* out_std,
+                        const rf_pixel_out* out_rgbd, void* stream);
+
+/* Number of kernel launches rf_fit_pixels issues for a given formulation mask. */
+int32_t rf_launches_per_call(int32_t formulation_mask);
+
+/* Thread-local message describing the last non-RF_OK status. */
+const char* rf_last_error(void);
+
+/* RF_ABI_VERSION of the loaded library. */
+int32_t rf_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RANGEFIT_B200_H */

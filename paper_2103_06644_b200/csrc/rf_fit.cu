@@ -1,0 +1,756 @@
+// rf_fit.cu -- sm_100a kernels + C ABI for the per-pixel windowed implicit
+// plane fit (reference: rangefit fitting.py / integral.py, see
+// include/rangefit_b200.h for the boundary and DESIGN.md for the design).
+//
+// One kernel per formulation.  A CTA owns a TW x TH tile of output pixels of
+// one frame and stages its (TW+2r) x (TH+2r) input halo once:
+//   1. load   : depth -> validity mask (synth.py:84,111-114) -> fp64 primary
+//               p = 1/Z (disparity form, integral.py:211-214) or Z (standard),
+//               0 for invalid pixels, into shared memory;
+//   2. columns: running vertical window sums of the p-moments (fp64) and of
+//               the validity geometry (int32), one thread per halo column;
+//   3. rows   : each thread owns KSEG consecutive pixels of one output row,
+//               forms the horizontal window sums with a running update,
+//               giving the window's centred scatter C (3x3), mean mu and
+//               count n in tile-local coordinates (exact integer geometry,
+//               fp64 depth moments -- never image-global magnitudes);
+//   4. solve  : smallest eigenpair of the uncentred 4x4 scatter through its
+//               Schur complement on the constant monomial (solve_window),
+//               curvature, canonical sign, outputs (fp32) and status byte.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/rangefit_b200.h"
+
+namespace {
+
+constexpr int TW = 64;       // output tile width  (pixels)
+constexpr int TH = 16;       // output tile height (pixels)
+constexpr int KSEG = 4;      // consecutive output pixels per thread
+constexpr int NTHREADS = (TW / KSEG) * TH;  // 256
+constexpr int MAX_RADIUS = 32;
+
+constexpr int VAR_STD = 0;   // implicit-standard
+constexpr int VAR_DF = 1;    // implicit-rgbd (disparity form)
+
+struct KParams {
+  const void* depth;
+  const uint8_t* mask;
+  const double* tan_x;  // [W]
+  const double* tan_y;  // [H]
+  double ifx, ify;
+  int64_t row_pitch;
+  int64_t frame_stride;
+  int64_t out_frame;    // H*W
+  int H, W, r, dtype;
+  float* normal;
+  float* offset;
+  float* residual;
+  float* curvature;
+  uint8_t* status;
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double rcp_approx(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+// reciprocal to ~1 ulp: approximate seed + two Newton steps (no IEEE fixup)
+__device__ __forceinline__ double rcp_fast(double x) {
+  double y = rcp_approx(x);
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// Roots l1 <= l2 <= l3 of l^3 - a2 l^2 + a1 l - a0 (three real roots), fp32.
+// l3 by the trigonometric formula, l1/l2 by deflation (product a0/l3, sum
+// (a1 - l1 l2)/l3) so that small roots keep relative accuracy.
+__device__ __forceinline__ void trig_cubic(float a2, float a1, float a0, float& l1, float& l2,
+                                           float& l3) {
+  float q = a2 * (1.0f / 3.0f);
+  float p = fmaxf(q * q - a1 * (1.0f / 3.0f), 0.0f);
+  float sp = sqrtf(p);
+  float h = q * q * q - 0.5f * q * a1 + 0.5f * a0;
+  float den = p * sp;
+  float c = den > 0.0f ? h / den : 1.0f;
+  c = fminf(fmaxf(c, -1.0f), 1.0f);
+  float phi = acosf(c) * (1.0f / 3.0f);
+  l3 = fmaxf(q + 2.0f * sp * cosf(phi), 1e-37f);
+  float P = a0 / l3;
+  float S = (a1 - P) / l3;
+  float disc = sqrtf(fmaxf(S * S - 4.0f * P, 0.0f));
+  l2 = 0.5f * (S + disc);
+  float sd = S + disc;
+  l1 = sd > 0.0f ? 2.0f * P / sd : 0.0f;
+}
+
+struct Sym3 {
+  double c00, c01, c02, c11, c12, c22;
+};
+
+struct WindowFit {
+  double lam;       // smallest eigenvalue of the 4x4 scatter
+  double u0, u1, u2;  // coefficients of the three non-constant monomials
+  double s;         // coefficient of the constant monomial
+  float kappa;      // curvature
+  bool degenerate;
+};
+
+// Smallest eigenpair of S = [[C + n mu mu^T, n mu], [n mu^T, n]] (the
+// uncentred scatter of [m0, m1, m2, 1], fitting.py:339-381) through the
+// Schur complement on the constant monomial: C u = lam (I + beta mu mu^T) u,
+// beta = n/(n - lam), s = -beta mu.u.  det(S - l I) is the quartic
+//   l^4 - q3 l^3 + q2 l^2 - q1 l + q0   with
+//   q3 = n + t + n nu, q2 = n t + c1 + n (t nu - mu.C.mu),
+//   q1 = n c1 + det C + n mu.adj(C).mu,  q0 = n det C.
+// lam1 is found by fp64 Newton from below (fp32 trigonometric seeds of the
+// fixed-beta cubic, beta iterated to its fixed point), or -- when
+// lam1 ~ lam2 (near-tie) -- by deflating the cubic's largest root in fp64,
+// solving the remaining quadratic and polishing on the quartic.  The eigenvector is the
+// dominant column of adj(C - lam (I + beta mu mu^T)).
+// Curvature lam_min(C)/tr(C) uses the same seeds/Newton/
+// deflation on det(C - l I).
+__device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1, double m2,
+                                             double n, WindowFit& out) {
+  const double c00 = C.c00, c01 = C.c01, c02 = C.c02, c11 = C.c11, c12 = C.c12, c22 = C.c22;
+  const double A00 = c11 * c22 - c12 * c12;
+  const double A11 = c00 * c22 - c02 * c02;
+  const double A22 = c00 * c11 - c01 * c01;
+  const double A01 = c02 * c12 - c01 * c22;
+  const double A02 = c01 * c12 - c02 * c11;
+  const double A12 = c01 * c02 - c00 * c12;
+  const double t = c00 + c11 + c22;
+  const double c1 = A00 + A11 + A22;
+  const double det = c00 * A00 + c01 * A01 + c02 * A02;
+  const double nu = m0 * m0 + m1 * m1 + m2 * m2;
+  const double Cm0 = c00 * m0 + c01 * m1 + c02 * m2;
+  const double Cm1 = c01 * m0 + c11 * m1 + c12 * m2;
+  const double Cm2 = c02 * m0 + c12 * m1 + c22 * m2;
+  const double mm = m0 * Cm0 + m1 * Cm1 + m2 * Cm2;
+  const double Am0 = A00 * m0 + A01 * m1 + A02 * m2;
+  const double Am1 = A01 * m0 + A11 * m1 + A12 * m2;
+  const double Am2 = A02 * m0 + A12 * m1 + A22 * m2;
+  const double aa = m0 * Am0 + m1 * Am1 + m2 * Am2;
+  const double q3 = n + t + n * nu;
+  const double q2 = fma(n, t, c1) + n * (t * nu - mm);
+  const double q1 = fma(n, c1, det) + n * aa;
+  const double q0 = n * det;
+
+  // fp32 seeds: roots of the pencil's cubic at a fixed beta,
+  //   (1 + b nu) l^3 - (t + b (t nu - mu.C.mu)) l^2 + (c1 + b mu.adj(C).mu) l - det C,
+  // with b iterated to the fixed point b = n/(n - lam1(b)).  lam1(b) decreases
+  // in b, so successive iterates bracket lam1; their minimum is a lower bound.
+  float g1, g2, g3, k1, k2, k3, glo;
+  float bst;  // beta of the last cubic
+  const float ft = (float)t, fx = (float)(t * nu - mm), fc1 = (float)c1, faa = (float)aa,
+              fdet = (float)det, fnu = (float)nu, fn = (float)n;
+  {
+    float b = 1.0f, prev = 3.0e38f;
+    glo = 3.0e38f;
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+      const float inv = 1.0f / (1.0f + b * fnu);
+      trig_cubic((ft + b * fx) * inv, (fc1 + b * faa) * inv, fdet * inv, g1, g2, g3);
+      glo = fminf(prev, g1);
+      prev = g1;
+      bst = b;
+      b = fn / fmaxf(fn - g1, 1e-6f * fn);
+    }
+    trig_cubic(ft, fc1, fdet, k1, k2, k3);
+  }
+
+  double lam, lam2;
+  const bool tie = (g2 - g1) < 0.05f * g2;
+  if (!tie) {
+    // (A) Newton on the quartic from below lam1
+    double l = (double)glo * (1.0 - 1e-4);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const double G = fma(fma(fma(l - q3, l, q2), l, -q1), l, q0);
+      const double dG = fma(fma(fma(4.0, l, -3.0 * q3), l, 2.0 * q2), l, -q1);
+      l = fma(-G, rcp_approx(dG), l);
+    }
+    lam = l;
+    lam2 = (double)g2;
+  } else {
+    // (B) near-tie lam1 ~ lam2: deflate the (well separated) largest root of
+    // the fixed-beta cubic in fp64, solve the remaining quadratic for
+    // lam1 <= lam2, then polish lam1 on the exact quartic.
+    const double b = (double)bst;
+    const double A3 = fma(b, nu, 1.0);
+    const double A2 = fma(b, t * nu - mm, t);
+    const double A1 = fma(b, aa, c1);
+    double l3 = (double)g3;
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+      const double P = fma(fma(fma(-A3, l3, A2), l3, -A1), l3, det);
+      const double dP = fma(fma(-3.0 * A3, l3, 2.0 * A2), l3, -A1);
+      l3 = fma(-P, rcp_approx(dP), l3);
+    }
+    const double iA3 = rcp_fast(A3);
+    const double ssum = fma(A2, iA3, -l3);        // lam1 + lam2
+    const double prod = det * iA3 * rcp_fast(l3);  // lam1 * lam2
+    const double disc = sqrt(fmax(fma(ssum, ssum, -4.0 * prod), 0.0));
+    const double den = ssum + disc;
+    double l = den > 0.0 ? 2.0 * prod / den : 0.0;
+    lam2 = 0.5 * den;
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const double G = fma(fma(fma(l - q3, l, q2), l, -q1), l, q0);
+      const double dG = fma(fma(fma(4.0, l, -3.0 * q3), l, 2.0 * q2), l, -q1);
+      l = dG != 0.0 ? fma(-G, rcp_approx(dG), l) : l;
+    }
+    lam = l;
+  }
+
+  // eigenvector: dominant column of adj(C - lam B), B = I + beta mu mu^T
+  const double beta = n * rcp_fast(n - lam);
+  const double gam = lam * beta;
+  const double E00 = c00 - lam - gam * m0 * m0;
+  const double E11 = c11 - lam - gam * m1 * m1;
+  const double E22 = c22 - lam - gam * m2 * m2;
+  const double E01 = c01 - gam * m0 * m1;
+  const double E02 = c02 - gam * m0 * m2;
+  const double E12 = c12 - gam * m1 * m2;
+  const double B00 = E11 * E22 - E12 * E12;
+  const double B11 = E00 * E22 - E02 * E02;
+  const double B22 = E00 * E11 - E01 * E01;
+  double u0, u1, u2;
+  {
+    const double a0 = fabs(B00), a1 = fabs(B11), a2 = fabs(B22);
+    if (a0 >= a1 && a0 >= a2) {
+      u0 = B00;
+      u1 = E02 * E12 - E01 * E22;
+      u2 = E01 * E12 - E02 * E11;
+    } else if (a1 >= a2) {
+      u0 = E02 * E12 - E01 * E22;
+      u1 = B11;
+      u2 = E01 * E02 - E00 * E12;
+    } else {
+      u0 = E01 * E12 - E02 * E11;
+      u1 = E01 * E02 - E00 * E12;
+      u2 = B22;
+    }
+    if (a0 == 0.0 && a1 == 0.0 && a2 == 0.0) {  // rank <= 1: any null vector
+      u0 = 0.0;
+      u1 = 0.0;
+      u2 = 1.0;
+    }
+  }
+  out.u0 = u0;
+  out.u1 = u1;
+  out.u2 = u2;
+  out.s = -beta * (m0 * u0 + m1 * u1 + m2 * u2);
+  out.lam = lam;
+
+  // degenerate: gap <= 1e-9 ||S||_F (fitting.py:552-554);
+  // ||S||_F^2 = ||C||_F^2 + 2 n mu.C.mu + n^2 (1 + nu)^2
+  {
+    const double fc = c00 * c00 + c11 * c11 + c22 * c22 + 2.0 * (c01 * c01 + c02 * c02 + c12 * c12);
+    const double np1 = n * (1.0 + nu);
+    const double fro2 = fc + 2.0 * n * mm + np1 * np1;
+    const double gap = lam2 - lam;
+    out.degenerate = gap <= 0.0 || gap * gap <= 1e-18 * fro2;
+  }
+
+  // curvature: lam_min(C) / tr(C)
+  {
+    double lk;
+    const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
+    if (!top) {
+      double l = (double)k1 * (1.0 - 1e-4);
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const double P = fma(fma(t - l, l, -c1), l, det);
+        const double dP = fma(fma(-3.0, l, 2.0 * t), l, -c1);
+        l = fma(-P, rcp_approx(dP), l);
+      }
+      lk = l;
+    } else {
+      double l = (double)k3 * (1.0 + 1e-6);
+#pragma unroll
+      for (int it = 0; it < 3; ++it) {
+        const double P = fma(fma(t - l, l, -c1), l, det);
+        const double dP = fma(fma(-3.0, l, 2.0 * t), l, -c1);
+        l = fma(-P, rcp_approx(dP), l);
+      }
+      const double S = t - l;
+      const double Pp = det * rcp_fast(l);
+      const double den = S + sqrt(fmax(fma(S, S, -4.0 * Pp), 0.0));
+      lk = den > 0.0 ? 2.0 * Pp / den : 0.0;
+    }
+    out.kappa = t > 0.0 ? (float)(lk * rcp_approx(t)) : 0.0f;
+  }
+}
+
+// canonical sign + unit normal / offset (fitting.py:76-94 and SURVEY A18)
+__device__ __forceinline__ void finish_plane(double a, double b, double c, double d, float& nx,
+                                             float& ny, float& nz, float& off) {
+  // exact power-of-two rescale so the fp32 conversion neither over- nor underflows
+  double mx = fmax(fmax(fabs(a), fabs(b)), fmax(fabs(c), fabs(d)));
+  const int hi = __double2hiint(mx);
+  const int e = (hi >> 20) & 0x7ff;
+  const double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023 - e)
+  const float fa = (float)(a * sc), fb = (float)(b * sc), fc = (float)(c * sc),
+              fd = (float)(d * sc);
+  const float n4 = rsqrtf(fa * fa + fb * fb + fc * fc + fd * fd);
+  float sign = 1.0f;
+  if (fabsf(fc * n4) > 1e-9f) sign = fc > 0.0f ? 1.0f : -1.0f;
+  else if (fabsf(fb * n4) > 1e-9f) sign = fb > 0.0f ? 1.0f : -1.0f;
+  else if (fabsf(fa * n4) > 1e-9f) sign = fa > 0.0f ? 1.0f : -1.0f;
+  else if (fd < 0.0f) sign = -1.0f;
+  const float in3 = sign * rsqrtf(fa * fa + fb * fb + fc * fc);
+  nx = fa * in3;
+  ny = fb * in3;
+  nz = fc * in3;
+  off = fd * in3;
+}
+
+// depth -> (valid, Z in fp64) exactly as DepthImage does
+__device__ __forceinline__ double load_z(const KParams& P, int64_t frame, int y, int x,
+                                         bool& valid) {
+  const int64_t off = frame * P.frame_stride + (int64_t)y * P.row_pitch + x;
+  double z;
+  if (P.dtype == RF_DEPTH_U16_MM) {
+    const unsigned short mm = __ldg(reinterpret_cast<const unsigned short*>(P.depth) + off);
+    valid = mm > 0;
+    z = __ddiv_rn((double)mm, 1000.0);
+  } else {
+    const float zf = __ldg(reinterpret_cast<const float*>(P.depth) + off);
+    valid = (zf > 0.0f) && (zf <= 3.402823466e38f);  // isfinite & > 0
+    z = (double)zf;
+  }
+  if (P.mask) valid = valid && (__ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0);
+  return z;
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(NTHREADS, 2) fit_tile_kernel(const KParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int r = P.r;
+  const int HW_ = TW + 2 * r;  // halo width
+  const int HH_ = TH + 2 * r;  // halo height
+  constexpr int NVD = VAR == VAR_DF ? 3 : 5;  // fp64 vertical channels
+  constexpr int NVI = VAR == VAR_DF ? 3 : 1;  // int vertical channels
+  double* prim = reinterpret_cast<double*>(smem_raw);             // [HH_][HW_]
+  double* vd = prim + HH_ * HW_;                                  // [NVD][TH][HW_]
+  int* vi = reinterpret_cast<int*>(vd + NVD * TH * HW_);          // [NVI][TH][HW_]
+
+  const int tid = threadIdx.x;
+  const int64_t frame = blockIdx.z;
+  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+
+  // ---- 1. load halo tile -> primary
+  for (int e = tid; e < HH_ * HW_; e += NTHREADS) {
+    const int row = e / HW_, col = e - row * HW_;
+    const int y = y0 - r + row, x = x0 - r + col;
+    double p = 0.0;
+    if (y >= 0 && y < P.H && x >= 0 && x < P.W) {
+      bool valid;
+      const double z = load_z(P, frame, y, x, valid);
+      if (valid) p = VAR == VAR_DF ? __drcp_rn(z) : z;
+    }
+    prim[e] = p;
+  }
+  __syncthreads();
+
+  // ---- 2. vertical running sums, one thread per halo column
+  if (tid < HW_) {
+    double a[NVD];
+    int b[NVI];
+#pragma unroll
+    for (int k = 0; k < NVD; ++k) a[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < NVI; ++k) b[k] = 0;
+    for (int ii = 0; ii < HH_; ++ii) {
+      {
+        const double p = prim[ii * HW_ + tid];
+        const int dy = ii - r;
+        const double fdy = (double)dy;
+        const int v = p > 0.0 ? 1 : 0;
+        if (VAR == VAR_DF) {
+          a[0] += p;
+          a[1] = fma(p, p, a[1]);
+          a[2] = fma(fdy, p, a[2]);
+          b[0] += v;
+          b[1] += v * dy;
+          b[2] += v * dy * dy;
+        } else {
+          const double p2 = p * p;
+          a[0] += p;
+          a[1] += p2;
+          a[2] = fma(fdy, p, a[2]);
+          a[3] = fma(fdy, p2, a[3]);
+          a[4] = fma(fdy * fdy, p2, a[4]);
+          b[0] += v;
+        }
+      }
+      if (ii >= 2 * r) {
+        const int orow = ii - 2 * r;
+#pragma unroll
+        for (int k = 0; k < NVD; ++k) vd[(k * TH + orow) * HW_ + tid] = a[k];
+#pragma unroll
+        for (int k = 0; k < NVI; ++k) vi[(k * TH + orow) * HW_ + tid] = b[k];
+        const int io = ii - 2 * r;
+        const double p = prim[io * HW_ + tid];
+        const int dy = io - r;
+        const double fdy = (double)dy;
+        const int v = p > 0.0 ? 1 : 0;
+        if (VAR == VAR_DF) {
+          a[0] -= p;
+          a[1] = fma(-p, p, a[1]);
+          a[2] = fma(-fdy, p, a[2]);
+          b[0] -= v;
+          b[1] -= v * dy;
+          b[2] -= v * dy * dy;
+        } else {
+          const double p2 = p * p;
+          a[0] -= p;
+          a[1] -= p2;
+          a[2] = fma(-fdy, p, a[2]);
+          a[3] = fma(-fdy, p2, a[3]);
+          a[4] = fma(-fdy * fdy, p2, a[4]);
+          b[0] -= v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 3/4. horizontal running sums + per-window solve
+  const int orow = tid / (TW / KSEG);
+  const int xs = (tid % (TW / KSEG)) * KSEG;  // tile-local x of the segment's first pixel
+  const int gy = y0 + orow;
+  if (gy >= P.H) return;
+  const int gxs = x0 + xs;
+  if (gxs >= P.W) return;
+
+  const double txo = __ldg(P.tan_x + gxs);
+  const double tyo = __ldg(P.tan_y + y0);
+  const double ifx = P.ifx, ify = P.ify;
+  const double* vrow = vd + orow * HW_;
+  const int* irow = vi + orow * HW_;
+  const int vstride = TH * HW_;
+
+  // running horizontal sums (origin: segment start xs, tile row y0)
+  double h[VAR == VAR_DF ? 4 : 9];
+  long long hi[VAR == VAR_DF ? 6 : 1];
+#pragma unroll
+  for (int k = 0; k < (VAR == VAR_DF ? 4 : 9); ++k) h[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < (VAR == VAR_DF ? 6 : 1); ++k) hi[k] = 0;
+
+  auto accum = [&](int c, double sgn) {
+    const int dx = c - r - xs;
+    const double fdx = (double)dx * sgn;
+    if (VAR == VAR_DF) {
+      const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
+      const int m = irow[c], my = irow[vstride + c], myy = irow[2 * vstride + c];
+      h[0] = fma(sgn, w, h[0]);    // sum w
+      h[1] = fma(sgn, ww, h[1]);   // sum w^2
+      h[2] = fma(sgn, yw, h[2]);   // sum dy w
+      h[3] = fma(fdx, w, h[3]);    // sum dx w
+      const long long s = sgn > 0 ? 1 : -1;
+      hi[0] += s * m;              // n
+      hi[1] += s * dx * m;         // sum dx
+      hi[2] += s * my;             // sum dy
+      hi[3] += s * dx * dx * m;    // sum dx^2
+      hi[4] += s * dx * my;        // sum dx dy
+      hi[5] += s * myy;            // sum dy^2
+    } else {
+      const double z = vrow[c], z2 = vrow[vstride + c], yz = vrow[2 * vstride + c],
+                   yz2 = vrow[3 * vstride + c], y2z2 = vrow[4 * vstride + c];
+      const double fdx2 = fdx * (double)dx;
+      h[0] = fma(sgn, z, h[0]);     // S3  = sum Z
+      h[1] = fma(sgn, z2, h[1]);    // S33 = sum Z^2
+      h[2] = fma(sgn, yz, h[2]);    // S2  = sum dy Z
+      h[3] = fma(sgn, yz2, h[3]);   // S23 = sum dy Z^2
+      h[4] = fma(sgn, y2z2, h[4]);  // S22 = sum dy^2 Z^2
+      h[5] = fma(fdx, z, h[5]);     // S1  = sum dx Z
+      h[6] = fma(fdx, z2, h[6]);    // S13 = sum dx Z^2
+      h[7] = fma(fdx, yz2, h[7]);   // S12 = sum dx dy Z^2
+      h[8] = fma(fdx2, z2, h[8]);   // S11 = sum dx^2 Z^2
+      hi[0] += (sgn > 0 ? 1 : -1) * irow[c];
+    }
+  };
+
+  for (int c = xs; c <= xs + 2 * r; ++c) accum(c, 1.0);
+
+  float o_n[KSEG][3], o_off[KSEG], o_res[KSEG], o_cur[KSEG];
+  uint8_t o_st[KSEG];
+
+#pragma unroll
+  for (int j = 0; j < KSEG; ++j) {
+    if (j > 0) {
+      accum(xs + j + 2 * r, 1.0);
+      accum(xs + j - 1, -1.0);
+    }
+    const int gx = gxs + j;
+    const double pc = prim[(orow + r) * HW_ + xs + j + r];
+    uint8_t st = pc > 0.0 ? RF_PIX_INPUT_VALID : 0;
+    const int nwin = (int)hi[0];
+    float nx = __int_as_float(0x7fc00000), ny = nx, nz = nx, off = nx, res = nx, cur = nx;
+    if (st && nwin >= 4 && gx < P.W) {
+      const double nd = (double)nwin;
+      const double invn = rcp_fast(nd);
+      Sym3 C;
+      double mu0, mu1, mu2;
+      if (VAR == VAR_DF) {
+        const long long n = hi[0], sx = hi[1], sy = hi[2], sxx = hi[3], sxy = hi[4], syy = hi[5];
+        const double cq00 = (double)(n * sxx - sx * sx) * invn;
+        const double cq01 = (double)(n * sxy - sx * sy) * invn;
+        const double cq11 = (double)(n * syy - sy * sy) * invn;
+        const double mw = h[0] * invn;
+        const double fsx = (double)sx, fsy = (double)sy;
+        const double cq02 = fma(-fsx, mw, h[3]);
+        const double cq12 = fma(-fsy, mw, h[2]);
+        const double cq22 = fma(-h[0], mw, h[1]);
+        C.c00 = cq00 * (ifx * ifx);
+        C.c01 = cq01 * (ifx * ify);
+        C.c11 = cq11 * (ify * ify);
+        C.c02 = cq02 * ifx;
+        C.c12 = cq12 * ify;
+        C.c22 = cq22;
+        mu0 = fma(fsx * invn, ifx, txo);
+        mu1 = fma(fsy * invn, ify, tyo);
+        mu2 = mw;
+      } else {
+        // q = (dx Z, dy Z, Z): sums S1=h5, S2=h2, S3=h0, S11=h8, S12=h7, S22=h4,
+        // S13=h6, S23=h3, S33=h1; C_q = S_ab - S_a S_b / n
+        const double q0 = h[5] * invn, q1 = h[2] * invn, q2 = h[0] * invn;
+        const double k00 = fma(-h[5], q0, h[8]);
+        const double k01 = fma(-h[5], q1, h[7]);
+        const double k02 = fma(-h[5], q2, h[6]);
+        const double k11 = fma(-h[2], q1, h[4]);
+        const double k12 = fma(-h[2], q2, h[3]);
+        const double k22 = fma(-h[0], q2, h[1]);
+        // m = L q, L = [[ifx, 0, txo], [0, ify, tyo], [0, 0, 1]]
+        const double r00 = fma(ifx, k00, txo * k02), r01 = fma(ifx, k01, txo * k12),
+                     r02 = fma(ifx, k02, txo * k22);
+        const double r11 = fma(ify, k11, tyo * k12), r12 = fma(ify, k12, tyo * k22);
+        C.c00 = fma(ifx, r00, txo * r02);
+        C.c01 = fma(ify, r01, tyo * r02);
+        C.c02 = r02;
+        C.c11 = fma(ify, r11, tyo * r12);
+        C.c12 = r12;
+        C.c22 = k22;
+        mu0 = fma(ifx, q0, txo * q2);
+        mu1 = fma(ify, q1, tyo * q2);
+        mu2 = q2;
+      }
+      WindowFit f;
+      solve_window(C, mu0, mu1, mu2, nd, f);
+      if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
+      else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
+      res = sqrtf(fmaxf((float)(f.lam * invn), 0.0f));
+      cur = f.kappa;
+      st |= RF_PIX_FIT;
+      if (f.degenerate) st |= RF_PIX_DEGENERATE;
+    }
+    o_n[j][0] = nx;
+    o_n[j][1] = ny;
+    o_n[j][2] = nz;
+    o_off[j] = off;
+    o_res[j] = res;
+    o_cur[j] = cur;
+    o_st[j] = st;
+  }
+
+  // ---- stores
+  const int64_t pix0 = frame * P.out_frame + (int64_t)gy * P.W + gxs;
+  const bool vec = ((P.W & (KSEG - 1)) == 0) && (gxs + KSEG <= P.W);
+  if (vec) {
+    float4* pn = reinterpret_cast<float4*>(P.normal + 3 * pix0);
+    pn[0] = make_float4(o_n[0][0], o_n[0][1], o_n[0][2], o_n[1][0]);
+    pn[1] = make_float4(o_n[1][1], o_n[1][2], o_n[2][0], o_n[2][1]);
+    pn[2] = make_float4(o_n[2][2], o_n[3][0], o_n[3][1], o_n[3][2]);
+    *reinterpret_cast<float4*>(P.offset + pix0) = make_float4(o_off[0], o_off[1], o_off[2], o_off[3]);
+    *reinterpret_cast<float4*>(P.residual + pix0) = make_float4(o_res[0], o_res[1], o_res[2], o_res[3]);
+    *reinterpret_cast<float4*>(P.curvature + pix0) = make_float4(o_cur[0], o_cur[1], o_cur[2], o_cur[3]);
+    *reinterpret_cast<uchar4*>(P.status + pix0) = make_uchar4(o_st[0], o_st[1], o_st[2], o_st[3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < KSEG; ++j) {
+      if (gxs + j >= P.W) break;
+      const int64_t p = pix0 + j;
+      P.normal[3 * p + 0] = o_n[j][0];
+      P.normal[3 * p + 1] = o_n[j][1];
+      P.normal[3 * p + 2] = o_n[j][2];
+      P.offset[p] = o_off[j];
+      P.residual[p] = o_res[j];
+      P.curvature[p] = o_cur[j];
+      P.status[p] = o_st[j];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ tables
+__global__ void tan_table_kernel(double* tx, double* ty, int W, int H, double fx, double fy,
+                                 double cx, double cy) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // compute_tan_maps (camera.py:131-134) with delta = 0: ((col + 0.0) - cx) / fx
+  if (i < W) tx[i] = __ddiv_rn(((double)i + 0.0) - cx, fx);
+  if (i < H) ty[i] = __ddiv_rn(((double)i + 0.0) - cy, fy);
+}
+
+thread_local char g_err[512] = "";
+
+rf_status fail(rf_status s, const char* fmt, const char* a = "", long long b = 0,
+               long long c = 0) {
+  snprintf(g_err, sizeof(g_err), fmt, a, b, c);
+  return s;
+}
+
+size_t smem_bytes(int var, int r) {
+  const int hw = TW + 2 * r, hh = TH + 2 * r;
+  const int nvd = var == VAR_DF ? 3 : 5, nvi = var == VAR_DF ? 3 : 1;
+  return sizeof(double) * ((size_t)hh * hw + (size_t)nvd * TH * hw) + sizeof(int) * (size_t)nvi * TH * hw;
+}
+
+}  // namespace
+
+struct rf_tables {
+  rf_intrinsics intr;
+  int device;
+  double* tan_x;  // [W] device
+  double* tan_y;  // [H] device
+};
+
+extern "C" {
+
+int32_t rf_abi_version(void) { return RF_ABI_VERSION; }
+
+const char* rf_last_error(void) { return g_err; }
+
+int32_t rf_launches_per_call(int32_t formulation_mask) {
+  return ((formulation_mask & RF_IMPLICIT_STANDARD) ? 1 : 0) +
+         ((formulation_mask & RF_IMPLICIT_RGBD) ? 1 : 0);
+}
+
+rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const double* delta_y,
+                           int device, rf_tables** out) {
+  if (!in || !out) return fail(RF_ERR_ARGUMENT, "rf_tables_create: null argument%s");
+  *out = nullptr;
+  // CameraIntrinsics.__post_init__ (camera.py:54-63)
+  if (!(in->fx > 0) || !(in->fy > 0))
+    return fail(RF_ERR_ARGUMENT, "focal lengths must be positive%s");
+  if (in->width <= 0 || in->height <= 0) return fail(RF_ERR_ARGUMENT, "image size must be positive%s");
+  if (!(in->cx >= 0 && in->cx < in->width && in->cy >= 0 && in->cy < in->height))
+    return fail(RF_ERR_ARGUMENT, "principal point outside the image%s");
+  const int64_t n = (int64_t)in->width * in->height;
+  for (int64_t i = 0; delta_x && i < n; ++i)
+    if (delta_x[i] != 0.0)
+      return fail(RF_ERR_UNSUPPORTED, "non-zero delta_x lattice%s: the sm_100a path needs separable tan maps");
+  for (int64_t i = 0; delta_y && i < n; ++i)
+    if (delta_y[i] != 0.0)
+      return fail(RF_ERR_UNSUPPORTED, "non-zero delta_y lattice%s: the sm_100a path needs separable tan maps");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(RF_ERR_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  rf_tables* t = new rf_tables();
+  t->intr = *in;
+  t->device = device;
+  e = cudaMalloc(&t->tan_x, sizeof(double) * in->width);
+  if (e == cudaSuccess) e = cudaMalloc(&t->tan_y, sizeof(double) * in->height);
+  if (e == cudaSuccess) {
+    const int m = in->width > in->height ? in->width : in->height;
+    tan_table_kernel<<<(m + 255) / 256, 256>>>(t->tan_x, t->tan_y, in->width, in->height, in->fx,
+                                               in->fy, in->cx, in->cy);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    cudaFree(t->tan_x);
+    cudaFree(t->tan_y);
+    delete t;
+    return fail(RF_ERR_CUDA, "rf_tables_create: %s", cudaGetErrorString(e));
+  }
+  *out = t;
+  return RF_OK;
+}
+
+rf_status rf_tables_destroy(rf_tables* t) {
+  if (!t) return RF_OK;
+  cudaFree(t->tan_x);
+  cudaFree(t->tan_y);
+  delete t;
+  return RF_OK;
+}
+
+rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_t batch,
+                        int32_t H, int32_t W, int64_t row_pitch, const uint8_t* mask,
+                        int32_t window, int32_t fmask, const rf_pixel_out* out_std,
+                        const rf_pixel_out* out_rgbd, void* stream) {
+  if (!t || !depth) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null tables or depth%s");
+  if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM)
+    return fail(RF_ERR_SHAPE, "unknown depth dtype%s %lld", "", dtype);
+  if (H != t->intr.height || W != t->intr.width)
+    return fail(RF_ERR_SHAPE, "depth %s%lldx%lld does not match the camera tables", "", W, H);
+  if (batch < 0 || batch > 65535) return fail(RF_ERR_ARGUMENT, "batch%s %lld out of range [0, 65535]", "", batch);
+  if (row_pitch < W) return fail(RF_ERR_ARGUMENT, "row_pitch%s %lld < width", "", row_pitch);
+  if (window < 1 || (window & 1) == 0 || window / 2 > MAX_RADIUS)
+    return fail(RF_ERR_ARGUMENT, "window%s must be odd and in [1, %lld], got %lld", "",
+                2 * MAX_RADIUS + 1, window);
+  if ((fmask & ~(RF_IMPLICIT_STANDARD | RF_IMPLICIT_RGBD)) != 0 || fmask == 0)
+    return fail(RF_ERR_ARGUMENT, "formulation_mask%s %lld invalid", "", fmask);
+  if ((fmask & RF_IMPLICIT_STANDARD) && (!out_std || !out_std->normal || !out_std->offset ||
+                                         !out_std->residual || !out_std->curvature || !out_std->status))
+    return fail(RF_ERR_ARGUMENT, "implicit-standard requested without output buffers%s");
+  if ((fmask & RF_IMPLICIT_RGBD) && (!out_rgbd || !out_rgbd->normal || !out_rgbd->offset ||
+                                     !out_rgbd->residual || !out_rgbd->curvature || !out_rgbd->status))
+    return fail(RF_ERR_ARGUMENT, "implicit-rgbd requested without output buffers%s");
+  if (batch == 0) return RF_OK;
+  const int r = window / 2;
+  const dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, (unsigned)batch);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int var = 0; var < 2; ++var) {
+    const rf_pixel_out* o = var == VAR_STD ? out_std : out_rgbd;
+    if (!(fmask & (var == VAR_STD ? RF_IMPLICIT_STANDARD : RF_IMPLICIT_RGBD))) continue;
+    KParams P;
+    P.depth = depth;
+    P.mask = mask;
+    P.tan_x = t->tan_x;
+    P.tan_y = t->tan_y;
+    P.ifx = 1.0 / t->intr.fx;
+    P.ify = 1.0 / t->intr.fy;
+    P.row_pitch = row_pitch;
+    P.frame_stride = row_pitch * H;
+    P.out_frame = (int64_t)H * W;
+    P.H = H;
+    P.W = W;
+    P.r = r;
+    P.dtype = dtype;
+    P.normal = o->normal;
+    P.offset = o->offset;
+    P.residual = o->residual;
+    P.curvature = o->curvature;
+    P.status = o->status;
+    const size_t sm = smem_bytes(var, r);
+    cudaError_t e;
+    if (var == VAR_STD) {
+      e = cudaFuncSetAttribute(fit_tile_kernel<VAR_STD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e == cudaSuccess) {
+        fit_tile_kernel<VAR_STD><<<grid, NTHREADS, sm, s>>>(P);
+        e = cudaGetLastError();
+      }
+    } else {
+      e = cudaFuncSetAttribute(fit_tile_kernel<VAR_DF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e == cudaSuccess) {
+        fit_tile_kernel<VAR_DF><<<grid, NTHREADS, sm, s>>>(P);
+        e = cudaGetLastError();
+      }
+    }
+    if (e != cudaSuccess) return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  }
+  return RF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,244 @@
+"""Host side of the per-pixel path: camera tables and the batched ``fit_pixels``.
+
+Mirrors the reference's fitting vocabulary (``rangefit``):
+
+* :class:`CameraIntrinsics` -- reference ``camera.py:35-75`` (same fields and
+  validation; ``delta_x``/``delta_y`` lattices must be zero, see below).
+* :func:`compute_tan_maps` -- reference ``camera.py:124-135``; here it builds
+  the per-camera device tables (``rf_tables_create``) once.
+* :func:`fit_pixels` -- the batched per-pixel entry the reference lacks: for
+  every pixel it is ``fit_rect(depth, maps, Rect(max(x-r,0), max(y-r,0),
+  min(x+r+1,W), min(y+r+1,H)), formulation, backend)`` (``fitting.py:757-786``)
+  followed by the A18 output convention of SURVEY.md: unit normal, offset,
+  ``rms_residual``, curvature and a status byte.  Per-pixel failures become
+  status bits, never exceptions; argument errors raise ``ValueError`` like the
+  reference.
+
+Everything runs through ``librangefit_b200.so``; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+IMPLICIT_STANDARD = "implicit-standard"
+IMPLICIT_RGBD = "implicit-rgbd"
+PIXEL_FORMULATIONS = (IMPLICIT_STANDARD, IMPLICIT_RGBD)
+_FORM_BIT = {IMPLICIT_STANDARD: N.RF_IMPLICIT_STANDARD, IMPLICIT_RGBD: N.RF_IMPLICIT_RGBD}
+
+STATUS_INPUT_VALID = N.RF_PIX_INPUT_VALID
+STATUS_FIT = N.RF_PIX_FIT
+STATUS_DEGENERATE = N.RF_PIX_DEGENERATE
+
+
+@dataclass(frozen=True)
+class CameraIntrinsics:
+    """Pinhole parameters (reference ``camera.py:35-75``)."""
+
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+    delta_x: np.ndarray | None = None
+    delta_y: np.ndarray | None = None
+
+    def __post_init__(self) -> None:
+        if self.fx <= 0 or self.fy <= 0:
+            raise ValueError(f"focal lengths must be positive, got ({self.fx}, {self.fy})")
+        if self.width <= 0 or self.height <= 0:
+            raise ValueError(f"image size must be positive, got {self.width}x{self.height}")
+        if not (0 <= self.cx < self.width and 0 <= self.cy < self.height):
+            raise ValueError(
+                f"principal point ({self.cx}, {self.cy}) outside {self.width}x{self.height} image"
+            )
+        for name in ("delta_x", "delta_y"):
+            lattice = getattr(self, name)
+            if lattice is None:
+                lattice = np.zeros((self.height, self.width))
+            else:
+                lattice = np.asarray(lattice, dtype=np.float64)
+                if lattice.shape != (self.height, self.width):
+                    raise ValueError(
+                        f"{name} shape {lattice.shape} does not match image ({self.height}, {self.width})"
+                    )
+            object.__setattr__(self, name, lattice)
+
+
+@dataclass
+class TanAngleMaps:
+    """Per-camera device tables (reference ``TanAngleMaps``, ``camera.py:78-96``).
+
+    The lattices are separable (``tan_x`` depends on the column only, ``tan_y``
+    on the row only), so the device holds W + H float64 values.
+    """
+
+    intrinsics: CameraIntrinsics
+    device: int
+    _handle: ctypes.c_void_p = field(repr=False)
+
+    @property
+    def width(self) -> int:
+        return self.intrinsics.width
+
+    @property
+    def height(self) -> int:
+        return self.intrinsics.height
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if not self._handle:
+            raise ValueError("camera tables were released")
+        return self._handle
+
+    def release(self) -> None:
+        if self._handle:
+            N.load().rf_tables_destroy(self._handle)
+            self._handle = ctypes.c_void_p()
+
+    def __del__(self) -> None:  # pragma: no cover - interpreter shutdown order
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def compute_tan_maps(intrinsics: CameraIntrinsics, device: int | torch.device | None = None) -> TanAngleMaps:
+    """Build the device tan tables once per camera (``camera.py:124-135``)."""
+    if device is None:
+        device = torch.cuda.current_device()
+    if isinstance(device, torch.device):
+        device = device.index if device.index is not None else torch.cuda.current_device()
+    lib = N.load()
+    intr = N.RfIntrinsics(intrinsics.fx, intrinsics.fy, intrinsics.cx, intrinsics.cy,
+                          intrinsics.width, intrinsics.height)
+    dx = np.ascontiguousarray(intrinsics.delta_x, dtype=np.float64)
+    dy = np.ascontiguousarray(intrinsics.delta_y, dtype=np.float64)
+    handle = ctypes.c_void_p()
+    st = lib.rf_tables_create(ctypes.byref(intr), dx.ctypes.data, dy.ctypes.data, int(device),
+                              ctypes.byref(handle))
+    N.check(st, "compute_tan_maps")
+    return TanAngleMaps(intrinsics=intrinsics, device=int(device), _handle=handle)
+
+
+@dataclass
+class PixelFits:
+    """Per-pixel outputs of one formulation, each ``[B, H, W]`` (normal ``[B, H, W, 3]``)."""
+
+    normal: torch.Tensor
+    offset: torch.Tensor
+    residual: torch.Tensor
+    curvature: torch.Tensor
+    status: torch.Tensor
+
+    @staticmethod
+    def empty(batch: int, height: int, width: int, device) -> "PixelFits":
+        f = dict(dtype=torch.float32, device=device)
+        return PixelFits(
+            normal=torch.empty((batch, height, width, 3), **f),
+            offset=torch.empty((batch, height, width), **f),
+            residual=torch.empty((batch, height, width), **f),
+            curvature=torch.empty((batch, height, width), **f),
+            status=torch.empty((batch, height, width), dtype=torch.uint8, device=device),
+        )
+
+    def _c(self) -> N.RfPixelOut:
+        for t in (self.normal, self.offset, self.residual, self.curvature, self.status):
+            if not t.is_contiguous():
+                raise ValueError("output tensors must be contiguous")
+        return N.RfPixelOut(self.normal.data_ptr(), self.offset.data_ptr(), self.residual.data_ptr(),
+                            self.curvature.data_ptr(), self.status.data_ptr())
+
+    @property
+    def fit_mask(self) -> torch.Tensor:
+        return (self.status & STATUS_FIT) != 0
+
+
+def _depth_dtype(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return N.RF_DEPTH_F32_M
+    if t.dtype in (torch.uint16, torch.int16):
+        return N.RF_DEPTH_U16_MM
+    raise ValueError(f"depth must be float32 metres or uint16 millimetres, got {t.dtype}")
+
+
+def fit_pixels(
+    depth: torch.Tensor,
+    maps: TanAngleMaps,
+    window: int,
+    formulations=PIXEL_FORMULATIONS,
+    mask: torch.Tensor | None = None,
+    out: dict | None = None,
+    stream: torch.cuda.Stream | None = None,
+) -> dict:
+    """Fit a plane over the (2r+1)-square window around every pixel.
+
+    ``depth``: CUDA tensor ``[B, H, W]`` or ``[H, W]``, float32 metres or uint16
+    millimetres (converted on device as ``mm / 1000.0``, reference
+    ``synth.py:111-114``).  Rows may be padded (``depth.stride(-2) >= W``); the
+    last dimension must be contiguous.  Returns ``{formulation: PixelFits}``.
+    The launch is asynchronous on ``stream`` (default: torch's current stream).
+    """
+    if isinstance(formulations, str):
+        formulations = (formulations,)
+    formulations = tuple(formulations)
+    for f in formulations:
+        if f not in _FORM_BIT:
+            raise ValueError(f"unknown formulation {f!r}; expected one of {PIXEL_FORMULATIONS}")
+    if not isinstance(depth, torch.Tensor) or not depth.is_cuda:
+        raise ValueError("depth must be a CUDA tensor (the sm_100a path has no CPU fallback)")
+    squeeze = depth.dim() == 2
+    d = depth.unsqueeze(0) if squeeze else depth
+    if d.dim() != 3:
+        raise ValueError(f"depth must be [B, H, W] or [H, W], got shape {tuple(depth.shape)}")
+    B, H, W = d.shape
+    if (H, W) != (maps.height, maps.width):
+        raise ValueError(f"depth {W}x{H} does not match maps {maps.width}x{maps.height}")
+    if d.stride(-1) != 1 or (B > 1 and d.stride(0) != d.stride(1) * H):
+        d = d.contiguous()
+    dtype = _depth_dtype(d)
+    if d.device.index != maps.device:
+        raise ValueError(f"depth on cuda:{d.device.index} but maps on cuda:{maps.device}")
+    if window < 1 or window % 2 == 0:
+        raise ValueError(f"window must be a positive odd integer, got {window}")
+    mptr = None
+    if mask is not None:
+        m = mask.unsqueeze(0) if mask.dim() == 2 else mask
+        if tuple(m.shape) != (B, H, W):
+            raise ValueError(f"mask shape {tuple(mask.shape)} != depth shape {tuple(depth.shape)}")
+        m = m.to(device=d.device, dtype=torch.uint8).contiguous()
+        mptr = m.data_ptr()
+    if out is None:
+        out = {f: PixelFits.empty(B, H, W, d.device) for f in formulations}
+    fmask = 0
+    for f in formulations:
+        fmask |= _FORM_BIT[f]
+    o_std = out[IMPLICIT_STANDARD]._c() if IMPLICIT_STANDARD in formulations else None
+    o_rgbd = out[IMPLICIT_RGBD]._c() if IMPLICIT_RGBD in formulations else None
+    if stream is None:
+        stream = torch.cuda.current_stream(d.device)
+    st = N.load().rf_fit_pixels(
+        maps.handle, d.data_ptr(), dtype, B, H, W, d.stride(-2), mptr, int(window), fmask,
+        ctypes.byref(o_std) if o_std is not None else None,
+        ctypes.byref(o_rgbd) if o_rgbd is not None else None,
+        ctypes.c_void_p(stream.cuda_stream),
+    )
+    N.check(st, "fit_pixels")
+    if squeeze:
+        return {f: PixelFits(*(getattr(out[f], k)[0] for k in ("normal", "offset", "residual", "curvature", "status")))
+                for f in formulations}
+    return {f: out[f] for f in formulations}
+
+
+def launches_per_call(formulations=PIXEL_FORMULATIONS) -> int:
+    fmask = 0
+    for f in formulations:
+        fmask |= _FORM_BIT[f]
+    return int(N.load().rf_launches_per_call(fmask))
