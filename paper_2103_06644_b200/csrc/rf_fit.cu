@@ -68,26 +68,52 @@ __device__ __forceinline__ double rcp_fast(double x) {
   return fma(y, e, y);
 }
 
-// Roots l1 <= l2 <= l3 of l^3 - a2 l^2 + a1 l - a0 (three real roots), fp32.
-// l3 by the trigonometric formula, l1/l2 by deflation (product a0/l3, sum
-// (a1 - l1 l2)/l3) so that small roots keep relative accuracy.
+__device__ __forceinline__ float frcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float fsqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// acos on [-1, 1], |error| <= 2e-8 rad (Abramowitz & Stegun 4.4.46)
+__device__ __forceinline__ float facos(float x) {
+  const float ax = fabsf(x);
+  float p = fmaf(ax, -0.0012624911f, 0.0066700901f);
+  p = fmaf(ax, p, -0.0170881256f);
+  p = fmaf(ax, p, 0.0308918810f);
+  p = fmaf(ax, p, -0.0501743046f);
+  p = fmaf(ax, p, 0.0889789874f);
+  p = fmaf(ax, p, -0.2145988016f);
+  p = fmaf(ax, p, 1.5707963050f);
+  const float r = fsqrt(fmaxf(1.0f - ax, 0.0f)) * p;
+  return x < 0.0f ? 3.14159265358979f - r : r;
+}
+
+// Roots l1 <= l2 <= l3 of l^3 - a2 l^2 + a1 l - a0 (three real roots), fp32
+// seeds for the fp64 refinement.  l3 by the trigonometric formula, l1/l2 by
+// deflation (product a0/l3, sum (a1 - l1 l2)/l3) so that small roots keep
+// their relative accuracy.  Fast approximate intrinsics throughout (~1e-6).
 __device__ __forceinline__ void trig_cubic(float a2, float a1, float a0, float& l1, float& l2,
                                            float& l3) {
-  float q = a2 * (1.0f / 3.0f);
-  float p = fmaxf(q * q - a1 * (1.0f / 3.0f), 0.0f);
-  float sp = sqrtf(p);
-  float h = q * q * q - 0.5f * q * a1 + 0.5f * a0;
-  float den = p * sp;
-  float c = den > 0.0f ? h / den : 1.0f;
-  c = fminf(fmaxf(c, -1.0f), 1.0f);
-  float phi = acosf(c) * (1.0f / 3.0f);
-  l3 = fmaxf(q + 2.0f * sp * cosf(phi), 1e-37f);
-  float P = a0 / l3;
-  float S = (a1 - P) / l3;
-  float disc = sqrtf(fmaxf(S * S - 4.0f * P, 0.0f));
-  l2 = 0.5f * (S + disc);
-  float sd = S + disc;
-  l1 = sd > 0.0f ? 2.0f * P / sd : 0.0f;
+  const float q = a2 * (1.0f / 3.0f);
+  const float p = fmaxf(fmaf(q, q, -a1 * (1.0f / 3.0f)), 1e-37f);
+  const float isp = rsqrtf(p);
+  const float sp = p * isp;
+  const float h = fmaf(q * q - 0.5f * a1, q, 0.5f * a0);
+  const float c = fminf(fmaxf(h * isp * isp * isp, -1.0f), 1.0f);
+  const float phi = facos(c) * (1.0f / 3.0f);
+  l3 = fmaxf(fmaf(2.0f * sp, __cosf(phi), q), 1e-37f);
+  const float il3 = frcp(l3);
+  const float P = a0 * il3;
+  const float S = (a1 - P) * il3;
+  const float sd = S + fsqrt(fmaxf(fmaf(S, S, -4.0f * P), 0.0f));
+  l2 = 0.5f * sd;
+  l1 = sd > 0.0f ? 2.0f * P * frcp(sd) : 0.0f;
 }
 
 struct Sym3 {
@@ -109,10 +135,10 @@ struct WindowFit {
 //   l^4 - q3 l^3 + q2 l^2 - q1 l + q0   with
 //   q3 = n + t + n nu, q2 = n t + c1 + n (t nu - mu.C.mu),
 //   q1 = n c1 + det C + n mu.adj(C).mu,  q0 = n det C.
-// lam1 is found by fp64 Newton from below (fp32 trigonometric seeds of the
-// fixed-beta cubic, beta iterated to its fixed point), or -- when
-// lam1 ~ lam2 (near-tie) -- by deflating the cubic's largest root in fp64,
-// solving the remaining quadratic and polishing on the quartic.  The eigenvector is the
+// lam1 is found by fp64 Newton from a lower bound (fp32 trigonometric seeds
+// of the beta=1 cubic), or -- when lam1 ~ lam2 (near-tie) -- by deflating
+// the cubic's largest root in fp64, solving the remaining quadratic and
+// polishing on the quartic.  The eigenvector is the
 // dominant column of adj(C - lam (I + beta mu mu^T)).
 // Curvature lam_min(C)/tr(C) uses the same seeds/Newton/
 // deflation on det(C - l I).
@@ -142,36 +168,26 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
   const double q1 = fma(n, c1, det) + n * aa;
   const double q0 = n * det;
 
-  // fp32 seeds: roots of the pencil's cubic at a fixed beta,
-  //   (1 + b nu) l^3 - (t + b (t nu - mu.C.mu)) l^2 + (c1 + b mu.adj(C).mu) l - det C,
-  // with b iterated to the fixed point b = n/(n - lam1(b)).  lam1(b) decreases
-  // in b, so successive iterates bracket lam1; their minimum is a lower bound.
-  float g1, g2, g3, k1, k2, k3, glo;
-  float bst;  // beta of the last cubic
-  const float ft = (float)t, fx = (float)(t * nu - mm), fc1 = (float)c1, faa = (float)aa,
-              fdet = (float)det, fnu = (float)nu, fn = (float)n;
+  // fp32 seeds: roots g1 <= g2 <= g3 of the pencil's cubic at beta = 1,
+  //   (1 + nu) l^3 - (t + t nu - mu.C.mu) l^2 + (c1 + mu.adj(C).mu) l - det C.
+  // lam1(beta) decreases with beta and d lam/d beta >= -lam/beta, so with
+  // beta(lam1) <= n/(n - g1):  g1 (1 - g1/n) <= lam1 <= g1.
+  float g1, g2, g3, k1, k2, k3;
+  const float ft = (float)t, fc1 = (float)c1, fdet = (float)det, fnu = (float)nu, fn = (float)n;
   {
-    float b = 1.0f, prev = 3.0e38f;
-    glo = 3.0e38f;
-#pragma unroll
-    for (int it = 0; it < 3; ++it) {
-      const float inv = 1.0f / (1.0f + b * fnu);
-      trig_cubic((ft + b * fx) * inv, (fc1 + b * faa) * inv, fdet * inv, g1, g2, g3);
-      glo = fminf(prev, g1);
-      prev = g1;
-      bst = b;
-      b = fn / fmaxf(fn - g1, 1e-6f * fn);
-    }
+    const float inv = frcp(1.0f + fnu);
+    trig_cubic((float)(t + t * nu - mm) * inv, (float)(c1 + aa) * inv, fdet * inv, g1, g2, g3);
     trig_cubic(ft, fc1, fdet, k1, k2, k3);
   }
+  const float grel = g1 * frcp(fn);
 
   double lam, lam2;
   const bool tie = (g2 - g1) < 0.05f * g2;
   if (!tie) {
-    // (A) Newton on the quartic from below lam1
-    double l = (double)glo * (1.0 - 1e-4);
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
+    // (A) Newton on the quartic from below lam1 (monotone convergence)
+    double l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
+    const int iters = grel > 1e-2f ? 8 : (grel > 1e-3f ? 4 : 3);
+    for (int it = 0; it < iters; ++it) {
       const double G = fma(fma(fma(l - q3, l, q2), l, -q1), l, q0);
       const double dG = fma(fma(fma(4.0, l, -3.0 * q3), l, 2.0 * q2), l, -q1);
       l = fma(-G, rcp_approx(dG), l);
@@ -180,15 +196,14 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     lam2 = (double)g2;
   } else {
     // (B) near-tie lam1 ~ lam2: deflate the (well separated) largest root of
-    // the fixed-beta cubic in fp64, solve the remaining quadratic for
-    // lam1 <= lam2, then polish lam1 on the exact quartic.
-    const double b = (double)bst;
+    // the cubic at beta* = n/(n - g1) in fp64, solve the remaining quadratic
+    // for lam1 <= lam2 of that pencil, then polish lam1 on the exact quartic.
+    const double b = n * rcp_fast(n - (double)g1);
     const double A3 = fma(b, nu, 1.0);
     const double A2 = fma(b, t * nu - mm, t);
     const double A1 = fma(b, aa, c1);
     double l3 = (double)g3;
-#pragma unroll
-    for (int it = 0; it < 3; ++it) {
+    for (int it = 0; it < 4; ++it) {
       const double P = fma(fma(fma(-A3, l3, A2), l3, -A1), l3, det);
       const double dP = fma(fma(-3.0 * A3, l3, 2.0 * A2), l3, -A1);
       l3 = fma(-P, rcp_approx(dP), l3);
@@ -196,12 +211,11 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     const double iA3 = rcp_fast(A3);
     const double ssum = fma(A2, iA3, -l3);        // lam1 + lam2
     const double prod = det * iA3 * rcp_fast(l3);  // lam1 * lam2
-    const double disc = sqrt(fmax(fma(ssum, ssum, -4.0 * prod), 0.0));
+    const double disc = (double)fsqrt((float)fmax(fma(ssum, ssum, -4.0 * prod), 0.0));
     const double den = ssum + disc;
-    double l = den > 0.0 ? 2.0 * prod / den : 0.0;
+    double l = den > 0.0 ? 2.0 * prod * rcp_fast(den) : 0.0;
     lam2 = 0.5 * den;
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {
+    for (int it = 0; it < 3; ++it) {
       const double G = fma(fma(fma(l - q3, l, q2), l, -q1), l, q0);
       const double dG = fma(fma(fma(4.0, l, -3.0 * q3), l, 2.0 * q2), l, -q1);
       l = dG != 0.0 ? fma(-G, rcp_approx(dG), l) : l;
@@ -251,12 +265,17 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
 
   // degenerate: gap <= 1e-9 ||S||_F (fitting.py:552-554);
   // ||S||_F^2 = ||C||_F^2 + 2 n mu.C.mu + n^2 (1 + nu)^2
+  // (trace(S)/2 <= ||S||_F <= trace(S) = q3 for PSD S: only near-ties need the norm)
   {
-    const double fc = c00 * c00 + c11 * c11 + c22 * c22 + 2.0 * (c01 * c01 + c02 * c02 + c12 * c12);
-    const double np1 = n * (1.0 + nu);
-    const double fro2 = fc + 2.0 * n * mm + np1 * np1;
     const double gap = lam2 - lam;
-    out.degenerate = gap <= 0.0 || gap * gap <= 1e-18 * fro2;
+    if (gap > 1e-9 * q3) {
+      out.degenerate = false;
+    } else {
+      const double fc = c00 * c00 + c11 * c11 + c22 * c22 + 2.0 * (c01 * c01 + c02 * c02 + c12 * c12);
+      const double np1 = n * (1.0 + nu);
+      const double fro2 = fc + 2.0 * n * mm + np1 * np1;
+      out.degenerate = gap <= 0.0 || gap * gap <= 1e-18 * fro2;
+    }
   }
 
   // curvature: lam_min(C) / tr(C)
@@ -264,9 +283,10 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     double lk;
     const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
     if (!top) {
-      double l = (double)k1 * (1.0 - 1e-4);
-#pragma unroll
-      for (int it = 0; it < 2; ++it) {
+      const bool wide = (k2 - k1) > 0.02f * k2;
+      double l = wide ? (double)k1 : (double)k1 * (1.0 - 1e-4);
+      const int iters = wide ? 1 : 3;
+      for (int it = 0; it < iters; ++it) {
         const double P = fma(fma(t - l, l, -c1), l, det);
         const double dP = fma(fma(-3.0, l, 2.0 * t), l, -c1);
         l = fma(-P, rcp_approx(dP), l);
@@ -282,10 +302,10 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
       }
       const double S = t - l;
       const double Pp = det * rcp_fast(l);
-      const double den = S + sqrt(fmax(fma(S, S, -4.0 * Pp), 0.0));
-      lk = den > 0.0 ? 2.0 * Pp / den : 0.0;
+      const double den = S + (double)fsqrt((float)fmax(fma(S, S, -4.0 * Pp), 0.0));
+      lk = den > 0.0 ? 2.0 * Pp * rcp_fast(den) : 0.0;
     }
-    out.kappa = t > 0.0 ? (float)(lk * rcp_approx(t)) : 0.0f;
+    out.kappa = t > 0.0 ? (float)lk * frcp(ft) : 0.0f;
   }
 }
 
@@ -293,9 +313,9 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
 __device__ __forceinline__ void finish_plane(double a, double b, double c, double d, float& nx,
                                              float& ny, float& nz, float& off) {
   // exact power-of-two rescale so the fp32 conversion neither over- nor underflows
-  double mx = fmax(fmax(fabs(a), fabs(b)), fmax(fabs(c), fabs(d)));
-  const int hi = __double2hiint(mx);
-  const int e = (hi >> 20) & 0x7ff;
+  const int hm = max(max(__double2hiint(a) & 0x7ff00000, __double2hiint(b) & 0x7ff00000),
+                     max(__double2hiint(c) & 0x7ff00000, __double2hiint(d) & 0x7ff00000));
+  const int e = hm >> 20;
   const double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023 - e)
   const float fa = (float)(a * sc), fb = (float)(b * sc), fc = (float)(c * sc),
               fd = (float)(d * sc);
@@ -347,77 +367,71 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_tile_kernel(const KParams P) 
   const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
 
   // ---- 1. load halo tile -> primary
-  for (int e = tid; e < HH_ * HW_; e += NTHREADS) {
-    const int row = e / HW_, col = e - row * HW_;
-    const int y = y0 - r + row, x = x0 - r + col;
-    double p = 0.0;
-    if (y >= 0 && y < P.H && x >= 0 && x < P.W) {
-      bool valid;
-      const double z = load_z(P, frame, y, x, valid);
-      if (valid) p = VAR == VAR_DF ? __drcp_rn(z) : z;
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int row = warp; row < HH_; row += NTHREADS / 32) {
+      const int y = y0 - r + row;
+      const bool yin = y >= 0 && y < P.H;
+      for (int col = lane; col < HW_; col += 32) {
+        const int x = x0 - r + col;
+        double p = 0.0;
+        if (yin && x >= 0 && x < P.W) {
+          bool valid;
+          const double z = load_z(P, frame, y, x, valid);
+          if (valid) p = VAR == VAR_DF ? rcp_fast(z) : z;
+        }
+        prim[row * HW_ + col] = p;
+      }
     }
-    prim[e] = p;
   }
   __syncthreads();
 
-  // ---- 2. vertical running sums, one thread per halo column
-  if (tid < HW_) {
-    double a[NVD];
-    int b[NVI];
+  // ---- 2. vertical running sums.  Each halo column is split into `parts`
+  // row segments so that every thread of the CTA has a column segment; each
+  // segment warms up on its 2r leading rows, then slides down.
+  {
+    const int parts = max(1, min(NTHREADS / HW_, TH));
+    const int col = tid % HW_;
+    const int part = tid / HW_;
+    if (part < parts) {
+      const int o0 = (part * TH) / parts, o1 = ((part + 1) * TH) / parts;  // output rows [o0, o1)
+      double a[NVD];
+      int b[NVI];
 #pragma unroll
-    for (int k = 0; k < NVD; ++k) a[k] = 0.0;
+      for (int k = 0; k < NVD; ++k) a[k] = 0.0;
 #pragma unroll
-    for (int k = 0; k < NVI; ++k) b[k] = 0;
-    for (int ii = 0; ii < HH_; ++ii) {
-      {
-        const double p = prim[ii * HW_ + tid];
+      for (int k = 0; k < NVI; ++k) b[k] = 0;
+      auto add = [&](int ii, double sg) {
+        const double p = prim[ii * HW_ + col];
         const int dy = ii - r;
-        const double fdy = (double)dy;
-        const int v = p > 0.0 ? 1 : 0;
+        const double fdy = __int2double_rn(dy) * sg;
+        const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
         if (VAR == VAR_DF) {
-          a[0] += p;
-          a[1] = fma(p, p, a[1]);
+          a[0] = fma(sg, p, a[0]);
+          a[1] = fma(sg * p, p, a[1]);
           a[2] = fma(fdy, p, a[2]);
           b[0] += v;
           b[1] += v * dy;
           b[2] += v * dy * dy;
         } else {
           const double p2 = p * p;
-          a[0] += p;
-          a[1] += p2;
+          a[0] = fma(sg, p, a[0]);
+          a[1] = fma(sg, p2, a[1]);
           a[2] = fma(fdy, p, a[2]);
           a[3] = fma(fdy, p2, a[3]);
-          a[4] = fma(fdy * fdy, p2, a[4]);
+          a[4] = fma(fdy * __int2double_rn(dy), p2, a[4]);
           b[0] += v;
         }
-      }
-      if (ii >= 2 * r) {
-        const int orow = ii - 2 * r;
+      };
+      // window of output row o covers input rows [o, o + 2r]
+      for (int ii = o0; ii < o0 + 2 * r; ++ii) add(ii, 1.0);
+      for (int o = o0; o < o1; ++o) {
+        add(o + 2 * r, 1.0);
 #pragma unroll
-        for (int k = 0; k < NVD; ++k) vd[(k * TH + orow) * HW_ + tid] = a[k];
+        for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * HW_ + col] = a[k];
 #pragma unroll
-        for (int k = 0; k < NVI; ++k) vi[(k * TH + orow) * HW_ + tid] = b[k];
-        const int io = ii - 2 * r;
-        const double p = prim[io * HW_ + tid];
-        const int dy = io - r;
-        const double fdy = (double)dy;
-        const int v = p > 0.0 ? 1 : 0;
-        if (VAR == VAR_DF) {
-          a[0] -= p;
-          a[1] = fma(-p, p, a[1]);
-          a[2] = fma(-fdy, p, a[2]);
-          b[0] -= v;
-          b[1] -= v * dy;
-          b[2] -= v * dy * dy;
-        } else {
-          const double p2 = p * p;
-          a[0] -= p;
-          a[1] -= p2;
-          a[2] = fma(-fdy, p, a[2]);
-          a[3] = fma(-fdy, p2, a[3]);
-          a[4] = fma(-fdy * fdy, p2, a[4]);
-          b[0] -= v;
-        }
+        for (int k = 0; k < NVI; ++k) vi[(k * TH + o) * HW_ + col] = b[k];
+        add(o, -1.0);
       }
     }
   }
@@ -448,7 +462,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_tile_kernel(const KParams P) 
 
   auto accum = [&](int c, double sgn) {
     const int dx = c - r - xs;
-    const double fdx = (double)dx * sgn;
+    const double fdx = __int2double_rn(dx) * sgn;
     if (VAR == VAR_DF) {
       const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
       const int m = irow[c], my = irow[vstride + c], myy = irow[2 * vstride + c];
@@ -548,7 +562,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_tile_kernel(const KParams P) 
       solve_window(C, mu0, mu1, mu2, nd, f);
       if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
       else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
-      res = sqrtf(fmaxf((float)(f.lam * invn), 0.0f));
+      res = fsqrt(fmaxf((float)(f.lam * invn), 0.0f));
       cur = f.kappa;
       st |= RF_PIX_FIT;
       if (f.degenerate) st |= RF_PIX_DEGENERATE;
