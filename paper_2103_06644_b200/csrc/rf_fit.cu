@@ -136,9 +136,9 @@ struct WindowFit {
 //   q3 = n + t + n nu, q2 = n t + c1 + n (t nu - mu.C.mu),
 //   q1 = n c1 + det C + n mu.adj(C).mu,  q0 = n det C.
 // lam1 is found by fp64 Newton from a lower bound (fp32 trigonometric seeds
-// of the beta=1 cubic), or -- when lam1 ~ lam2 (near-tie) -- by deflating
-// the cubic's largest root in fp64, solving the remaining quadratic and
-// polishing on the quartic.  The eigenvector is the
+// of the beta=1 cubic), or -- when lam1 ~ lam2 (near-tie) -- by exact
+// backward deflation of the quartic's two largest roots and the remaining
+// quadratic.  The eigenvector is the
 // dominant column of adj(C - lam (I + beta mu mu^T)).
 // Curvature lam_min(C)/tr(C) uses the same seeds/Newton/
 // deflation on det(C - l I).
@@ -184,43 +184,53 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
   double lam, lam2;
   const bool tie = (g2 - g1) < 0.05f * g2;
   if (!tie) {
-    // (A) Newton on the quartic from below lam1 (monotone convergence)
+    // (A) Newton on the quartic from the lower bound: monotone convergence,
+    // stop once the step is below 1e-9 relative (the remaining error is then
+    // ~step^2/gap).  Three steps in the common case; pathological windows
+    // (lam/n not small) take longer.
     double l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
-    const int iters = grel > 1e-2f ? 8 : (grel > 1e-3f ? 4 : 3);
-    for (int it = 0; it < iters; ++it) {
+    for (int it = 0; it < 64; ++it) {
       const double G = fma(fma(fma(l - q3, l, q2), l, -q1), l, q0);
       const double dG = fma(fma(fma(4.0, l, -3.0 * q3), l, 2.0 * q2), l, -q1);
-      l = fma(-G, rcp_approx(dG), l);
+      const double step = G * rcp_approx(dG);
+      l -= step;
+      if (!(fabs(step) > 1e-9 * l)) break;
     }
     lam = l;
     lam2 = (double)g2;
   } else {
-    // (B) near-tie lam1 ~ lam2: deflate the (well separated) largest root of
-    // the cubic at beta* = n/(n - g1) in fp64, solve the remaining quadratic
-    // for lam1 <= lam2 of that pencil, then polish lam1 on the exact quartic.
-    const double b = n * rcp_fast(n - (double)g1);
-    const double A3 = fma(b, nu, 1.0);
-    const double A2 = fma(b, t * nu - mm, t);
-    const double A1 = fma(b, aa, c1);
-    double l3 = (double)g3;
-    for (int it = 0; it < 4; ++it) {
-      const double P = fma(fma(fma(-A3, l3, A2), l3, -A1), l3, det);
-      const double dP = fma(fma(-3.0 * A3, l3, 2.0 * A2), l3, -A1);
-      l3 = fma(-P, rcp_approx(dP), l3);
+    // (B) near-tie lam1 ~ lam2: exact deflation of the quartic.  lam4 (the
+    // largest root, ~n(1+nu)) and then lam3 are found by Newton from above
+    // (upper bounds q3 and lam1+lam2+lam3), each divided out by backward
+    // deflation (stable for the largest root); the quadratic left over has
+    // roots lam1 <= lam2, solved in the cancellation-free form.
+    double l4 = q3;
+    for (int it = 0; it < 64; ++it) {
+      const double G = fma(fma(fma(l4 - q3, l4, q2), l4, -q1), l4, q0);
+      const double dG = fma(fma(fma(4.0, l4, -3.0 * q3), l4, 2.0 * q2), l4, -q1);
+      const double step = G * rcp_approx(dG);
+      l4 -= step;
+      if (!(fabs(step) > 1e-15 * l4)) break;
     }
-    const double iA3 = rcp_fast(A3);
-    const double ssum = fma(A2, iA3, -l3);        // lam1 + lam2
-    const double prod = det * iA3 * rcp_fast(l3);  // lam1 * lam2
-    const double disc = (double)fsqrt((float)fmax(fma(ssum, ssum, -4.0 * prod), 0.0));
-    const double den = ssum + disc;
-    double l = den > 0.0 ? 2.0 * prod * rcp_fast(den) : 0.0;
+    const double i4 = rcp_fast(l4);
+    const double h0 = -q0 * i4;             // -lam1 lam2 lam3
+    const double h1 = (q1 + h0) * i4;       // lam1 lam2 + lam1 lam3 + lam2 lam3
+    const double h2 = (h1 - q2) * i4;       // -(lam1 + lam2 + lam3)
+    double l3 = -h2;
+    for (int it = 0; it < 64; ++it) {
+      const double H = fma(fma(l3 + h2, l3, h1), l3, h0);
+      const double dH = fma(fma(3.0, l3, 2.0 * h2), l3, h1);
+      const double step = H * rcp_approx(dH);
+      l3 -= step;
+      if (!(fabs(step) > 1e-15 * l3)) break;
+    }
+    const double i3 = rcp_fast(l3);
+    const double e0 = -h0 * i3;             // lam1 lam2
+    const double e1 = (e0 - h1) * i3;       // -(lam1 + lam2)
+    const double disc = (double)fsqrt((float)fmax(fma(e1, e1, -4.0 * e0), 0.0));
+    const double den = disc - e1;           // 2 lam2
+    lam = den > 0.0 ? 2.0 * e0 * rcp_fast(den) : 0.0;
     lam2 = 0.5 * den;
-    for (int it = 0; it < 3; ++it) {
-      const double G = fma(fma(fma(l - q3, l, q2), l, -q1), l, q0);
-      const double dG = fma(fma(fma(4.0, l, -3.0 * q3), l, 2.0 * q2), l, -q1);
-      l = dG != 0.0 ? fma(-G, rcp_approx(dG), l) : l;
-    }
-    lam = l;
   }
 
   // eigenvector: dominant column of adj(C - lam B), B = I + beta mu mu^T
@@ -283,22 +293,25 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     double lk;
     const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
     if (!top) {
-      const bool wide = (k2 - k1) > 0.02f * k2;
-      double l = wide ? (double)k1 : (double)k1 * (1.0 - 1e-4);
-      const int iters = wide ? 1 : 3;
-      for (int it = 0; it < iters; ++it) {
+      // Newton from below lam_min (monotone); 1-2 steps when well separated
+      double l = (double)k1 * (1.0 - 1e-5);
+      for (int it = 0; it < 64; ++it) {
         const double P = fma(fma(t - l, l, -c1), l, det);
         const double dP = fma(fma(-3.0, l, 2.0 * t), l, -c1);
-        l = fma(-P, rcp_approx(dP), l);
+        const double step = P * rcp_approx(dP);
+        l -= step;
+        if (!(fabs(step) > 1e-8 * l)) break;
       }
       lk = l;
     } else {
-      double l = (double)k3 * (1.0 + 1e-6);
-#pragma unroll
-      for (int it = 0; it < 3; ++it) {
+      // near-tie at the bottom: Newton from above lam_max, then deflate
+      double l = fmin((double)k3 * (1.0 + 1e-5), t);
+      for (int it = 0; it < 64; ++it) {
         const double P = fma(fma(t - l, l, -c1), l, det);
         const double dP = fma(fma(-3.0, l, 2.0 * t), l, -c1);
-        l = fma(-P, rcp_approx(dP), l);
+        const double step = P * rcp_approx(dP);
+        l -= step;
+        if (!(fabs(step) > 1e-14 * l)) break;
       }
       const double S = t - l;
       const double Pp = det * rcp_fast(l);
