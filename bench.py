@@ -135,13 +135,9 @@ def barrier(world):
 
 
 def max_over_ranks(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch.distributed as dist
+    from paper_2103_06644_b200.shard import max_over_ranks as _max
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return _max(x, world, "cuda" if torch.cuda.is_available() else "cpu")
 
 
 # ----------------------------------------------------------------- CPU legs
@@ -213,7 +209,9 @@ def run_ours(args, world, rank, local):
     dev = torch.device("cuda", local)
     cfg = scenes.CONFIGS[CONFIG_NAME]
     B, H, W = FRAMES, cfg.height, cfg.width
-    depth = scenes.render_batch(cfg, frames=B, device=dev, seed_base=1000 * 2 + 100000 * rank)
+    from paper_2103_06644_b200.shard import rank_seed_base
+
+    depth = scenes.render_batch(cfg, frames=B, device=dev, seed_base=rank_seed_base(2, rank))
     cam = rf.CameraIntrinsics(cfg.f, cfg.f, cfg.cx, cfg.cy, W, H)
     maps = rf.compute_tan_maps(cam, dev)
     forms = rf.PIXEL_FORMULATIONS

@@ -716,7 +716,8 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
                         int32_t H, int32_t W, int64_t row_pitch, const uint8_t* mask,
                         int32_t window, int32_t fmask, const rf_pixel_out* out_std,
                         const rf_pixel_out* out_rgbd, void* stream) {
-  if (!t || !depth) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null tables or depth%s");
+  if (!t) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null tables%s");
+  if (!depth && batch != 0) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null depth%s");
   if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM)
     return fail(RF_ERR_SHAPE, "unknown depth dtype%s %lld", "", dtype);
   if (H != t->intr.height || W != t->intr.width)
@@ -728,13 +729,13 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
                 2 * MAX_RADIUS + 1, window);
   if ((fmask & ~(RF_IMPLICIT_STANDARD | RF_IMPLICIT_RGBD)) != 0 || fmask == 0)
     return fail(RF_ERR_ARGUMENT, "formulation_mask%s %lld invalid", "", fmask);
+  if (batch == 0) return RF_OK;
   if ((fmask & RF_IMPLICIT_STANDARD) && (!out_std || !out_std->normal || !out_std->offset ||
                                          !out_std->residual || !out_std->curvature || !out_std->status))
     return fail(RF_ERR_ARGUMENT, "implicit-standard requested without output buffers%s");
   if ((fmask & RF_IMPLICIT_RGBD) && (!out_rgbd || !out_rgbd->normal || !out_rgbd->offset ||
                                      !out_rgbd->residual || !out_rgbd->curvature || !out_rgbd->status))
     return fail(RF_ERR_ARGUMENT, "implicit-rgbd requested without output buffers%s");
-  if (batch == 0) return RF_OK;
   const int r = window / 2;
   const dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, (unsigned)batch);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -1,0 +1,157 @@
+"""Generate the golden per-pixel fixtures from the REFERENCE itself.
+
+Run in the build container (the reference is importable there, read-only):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+For every pixel of each small case this calls the reference's own per-window
+pipeline on the clipped centred window:
+
+    gather_window_samples + accumulate_scatter_naive   (fitting.py:339-402)
+    FIT_BY_FORMULATION[formulation](scatter)            (fitting.py:546-579)
+
+i.e. exactly ``fit_rect(depth, maps, rect, formulation, "naive")``
+(fitting.py:757-786), and records the canonical coefficients, eigenvalue,
+rms residual, degenerate flag and sample count.  Curvature is the A17
+extension computed from the reference's own Scatter4 with numpy eigvalsh.
+Inputs are rendered with the reference's renderer (synth.render_scene) and
+stored as float32 (or uint16 mm) so the GPU later reads the same bits.
+The reference is never needed at test time: the .npz files are committed.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+
+try:
+    import rangefit as rf
+except ImportError:  # pragma: no cover
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import rangefit as rf
+
+from rangefit.fitting import FIT_BY_FORMULATION, accumulate_scatter_naive, gather_window_samples
+
+FORMS = ("implicit-rgbd", "implicit-standard")
+
+
+def curvature(matrix: np.ndarray, formulation: str) -> float:
+    if formulation == "implicit-standard":
+        I, k = [0, 1, 2], 3
+    else:
+        I, k = [0, 1, 3], 2
+    S = matrix
+    C3 = S[np.ix_(I, I)] - np.outer(S[I, k], S[I, k]) / S[k, k]
+    ev = np.linalg.eigvalsh(C3)
+    tr = float(np.trace(C3))
+    return float(ev.min() / tr) if tr > 0 else 0.0
+
+
+def run_case(name, cam, depth_img: "rf.DepthImage", stored, window, dtype):
+    maps = rf.compute_tan_maps(cam)
+    H, W = cam.height, cam.width
+    r = window // 2
+    out = {"depth": stored, "fx": cam.fx, "fy": cam.fy, "cx": cam.cx, "cy": cam.cy,
+           "window": window, "dtype": dtype}
+    if depth_img.valid is not None:
+        out["valid"] = depth_img.valid.astype(np.uint8)
+    for form in FORMS:
+        coef = np.full((H * W, 4), np.nan)
+        lam = np.full(H * W, np.nan)
+        rms = np.full(H * W, np.nan)
+        curv = np.full(H * W, np.nan)
+        npts = np.zeros(H * W, np.int32)
+        status = np.zeros(H * W, np.uint8)
+        fro = np.full(H * W, np.nan)
+        for y in range(H):
+            for x in range(W):
+                i = y * W + x
+                if not depth_img.valid[y, x]:
+                    continue
+                status[i] = 1
+                rect = rf.Rect(max(x - r, 0), max(y - r, 0), min(x + r + 1, W), min(y + r + 1, H))
+                samples = gather_window_samples(depth_img, maps, rect, form)
+                try:
+                    scatter = accumulate_scatter_naive(samples, form)
+                except rf.InsufficientSamplesError:
+                    continue
+                res = FIT_BY_FORMULATION[form](scatter)
+                status[i] |= 2 | (4 if res.degenerate else 0)
+                coef[i] = res.plane.coefficients
+                lam[i] = res.eigenvalue
+                rms[i] = res.rms_residual
+                npts[i] = res.n_points
+                curv[i] = curvature(scatter.matrix, form)
+                fro[i] = float(np.linalg.norm(scatter.matrix)) / res.n_points
+        key = "rgbd" if form == "implicit-rgbd" else "std"
+        out.update({f"{key}_coef": coef, f"{key}_lam": lam, f"{key}_rms": rms, f"{key}_curv": curv,
+                    f"{key}_n": npts, f"{key}_status": status, f"{key}_scale": fro})
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, "fits:", {k: int((out[f"{k}_status"] & 2).sum()) for k in ("rgbd", "std")})
+
+
+def random_plane(rng, zlo, zhi):
+    while True:
+        n = rng.standard_normal(3)
+        n /= np.linalg.norm(n)
+        if n[2] > 0:
+            n = -n
+        if -n[2] > 0.45:
+            break
+    z0 = rng.uniform(zlo, zhi)
+    return rf.GroundTruthPlane(np.array([*n, -n[2] * z0]))
+
+
+def main():
+    # 1. noisy three-plane scene, 10% dropout, float32 metres (small_camera of the reference tests)
+    cam = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=31.5, cy=23.5, width=64, height=48)
+    maps = rf.compute_tan_maps(cam)
+    rng = np.random.default_rng(11)
+    scene = rf.SyntheticScene(tuple(random_plane(rng, 1.0, 4.0) for _ in range(3)))
+    d, _ = rf.render_scene(scene, maps, noise=rf.NoiseModel(), seed=3, dropout=0.1)
+    z32 = np.where(d.valid, d.values, 0.0).astype(np.float32)
+    for w in (3, 5):
+        run_case(f"planes_f32_w{w}", cam, rf.DepthImage(values=z32.astype(np.float64)), z32, w, "f32")
+
+    # 1b. explicit validity mask: DepthImage(values, valid=mask) (synth.py:88-94)
+    mask = np.random.default_rng(5).random(z32.shape) > 0.2
+    dm = rf.DepthImage(values=z32.astype(np.float64), valid=mask)
+    run_case("planes_f32_mask_w5", cam, dm, z32, 5, "f32")
+
+    # 2. uint16 millimetres through DepthImage.from_millimeters
+    cam2 = rf.CameraIntrinsics(fx=40.0, fy=42.0, cx=15.5, cy=11.5, width=32, height=24)
+    maps2 = rf.compute_tan_maps(cam2)
+    scene2 = rf.SyntheticScene((random_plane(rng, 0.6, 3.0), random_plane(rng, 0.6, 3.0)))
+    d2, _ = rf.render_scene(scene2, maps2, noise=rf.NoiseModel(), seed=4, dropout=0.05)
+    mm = d2.to_millimeters()
+    run_case("planes_u16_w5", cam2, rf.DepthImage.from_millimeters(mm), mm, 5, "u16")
+
+    # 3. noiseless frontal plane Z = 3 (tests/test_fitting.py:266-281 golden (0,0,1,-3)/sqrt(10))
+    cam3 = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=7.5, cy=5.5, width=16, height=12)
+    maps3 = rf.compute_tan_maps(cam3)
+    d3, _ = rf.render_scene(rf.SyntheticScene((rf.GroundTruthPlane(np.array([0.0, 0.0, 1.0, -3.0])),)), maps3)
+    z3 = d3.values.astype(np.float32)
+    run_case("frontal_z3_w5", cam3, rf.DepthImage(values=z3.astype(np.float64)), z3, 5, "f32")
+
+    # 4. left half invalid (mask_rect), window 3: status bits at the hole boundary
+    masked = rf.GroundTruthPlane(np.array([0.1, -0.2, 1.0, -2.0]), mask_rect=(10, 0, 24, 12))
+    d4, _ = rf.render_scene(rf.SyntheticScene((masked,)), maps3, noise=rf.NoiseModel(), seed=9)
+    z4 = np.where(d4.valid, d4.values, 0.0).astype(np.float32)
+    run_case("half_invalid_w3", cam3, rf.DepthImage(values=z4.astype(np.float64)), z4, 3, "f32")
+
+    # 5. high-resolution intrinsics, near and far depth (C5-like f=2900 crop), window 7
+    cam5 = rf.CameraIntrinsics(fx=2900.0, fy=2900.0, cx=20.5, cy=15.5, width=40, height=32)
+    maps5 = rf.compute_tan_maps(cam5)
+    scene5 = rf.SyntheticScene((rf.GroundTruthPlane(np.array([0.05, 0.02, -1.0, 0.31]), mask_rect=(0, 0, 20, 32)),
+                                rf.GroundTruthPlane(np.array([-0.1, 0.3, -1.0, 18.0]), mask_rect=(20, 0, 40, 32))))
+    d5, _ = rf.render_scene(scene5, maps5, noise=rf.NoiseModel(), seed=12, dropout=0.05)
+    z5 = np.where(d5.valid, d5.values, 0.0).astype(np.float32)
+    run_case("near_far_w7", cam5, rf.DepthImage(values=z5.astype(np.float64)), z5, 7, "f32")
+
+
+if __name__ == "__main__":
+    main()

@@ -45,3 +45,44 @@ def check_frame(depth_gpu, fits, cam, window, formulation, frame=0, pixels=None,
                        mask=None if mask is None else (mask[frame] if mask.dim() == 3 else mask))
     got = gpu_flat(fits, frame, pixels)
     return compare(got, ref), got, ref
+
+
+# ------------------------------------------------------------ golden fixtures
+GOLDEN_DIR = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+GOLDEN_CASES = ("planes_f32_w3", "planes_f32_w5", "planes_f32_mask_w5", "planes_u16_w5",
+                "frontal_z3_w5", "half_invalid_w3", "near_far_w7")
+
+
+class Cam:
+    def __init__(self, fx, fy, cx, cy, width, height):
+        self.fx, self.fy, self.cx, self.cy, self.width, self.height = fx, fy, cx, cy, width, height
+
+
+def load_golden(name: str) -> dict:
+    """Golden case written by tests/golden/make_golden.py (reference outputs, per pixel)."""
+    z = np.load(GOLDEN_DIR / f"{name}.npz")
+    depth = z["depth"]
+    H, W = depth.shape
+    cam = Cam(float(z["fx"]), float(z["fy"]), float(z["cx"]), float(z["cy"]), W, H)
+    g = {"depth": depth, "cam": cam, "window": int(z["window"]), "dtype": str(z["dtype"]),
+         "valid": z["valid"].astype(bool) if "valid" in z.files else None}
+    for key, form in (("rgbd", "implicit-rgbd"), ("std", "implicit-standard")):
+        coef = z[f"{key}_coef"]
+        nrm = np.linalg.norm(coef[:, :3], axis=1)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            normal = coef[:, :3] / nrm[:, None]
+            offset = coef[:, 3] / nrm
+        g[form] = {"normal": normal, "offset": offset, "residual": z[f"{key}_rms"],
+                   "curvature": z[f"{key}_curv"], "status": z[f"{key}_status"],
+                   "scale": z[f"{key}_scale"], "coef": coef, "lam": z[f"{key}_lam"],
+                   "n": z[f"{key}_n"]}
+    return g
+
+
+def golden_mask(g: dict):
+    """Explicit validity mask of a golden case (None when derived from the depth values)."""
+    d = g["depth"]
+    derived = (d > 0) if d.dtype == np.uint16 else (np.isfinite(d) & (d > 0))
+    if g["valid"] is None or np.array_equal(g["valid"], derived):
+        return None
+    return g["valid"]

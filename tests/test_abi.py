@@ -1,0 +1,85 @@
+"""The C-ABI library: loads without a GPU, exports every symbol that
+include/rangefit_b200.h declares, and validates arguments (reference
+ValueError conventions) before touching the device.  No compute calls."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2103_06644_b200 import _native as N
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "rangefit_b200.h"
+
+
+def header_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:rf_status|int32_t|const char\*)\s+(rf_\w+)\(", text, re.M)))
+
+
+def test_header_and_binding_agree():
+    assert header_functions() == sorted(N.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_symbol():
+    lib = N.load()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    assert lib.rf_abi_version() == 1
+
+
+def test_launch_count():
+    lib = N.load()
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD) == 1
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_RGBD) == 1
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_IMPLICIT_RGBD) == 2
+
+
+@pytest.mark.parametrize("fx,fy,cx,cy,w,h,msg", [
+    (0.0, 1.0, 0.5, 0.5, 4, 4, "focal"),           # camera.py:55-56
+    (1.0, -1.0, 0.5, 0.5, 4, 4, "focal"),
+    (1.0, 1.0, 0.5, 0.5, 0, 4, "size"),            # camera.py:57-58
+    (1.0, 1.0, 4.0, 0.5, 4, 4, "principal"),       # camera.py:59-63
+    (1.0, 1.0, 0.5, -0.1, 4, 4, "principal"),
+])
+def test_tables_create_validation(fx, fy, cx, cy, w, h, msg):
+    lib = N.load()
+    intr = N.RfIntrinsics(fx, fy, cx, cy, w, h)
+    out = ctypes.c_void_p()
+    st = lib.rf_tables_create(ctypes.byref(intr), None, None, 0, ctypes.byref(out))
+    assert st == N.RF_ERR_ARGUMENT
+    assert msg in N.last_error()
+    assert not out
+
+
+def test_tables_create_rejects_nonseparable_distortion():
+    lib = N.load()
+    intr = N.RfIntrinsics(10.0, 10.0, 1.5, 1.5, 4, 4)
+    dx = np.zeros(16)
+    dx[5] = 0.25
+    out = ctypes.c_void_p()
+    st = lib.rf_tables_create(ctypes.byref(intr), dx.ctypes.data, None, 0, ctypes.byref(out))
+    assert st == N.RF_ERR_UNSUPPORTED
+    with pytest.raises(NotImplementedError):
+        N.check(st, "compute_tan_maps")
+
+
+def test_fit_pixels_null_arguments():
+    lib = N.load()
+    st = lib.rf_fit_pixels(None, None, 0, 1, 4, 4, 4, None, 5, 3, None, None, None)
+    assert st == N.RF_ERR_ARGUMENT
+    with pytest.raises(ValueError):
+        N.check(st, "fit_pixels")
+
+
+def test_check_maps_status_to_exceptions():
+    N.check(N.RF_OK, "x")
+    with pytest.raises(ValueError):
+        N.check(N.RF_ERR_SHAPE, "x")
+    with pytest.raises(RuntimeError):
+        N.check(N.RF_ERR_CUDA, "x")
