@@ -8,11 +8,12 @@ fallback: if the library is missing every entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 PKG_DIR = Path(__file__).resolve().parent
 LIB_NAME = "librangefit_b200.so"
-LIB_PATH = PKG_DIR / LIB_NAME
+LIB_PATH = Path(os.environ["RF_LIB_PATH"]) if os.environ.get("RF_LIB_PATH") else PKG_DIR / LIB_NAME
 
 RF_OK = 0
 RF_ERR_ARGUMENT = 1

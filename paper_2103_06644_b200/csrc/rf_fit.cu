@@ -17,10 +17,13 @@
 //   4. solve  : smallest eigenpair of the uncentred 4x4 scatter through its
 //               Schur complement on the constant monomial (solve_window),
 //               curvature, canonical sign, outputs (fp32) and status byte.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/rangefit_b200.h"
@@ -32,6 +35,12 @@ constexpr int TH = 16;       // output tile height (pixels)
 constexpr int KSEG = 4;      // consecutive output pixels per thread
 constexpr int NTHREADS = (TW / KSEG) * TH;  // 256
 constexpr int MAX_RADIUS = 32;
+#ifndef RF_STAGE_OUTPUTS
+#define RF_STAGE_OUTPUTS 1
+#endif
+#ifndef RF_MIN_BLOCKS
+#define RF_MIN_BLOCKS 2
+#endif
 
 constexpr int VAR_STD = 0;   // implicit-standard
 constexpr int VAR_DF = 1;    // implicit-rgbd (disparity form)
@@ -45,6 +54,7 @@ struct KParams {
   int64_t row_pitch;
   int64_t frame_stride;
   int64_t out_frame;    // H*W
+  int64_t batch;
   int H, W, r, dtype;
   float* normal;
   float* offset;
@@ -345,275 +355,413 @@ __device__ __forceinline__ void finish_plane(double a, double b, double c, doubl
   off = fd * in3;
 }
 
-// depth -> (valid, Z in fp64) exactly as DepthImage does
-__device__ __forceinline__ double load_z(const KParams& P, int64_t frame, int y, int x,
-                                         bool& valid) {
-  const int64_t off = frame * P.frame_stride + (int64_t)y * P.row_pitch + x;
-  double z;
-  if (P.dtype == RF_DEPTH_U16_MM) {
-    const unsigned short mm = __ldg(reinterpret_cast<const unsigned short*>(P.depth) + off);
-    valid = mm > 0;
-    z = __ddiv_rn((double)mm, 1000.0);
-  } else {
-    const float zf = __ldg(reinterpret_cast<const float*>(P.depth) + off);
-    valid = (zf > 0.0f) && (zf <= 3.402823466e38f);  // isfinite & > 0
-    z = (double)zf;
-  }
-  if (P.mask) valid = valid && (__ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0);
-  return z;
+// ---- TMA / mbarrier helpers (sm_90+ async proxy; SASS UTMALDG + SYNCS)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// one TMA box (HWP x HH x 1 elements) of the [B, H, W] depth tensor; coordinates past
+// the right/bottom edge are zero-filled (= invalid depth).  Measured on this
+// sm_100a/driver: a negative box origin, or an x origin that is not 16-byte
+// aligned, raises an illegal-instruction fault -- so the caller aligns the box
+// origin down to 16 bytes, clamps it to >= 0, and masks the left/top halo itself.
+__device__ __forceinline__ int box_x(int x, int al) { return x > 0 ? (x / al) * al : 0; }
+__device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* tmap, int x, int y, int z,
+                                              uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
 }
 
+struct TileGeom {
+  int64_t frame;
+  int x0, y0;
+};
+
+__device__ __forceinline__ TileGeom tile_of(int64_t t, int ntx, int nty) {
+  TileGeom g;
+  const int64_t per_frame = (int64_t)ntx * nty;
+  g.frame = t / per_frame;
+  const int rem = (int)(t - g.frame * per_frame);
+  const int ty = rem / ntx;
+  g.y0 = ty * TH;
+  g.x0 = (rem - ty * ntx) * TW;
+  return g;
+}
+
+// depth element -> fp64 primary p (0 = invalid): DepthImage validity (synth.py:84, 111-114)
 template <int VAR>
-__global__ void __launch_bounds__(NTHREADS, 2) fit_tile_kernel(const KParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ double primary_from_f32(float zf, bool mask_ok) {
+  const bool valid = mask_ok && (zf > 0.0f) && (zf <= 3.402823466e38f);  // isfinite & > 0
+  const double z = (double)zf;
+  return valid ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
+}
+template <int VAR>
+__device__ __forceinline__ double primary_from_u16(unsigned short mm, bool mask_ok) {
+  if (!(mask_ok && mm > 0)) return 0.0;
+  const double z = __ddiv_rn((double)mm, 1000.0);  // mm / 1000.0 exactly as the reference
+  return VAR == VAR_DF ? rcp_fast(z) : z;
+}
+
+// One persistent CTA walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
+// With USE_TMA the raw halo tile of the NEXT tile is fetched by TMA into the
+// other of two shared buffers while this tile's column and row passes run.
+template <int VAR, bool USE_TMA>
+__global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
+    fit_tile_kernel(const KParams P, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smem_dyn[];
+  // TMA destinations must be 128-byte aligned: align the dynamic base explicitly
+  unsigned char* smem_raw = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_dyn) + 127) & ~uintptr_t(127));
   const int r = P.r;
   const int HW_ = TW + 2 * r;  // halo width
   const int HH_ = TH + 2 * r;  // halo height
   constexpr int NVD = VAR == VAR_DF ? 3 : 5;  // fp64 vertical channels
   constexpr int NVI = VAR == VAR_DF ? 3 : 1;  // int vertical channels
-  double* prim = reinterpret_cast<double*>(smem_raw);             // [HH_][HW_]
-  double* vd = prim + HH_ * HW_;                                  // [NVD][TH][HW_]
-  int* vi = reinterpret_cast<int*>(vd + NVD * TH * HW_);          // [NVI][TH][HW_]
+  const int esz = P.dtype == RF_DEPTH_U16_MM ? 2 : 4;
+  const int al = 16 / esz;  // TMA box x origin must be 16-byte aligned
+  const int HWP = (HW_ + al - 1 + 7) & ~7;  // TMA box width (covers the alignment shift)
+  const int raw_bytes = USE_TMA ? ((HH_ * HWP * esz + 127) & ~127) : 0;
+  unsigned char* raw0 = smem_raw;
+  unsigned char* raw1 = smem_raw + raw_bytes;
+  double* prim = reinterpret_cast<double*>(smem_raw + 2 * raw_bytes);  // [HH_][HW_]
+  double* vd = prim + HH_ * HW_;                                         // [NVD][TH][HW_]
+  int* vi = reinterpret_cast<int*>(vd + NVD * TH * HW_);                 // [NVI][TH][HW_]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(vi + NVI * TH * HW_) + 7) & ~uintptr_t(7));
 
   const int tid = threadIdx.x;
-  const int64_t frame = blockIdx.z;
-  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+  const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;
+  const int64_t total = (int64_t)ntx * nty * P.batch;
+  const uint32_t box_bytes = (uint32_t)(HH_ * HWP * esz);
 
-  // ---- 1. load halo tile -> primary
-  {
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int row = warp; row < HH_; row += NTHREADS / 32) {
-      const int y = y0 - r + row;
-      const bool yin = y >= 0 && y < P.H;
-      for (int col = lane; col < HW_; col += 32) {
-        const int x = x0 - r + col;
-        double p = 0.0;
-        if (yin && x >= 0 && x < P.W) {
-          bool valid;
-          const double z = load_z(P, frame, y, x, valid);
-          if (valid) p = VAR == VAR_DF ? rcp_fast(z) : z;
-        }
-        prim[row * HW_ + col] = p;
-      }
+  if (USE_TMA) {
+    if (tid == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0 && blockIdx.x < total) {
+      const TileGeom g = tile_of(blockIdx.x, ntx, nty);
+      mbar_expect_tx(&bars[0], box_bytes);
+      tma_load_tile(raw0, &tmap, box_x(g.x0 - r, al), max(g.y0 - r, 0), (int)g.frame, &bars[0]);
     }
   }
-  __syncthreads();
 
-  // ---- 2. vertical running sums.  Each halo column is split into `parts`
-  // row segments so that every thread of the CTA has a column segment; each
-  // segment warms up on its 2r leading rows, then slides down.
-  {
-    const int parts = max(1, min(NTHREADS / HW_, TH));
-    const int col = tid % HW_;
-    const int part = tid / HW_;
-    if (part < parts) {
-      const int o0 = (part * TH) / parts, o1 = ((part + 1) * TH) / parts;  // output rows [o0, o1)
-      double a[NVD];
-      int b[NVI];
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    const TileGeom g = tile_of(t, ntx, nty);
+    const int64_t frame = g.frame;
+    const int x0 = g.x0, y0 = g.y0;
+
+    // ---- 1. halo tile -> primary
+    if (USE_TMA) {
+      const int b = it & 1;
+      mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
+      const unsigned char* raw = b ? raw1 : raw0;
+      const int bx = box_x(x0 - r, al), by = max(y0 - r, 0);
+      const int sx = (x0 - r) - bx, sy = (y0 - r) - by;  // raw index = tile index + shift
+      for (int row = tid >> 5; row < HH_; row += NTHREADS / 32) {
+        const int y = y0 - r + row;
+        for (int col = tid & 31; col < HW_; col += 32) {
+          double p = 0.0;
+          if (row + sy >= 0 && col + sx >= 0) {
+            bool mask_ok = true;
+            if (P.mask) {
+              const int x = x0 - r + col;
+              mask_ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
+            }
+            const int ri = (row + sy) * HWP + (col + sx);
+            p = esz == 2 ? primary_from_u16<VAR>(reinterpret_cast<const unsigned short*>(raw)[ri], mask_ok)
+                         : primary_from_f32<VAR>(reinterpret_cast<const float*>(raw)[ri], mask_ok);
+          }
+          prim[row * HW_ + col] = p;
+        }
+      }
+      __syncthreads();
+      // the other buffer was consumed in the previous iteration: prefetch the next tile into it
+      if (tid == 0 && t + gridDim.x < total) {
+        const TileGeom gn = tile_of(t + gridDim.x, ntx, nty);
+        unsigned char* dst = b ? raw0 : raw1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bars[b ^ 1], box_bytes);
+        tma_load_tile(dst, &tmap, box_x(gn.x0 - r, al), max(gn.y0 - r, 0), (int)gn.frame, &bars[b ^ 1]);
+      }
+    } else {
+      for (int row = tid >> 5; row < HH_; row += NTHREADS / 32) {
+        const int y = y0 - r + row;
+        const bool yin = y >= 0 && y < P.H;
+        for (int col = tid & 31; col < HW_; col += 32) {
+          const int x = x0 - r + col;
+          double p = 0.0;
+          if (yin && x >= 0 && x < P.W) {
+            const int64_t off = frame * P.frame_stride + (int64_t)y * P.row_pitch + x;
+            const bool mask_ok =
+                !P.mask || __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
+            p = esz == 2 ? primary_from_u16<VAR>(__ldg(reinterpret_cast<const unsigned short*>(P.depth) + off), mask_ok)
+                         : primary_from_f32<VAR>(__ldg(reinterpret_cast<const float*>(P.depth) + off), mask_ok);
+          }
+          prim[row * HW_ + col] = p;
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- 2. vertical running sums.  Each halo column is split into `parts`
+    // row segments so that every thread of the CTA has a column segment; each
+    // segment warms up on its 2r leading rows, then slides down.
+    {
+      const int parts = max(1, min(NTHREADS / HW_, TH));
+      const int col = tid % HW_;
+      const int part = tid / HW_;
+      if (part < parts) {
+        const int o0 = (part * TH) / parts, o1 = ((part + 1) * TH) / parts;  // output rows [o0, o1)
+        double a[NVD];
+        int bb[NVI];
 #pragma unroll
-      for (int k = 0; k < NVD; ++k) a[k] = 0.0;
+        for (int k = 0; k < NVD; ++k) a[k] = 0.0;
 #pragma unroll
-      for (int k = 0; k < NVI; ++k) b[k] = 0;
-      auto add = [&](int ii, double sg) {
-        const double p = prim[ii * HW_ + col];
-        const int dy = ii - r;
-        const double fdy = __int2double_rn(dy) * sg;
-        const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
+        for (int k = 0; k < NVI; ++k) bb[k] = 0;
+        // dy of input row ii is ii - r (origin: the tile's first output row)
+        auto add = [&](int ii, double fdy, int dy, double sg) {
+          const double p = prim[ii * HW_ + col];
+          const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
+          if (VAR == VAR_DF) {
+            a[0] = fma(sg, p, a[0]);
+            a[1] = fma(sg * p, p, a[1]);
+            a[2] = fma(sg * fdy, p, a[2]);
+            bb[0] += v;
+            bb[1] += v * dy;
+            bb[2] += v * dy * dy;
+          } else {
+            const double p2 = p * p;
+            const double sfdy = sg * fdy;
+            a[0] = fma(sg, p, a[0]);
+            a[1] = fma(sg, p2, a[1]);
+            a[2] = fma(sfdy, p, a[2]);
+            a[3] = fma(sfdy, p2, a[3]);
+            a[4] = fma(sfdy * fdy, p2, a[4]);
+            bb[0] += v;
+          }
+        };
+        // window of output row o covers input rows [o, o + 2r]
+        double fdy = (double)(o0 - r);
+        for (int ii = o0; ii < o0 + 2 * r; ++ii, fdy += 1.0) add(ii, fdy, ii - r, 1.0);
+        double fdy_lo = (double)(o0 - r);
+        for (int o = o0; o < o1; ++o, fdy += 1.0, fdy_lo += 1.0) {
+          add(o + 2 * r, fdy, o + r, 1.0);
+#pragma unroll
+          for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * HW_ + col] = a[k];
+#pragma unroll
+          for (int k = 0; k < NVI; ++k) vi[(k * TH + o) * HW_ + col] = bb[k];
+          add(o, fdy_lo, o - r, -1.0);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- 3/4. horizontal running sums + per-window solve
+    {
+      const int orow = tid / (TW / KSEG);
+      const int xs = (tid % (TW / KSEG)) * KSEG;  // tile-local x of the segment's first pixel
+      const int gy = y0 + orow;
+      const int gxs = x0 + xs;
+      if (gy < P.H && gxs < P.W) {
+      const double txo = __ldg(P.tan_x + gxs);
+      const double tyo = __ldg(P.tan_y + y0);
+      const double ifx = P.ifx, ify = P.ify;
+      const double* vrow = vd + orow * HW_;
+      const int* irow = vi + orow * HW_;
+      const int vstride = TH * HW_;
+
+      // running horizontal sums (origin: segment start xs, tile row y0)
+      double h[VAR == VAR_DF ? 4 : 9];
+      long long hi[VAR == VAR_DF ? 6 : 1];
+    #pragma unroll
+      for (int k = 0; k < (VAR == VAR_DF ? 4 : 9); ++k) h[k] = 0.0;
+    #pragma unroll
+      for (int k = 0; k < (VAR == VAR_DF ? 6 : 1); ++k) hi[k] = 0;
+
+      auto accum = [&](int c, double sgn) {
+        const int dx = c - r - xs;
+        const double fdx = __int2double_rn(dx) * sgn;
         if (VAR == VAR_DF) {
-          a[0] = fma(sg, p, a[0]);
-          a[1] = fma(sg * p, p, a[1]);
-          a[2] = fma(fdy, p, a[2]);
-          b[0] += v;
-          b[1] += v * dy;
-          b[2] += v * dy * dy;
+          const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
+          const int m = irow[c], my = irow[vstride + c], myy = irow[2 * vstride + c];
+          h[0] = fma(sgn, w, h[0]);    // sum w
+          h[1] = fma(sgn, ww, h[1]);   // sum w^2
+          h[2] = fma(sgn, yw, h[2]);   // sum dy w
+          h[3] = fma(fdx, w, h[3]);    // sum dx w
+          const long long s = sgn > 0 ? 1 : -1;
+          hi[0] += s * m;              // n
+          hi[1] += s * dx * m;         // sum dx
+          hi[2] += s * my;             // sum dy
+          hi[3] += s * dx * dx * m;    // sum dx^2
+          hi[4] += s * dx * my;        // sum dx dy
+          hi[5] += s * myy;            // sum dy^2
         } else {
-          const double p2 = p * p;
-          a[0] = fma(sg, p, a[0]);
-          a[1] = fma(sg, p2, a[1]);
-          a[2] = fma(fdy, p, a[2]);
-          a[3] = fma(fdy, p2, a[3]);
-          a[4] = fma(fdy * __int2double_rn(dy), p2, a[4]);
-          b[0] += v;
+          const double z = vrow[c], z2 = vrow[vstride + c], yz = vrow[2 * vstride + c],
+                       yz2 = vrow[3 * vstride + c], y2z2 = vrow[4 * vstride + c];
+          const double fdx2 = fdx * (double)dx;
+          h[0] = fma(sgn, z, h[0]);     // S3  = sum Z
+          h[1] = fma(sgn, z2, h[1]);    // S33 = sum Z^2
+          h[2] = fma(sgn, yz, h[2]);    // S2  = sum dy Z
+          h[3] = fma(sgn, yz2, h[3]);   // S23 = sum dy Z^2
+          h[4] = fma(sgn, y2z2, h[4]);  // S22 = sum dy^2 Z^2
+          h[5] = fma(fdx, z, h[5]);     // S1  = sum dx Z
+          h[6] = fma(fdx, z2, h[6]);    // S13 = sum dx Z^2
+          h[7] = fma(fdx, yz2, h[7]);   // S12 = sum dx dy Z^2
+          h[8] = fma(fdx2, z2, h[8]);   // S11 = sum dx^2 Z^2
+          hi[0] += (sgn > 0 ? 1 : -1) * irow[c];
         }
       };
-      // window of output row o covers input rows [o, o + 2r]
-      for (int ii = o0; ii < o0 + 2 * r; ++ii) add(ii, 1.0);
-      for (int o = o0; o < o1; ++o) {
-        add(o + 2 * r, 1.0);
-#pragma unroll
-        for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * HW_ + col] = a[k];
-#pragma unroll
-        for (int k = 0; k < NVI; ++k) vi[(k * TH + o) * HW_ + col] = b[k];
-        add(o, -1.0);
+
+      for (int c = xs; c <= xs + 2 * r; ++c) accum(c, 1.0);
+
+    #if RF_STAGE_OUTPUTS
+      float o_n[KSEG][3], o_off[KSEG], o_res[KSEG], o_cur[KSEG];
+      uint8_t o_st[KSEG];
+    #endif
+
+    #pragma unroll
+      for (int j = 0; j < KSEG; ++j) {
+        if (j > 0) {
+          accum(xs + j + 2 * r, 1.0);
+          accum(xs + j - 1, -1.0);
+        }
+        const int gx = gxs + j;
+        const double pc = prim[(orow + r) * HW_ + xs + j + r];
+        uint8_t st = pc > 0.0 ? RF_PIX_INPUT_VALID : 0;
+        const int nwin = (int)hi[0];
+        float nx = __int_as_float(0x7fc00000), ny = nx, nz = nx, off = nx, res = nx, cur = nx;
+        if (st && nwin >= 4 && gx < P.W) {
+          const double nd = (double)nwin;
+          const double invn = rcp_fast(nd);
+          Sym3 C;
+          double mu0, mu1, mu2;
+          if (VAR == VAR_DF) {
+            const long long n = hi[0], sx = hi[1], sy = hi[2], sxx = hi[3], sxy = hi[4], syy = hi[5];
+            const double cq00 = (double)(n * sxx - sx * sx) * invn;
+            const double cq01 = (double)(n * sxy - sx * sy) * invn;
+            const double cq11 = (double)(n * syy - sy * sy) * invn;
+            const double mw = h[0] * invn;
+            const double fsx = (double)sx, fsy = (double)sy;
+            const double cq02 = fma(-fsx, mw, h[3]);
+            const double cq12 = fma(-fsy, mw, h[2]);
+            const double cq22 = fma(-h[0], mw, h[1]);
+            C.c00 = cq00 * (ifx * ifx);
+            C.c01 = cq01 * (ifx * ify);
+            C.c11 = cq11 * (ify * ify);
+            C.c02 = cq02 * ifx;
+            C.c12 = cq12 * ify;
+            C.c22 = cq22;
+            mu0 = fma(fsx * invn, ifx, txo);
+            mu1 = fma(fsy * invn, ify, tyo);
+            mu2 = mw;
+          } else {
+            // q = (dx Z, dy Z, Z): sums S1=h5, S2=h2, S3=h0, S11=h8, S12=h7, S22=h4,
+            // S13=h6, S23=h3, S33=h1; C_q = S_ab - S_a S_b / n
+            const double q0 = h[5] * invn, q1 = h[2] * invn, q2 = h[0] * invn;
+            const double k00 = fma(-h[5], q0, h[8]);
+            const double k01 = fma(-h[5], q1, h[7]);
+            const double k02 = fma(-h[5], q2, h[6]);
+            const double k11 = fma(-h[2], q1, h[4]);
+            const double k12 = fma(-h[2], q2, h[3]);
+            const double k22 = fma(-h[0], q2, h[1]);
+            // m = L q, L = [[ifx, 0, txo], [0, ify, tyo], [0, 0, 1]]
+            const double r00 = fma(ifx, k00, txo * k02), r01 = fma(ifx, k01, txo * k12),
+                         r02 = fma(ifx, k02, txo * k22);
+            const double r11 = fma(ify, k11, tyo * k12), r12 = fma(ify, k12, tyo * k22);
+            C.c00 = fma(ifx, r00, txo * r02);
+            C.c01 = fma(ify, r01, tyo * r02);
+            C.c02 = r02;
+            C.c11 = fma(ify, r11, tyo * r12);
+            C.c12 = r12;
+            C.c22 = k22;
+            mu0 = fma(ifx, q0, txo * q2);
+            mu1 = fma(ify, q1, tyo * q2);
+            mu2 = q2;
+          }
+          WindowFit f;
+          solve_window(C, mu0, mu1, mu2, nd, f);
+          if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
+          else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
+          res = fsqrt(fmaxf((float)(f.lam * invn), 0.0f));
+          cur = f.kappa;
+          st |= RF_PIX_FIT;
+          if (f.degenerate) st |= RF_PIX_DEGENERATE;
+        }
+    #if RF_STAGE_OUTPUTS
+        o_n[j][0] = nx;
+        o_n[j][1] = ny;
+        o_n[j][2] = nz;
+        o_off[j] = off;
+        o_res[j] = res;
+        o_cur[j] = cur;
+        o_st[j] = st;
+    #else
+        if (gx < P.W) {
+          const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
+          P.normal[3 * p + 0] = nx;
+          P.normal[3 * p + 1] = ny;
+          P.normal[3 * p + 2] = nz;
+          P.offset[p] = off;
+          P.residual[p] = res;
+          P.curvature[p] = cur;
+          P.status[p] = st;
+        }
+    #endif
       }
-    }
-  }
-  __syncthreads();
 
-  // ---- 3/4. horizontal running sums + per-window solve
-  const int orow = tid / (TW / KSEG);
-  const int xs = (tid % (TW / KSEG)) * KSEG;  // tile-local x of the segment's first pixel
-  const int gy = y0 + orow;
-  if (gy >= P.H) return;
-  const int gxs = x0 + xs;
-  if (gxs >= P.W) return;
-
-  const double txo = __ldg(P.tan_x + gxs);
-  const double tyo = __ldg(P.tan_y + y0);
-  const double ifx = P.ifx, ify = P.ify;
-  const double* vrow = vd + orow * HW_;
-  const int* irow = vi + orow * HW_;
-  const int vstride = TH * HW_;
-
-  // running horizontal sums (origin: segment start xs, tile row y0)
-  double h[VAR == VAR_DF ? 4 : 9];
-  long long hi[VAR == VAR_DF ? 6 : 1];
-#pragma unroll
-  for (int k = 0; k < (VAR == VAR_DF ? 4 : 9); ++k) h[k] = 0.0;
-#pragma unroll
-  for (int k = 0; k < (VAR == VAR_DF ? 6 : 1); ++k) hi[k] = 0;
-
-  auto accum = [&](int c, double sgn) {
-    const int dx = c - r - xs;
-    const double fdx = __int2double_rn(dx) * sgn;
-    if (VAR == VAR_DF) {
-      const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
-      const int m = irow[c], my = irow[vstride + c], myy = irow[2 * vstride + c];
-      h[0] = fma(sgn, w, h[0]);    // sum w
-      h[1] = fma(sgn, ww, h[1]);   // sum w^2
-      h[2] = fma(sgn, yw, h[2]);   // sum dy w
-      h[3] = fma(fdx, w, h[3]);    // sum dx w
-      const long long s = sgn > 0 ? 1 : -1;
-      hi[0] += s * m;              // n
-      hi[1] += s * dx * m;         // sum dx
-      hi[2] += s * my;             // sum dy
-      hi[3] += s * dx * dx * m;    // sum dx^2
-      hi[4] += s * dx * my;        // sum dx dy
-      hi[5] += s * myy;            // sum dy^2
-    } else {
-      const double z = vrow[c], z2 = vrow[vstride + c], yz = vrow[2 * vstride + c],
-                   yz2 = vrow[3 * vstride + c], y2z2 = vrow[4 * vstride + c];
-      const double fdx2 = fdx * (double)dx;
-      h[0] = fma(sgn, z, h[0]);     // S3  = sum Z
-      h[1] = fma(sgn, z2, h[1]);    // S33 = sum Z^2
-      h[2] = fma(sgn, yz, h[2]);    // S2  = sum dy Z
-      h[3] = fma(sgn, yz2, h[3]);   // S23 = sum dy Z^2
-      h[4] = fma(sgn, y2z2, h[4]);  // S22 = sum dy^2 Z^2
-      h[5] = fma(fdx, z, h[5]);     // S1  = sum dx Z
-      h[6] = fma(fdx, z2, h[6]);    // S13 = sum dx Z^2
-      h[7] = fma(fdx, yz2, h[7]);   // S12 = sum dx dy Z^2
-      h[8] = fma(fdx2, z2, h[8]);   // S11 = sum dx^2 Z^2
-      hi[0] += (sgn > 0 ? 1 : -1) * irow[c];
-    }
-  };
-
-  for (int c = xs; c <= xs + 2 * r; ++c) accum(c, 1.0);
-
-  float o_n[KSEG][3], o_off[KSEG], o_res[KSEG], o_cur[KSEG];
-  uint8_t o_st[KSEG];
-
-#pragma unroll
-  for (int j = 0; j < KSEG; ++j) {
-    if (j > 0) {
-      accum(xs + j + 2 * r, 1.0);
-      accum(xs + j - 1, -1.0);
-    }
-    const int gx = gxs + j;
-    const double pc = prim[(orow + r) * HW_ + xs + j + r];
-    uint8_t st = pc > 0.0 ? RF_PIX_INPUT_VALID : 0;
-    const int nwin = (int)hi[0];
-    float nx = __int_as_float(0x7fc00000), ny = nx, nz = nx, off = nx, res = nx, cur = nx;
-    if (st && nwin >= 4 && gx < P.W) {
-      const double nd = (double)nwin;
-      const double invn = rcp_fast(nd);
-      Sym3 C;
-      double mu0, mu1, mu2;
-      if (VAR == VAR_DF) {
-        const long long n = hi[0], sx = hi[1], sy = hi[2], sxx = hi[3], sxy = hi[4], syy = hi[5];
-        const double cq00 = (double)(n * sxx - sx * sx) * invn;
-        const double cq01 = (double)(n * sxy - sx * sy) * invn;
-        const double cq11 = (double)(n * syy - sy * sy) * invn;
-        const double mw = h[0] * invn;
-        const double fsx = (double)sx, fsy = (double)sy;
-        const double cq02 = fma(-fsx, mw, h[3]);
-        const double cq12 = fma(-fsy, mw, h[2]);
-        const double cq22 = fma(-h[0], mw, h[1]);
-        C.c00 = cq00 * (ifx * ifx);
-        C.c01 = cq01 * (ifx * ify);
-        C.c11 = cq11 * (ify * ify);
-        C.c02 = cq02 * ifx;
-        C.c12 = cq12 * ify;
-        C.c22 = cq22;
-        mu0 = fma(fsx * invn, ifx, txo);
-        mu1 = fma(fsy * invn, ify, tyo);
-        mu2 = mw;
+    #if RF_STAGE_OUTPUTS
+      // ---- stores
+      const int64_t pix0 = frame * P.out_frame + (int64_t)gy * P.W + gxs;
+      const bool vec = ((P.W & (KSEG - 1)) == 0) && (gxs + KSEG <= P.W);
+      if (vec) {
+        float4* pn = reinterpret_cast<float4*>(P.normal + 3 * pix0);
+        pn[0] = make_float4(o_n[0][0], o_n[0][1], o_n[0][2], o_n[1][0]);
+        pn[1] = make_float4(o_n[1][1], o_n[1][2], o_n[2][0], o_n[2][1]);
+        pn[2] = make_float4(o_n[2][2], o_n[3][0], o_n[3][1], o_n[3][2]);
+        *reinterpret_cast<float4*>(P.offset + pix0) = make_float4(o_off[0], o_off[1], o_off[2], o_off[3]);
+        *reinterpret_cast<float4*>(P.residual + pix0) = make_float4(o_res[0], o_res[1], o_res[2], o_res[3]);
+        *reinterpret_cast<float4*>(P.curvature + pix0) = make_float4(o_cur[0], o_cur[1], o_cur[2], o_cur[3]);
+        *reinterpret_cast<uchar4*>(P.status + pix0) = make_uchar4(o_st[0], o_st[1], o_st[2], o_st[3]);
       } else {
-        // q = (dx Z, dy Z, Z): sums S1=h5, S2=h2, S3=h0, S11=h8, S12=h7, S22=h4,
-        // S13=h6, S23=h3, S33=h1; C_q = S_ab - S_a S_b / n
-        const double q0 = h[5] * invn, q1 = h[2] * invn, q2 = h[0] * invn;
-        const double k00 = fma(-h[5], q0, h[8]);
-        const double k01 = fma(-h[5], q1, h[7]);
-        const double k02 = fma(-h[5], q2, h[6]);
-        const double k11 = fma(-h[2], q1, h[4]);
-        const double k12 = fma(-h[2], q2, h[3]);
-        const double k22 = fma(-h[0], q2, h[1]);
-        // m = L q, L = [[ifx, 0, txo], [0, ify, tyo], [0, 0, 1]]
-        const double r00 = fma(ifx, k00, txo * k02), r01 = fma(ifx, k01, txo * k12),
-                     r02 = fma(ifx, k02, txo * k22);
-        const double r11 = fma(ify, k11, tyo * k12), r12 = fma(ify, k12, tyo * k22);
-        C.c00 = fma(ifx, r00, txo * r02);
-        C.c01 = fma(ify, r01, tyo * r02);
-        C.c02 = r02;
-        C.c11 = fma(ify, r11, tyo * r12);
-        C.c12 = r12;
-        C.c22 = k22;
-        mu0 = fma(ifx, q0, txo * q2);
-        mu1 = fma(ify, q1, tyo * q2);
-        mu2 = q2;
+    #pragma unroll
+        for (int j = 0; j < KSEG; ++j) {
+          if (gxs + j >= P.W) break;
+          const int64_t p = pix0 + j;
+          P.normal[3 * p + 0] = o_n[j][0];
+          P.normal[3 * p + 1] = o_n[j][1];
+          P.normal[3 * p + 2] = o_n[j][2];
+          P.offset[p] = o_off[j];
+          P.residual[p] = o_res[j];
+          P.curvature[p] = o_cur[j];
+          P.status[p] = o_st[j];
+        }
       }
-      WindowFit f;
-      solve_window(C, mu0, mu1, mu2, nd, f);
-      if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
-      else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
-      res = fsqrt(fmaxf((float)(f.lam * invn), 0.0f));
-      cur = f.kappa;
-      st |= RF_PIX_FIT;
-      if (f.degenerate) st |= RF_PIX_DEGENERATE;
+    #endif
+      }
     }
-    o_n[j][0] = nx;
-    o_n[j][1] = ny;
-    o_n[j][2] = nz;
-    o_off[j] = off;
-    o_res[j] = res;
-    o_cur[j] = cur;
-    o_st[j] = st;
-  }
-
-  // ---- stores
-  const int64_t pix0 = frame * P.out_frame + (int64_t)gy * P.W + gxs;
-  const bool vec = ((P.W & (KSEG - 1)) == 0) && (gxs + KSEG <= P.W);
-  if (vec) {
-    float4* pn = reinterpret_cast<float4*>(P.normal + 3 * pix0);
-    pn[0] = make_float4(o_n[0][0], o_n[0][1], o_n[0][2], o_n[1][0]);
-    pn[1] = make_float4(o_n[1][1], o_n[1][2], o_n[2][0], o_n[2][1]);
-    pn[2] = make_float4(o_n[2][2], o_n[3][0], o_n[3][1], o_n[3][2]);
-    *reinterpret_cast<float4*>(P.offset + pix0) = make_float4(o_off[0], o_off[1], o_off[2], o_off[3]);
-    *reinterpret_cast<float4*>(P.residual + pix0) = make_float4(o_res[0], o_res[1], o_res[2], o_res[3]);
-    *reinterpret_cast<float4*>(P.curvature + pix0) = make_float4(o_cur[0], o_cur[1], o_cur[2], o_cur[3]);
-    *reinterpret_cast<uchar4*>(P.status + pix0) = make_uchar4(o_st[0], o_st[1], o_st[2], o_st[3]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < KSEG; ++j) {
-      if (gxs + j >= P.W) break;
-      const int64_t p = pix0 + j;
-      P.normal[3 * p + 0] = o_n[j][0];
-      P.normal[3 * p + 1] = o_n[j][1];
-      P.normal[3 * p + 2] = o_n[j][2];
-      P.offset[p] = o_off[j];
-      P.residual[p] = o_res[j];
-      P.curvature[p] = o_cur[j];
-      P.status[p] = o_st[j];
-    }
+    __syncthreads();  // prim / vd are rewritten by the next tile
   }
 }
 
@@ -634,10 +782,65 @@ rf_status fail(rf_status s, const char* fmt, const char* a = "", long long b = 0
   return s;
 }
 
-size_t smem_bytes(int var, int r) {
-  const int hw = TW + 2 * r, hh = TH + 2 * r;
+size_t smem_bytes(int var, int r, bool tma, int esz) {
+  const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
   const int nvd = var == VAR_DF ? 3 : 5, nvi = var == VAR_DF ? 3 : 1;
-  return sizeof(double) * ((size_t)hh * hw + (size_t)nvd * TH * hw) + sizeof(int) * (size_t)nvi * TH * hw;
+  const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
+  return 2 * raw + sizeof(double) * ((size_t)hh * hw + (size_t)nvd * TH * hw) +
+         sizeof(int) * (size_t)nvi * TH * hw + 8 /* align */ + 2 * sizeof(uint64_t) + 128 /* base align */;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 3-D tensor map over the [batch, H, W] depth (row pitch row_pitch elements), box
+// (hwp, hh, 1), zero fill out of range.  Returns false when TMA cannot address it.
+bool make_depth_tmap(CUtensorMap* m, const void* depth, int dtype, int64_t batch, int H, int W,
+                     int64_t row_pitch, int r) {
+  const int esz = dtype == RF_DEPTH_U16_MM ? 2 : 4;
+  const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
+  if (hwp > 256 || hh > 256) return false;
+  if ((reinterpret_cast<uintptr_t>(depth) & 15) != 0) return false;
+  if (((row_pitch * esz) & 15) != 0 || ((row_pitch * H * esz) & 15) != 0) return false;
+  if (batch > 0x7fffffff) return false;
+  PFN_cuTensorMapEncodeTiled_v12000 fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)(row_pitch * esz), (cuuint64_t)(row_pitch * H * esz)};
+  const cuuint32_t box[3] = {(cuuint32_t)hwp, (cuuint32_t)hh, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult res = fn(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                          const_cast<void*>(depth), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS;
+}
+
+template <int VAR, bool TMA>
+cudaError_t launch_var(const KParams& P, const CUtensorMap& tmap, size_t sm, int64_t tiles, cudaStream_t s) {
+  auto kern = fit_tile_kernel<VAR, TMA>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, sm);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t grid = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
+  kern<<<(unsigned)grid, NTHREADS, sm, s>>>(P, tmap);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -737,8 +940,13 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
                                      !out_rgbd->residual || !out_rgbd->curvature || !out_rgbd->status))
     return fail(RF_ERR_ARGUMENT, "implicit-rgbd requested without output buffers%s");
   const int r = window / 2;
-  const dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, (unsigned)batch);
+  const int64_t tiles = (int64_t)((W + TW - 1) / TW) * ((H + TH - 1) / TH) * batch;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  const bool tma = getenv("RF_DISABLE_TMA") == nullptr &&
+                   make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
+  const int esz = dtype == RF_DEPTH_U16_MM ? 2 : 4;
   for (int var = 0; var < 2; ++var) {
     const rf_pixel_out* o = var == VAR_STD ? out_std : out_rgbd;
     if (!(fmask & (var == VAR_STD ? RF_IMPLICIT_STANDARD : RF_IMPLICIT_RGBD))) continue;
@@ -761,21 +969,13 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     P.residual = o->residual;
     P.curvature = o->curvature;
     P.status = o->status;
-    const size_t sm = smem_bytes(var, r);
+    P.batch = batch;
+    const size_t sm = smem_bytes(var, r, tma, esz);
     cudaError_t e;
-    if (var == VAR_STD) {
-      e = cudaFuncSetAttribute(fit_tile_kernel<VAR_STD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e == cudaSuccess) {
-        fit_tile_kernel<VAR_STD><<<grid, NTHREADS, sm, s>>>(P);
-        e = cudaGetLastError();
-      }
-    } else {
-      e = cudaFuncSetAttribute(fit_tile_kernel<VAR_DF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e == cudaSuccess) {
-        fit_tile_kernel<VAR_DF><<<grid, NTHREADS, sm, s>>>(P);
-        e = cudaGetLastError();
-      }
-    }
+    if (var == VAR_STD)
+      e = tma ? launch_var<VAR_STD, true>(P, tmap, sm, tiles, s) : launch_var<VAR_STD, false>(P, tmap, sm, tiles, s);
+    else
+      e = tma ? launch_var<VAR_DF, true>(P, tmap, sm, tiles, s) : launch_var<VAR_DF, false>(P, tmap, sm, tiles, s);
     if (e != cudaSuccess) return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   }
   return RF_OK;
