@@ -35,6 +35,9 @@ constexpr int TH = 16;       // output tile height (pixels)
 constexpr int KSEG = 4;      // consecutive output pixels per thread
 constexpr int NTHREADS = (TW / KSEG) * TH;  // 256
 constexpr int MAX_RADIUS = 32;
+#ifndef RF_ABLATE
+#define RF_ABLATE 0
+#endif
 #ifndef RF_STAGE_OUTPUTS
 #define RF_STAGE_OUTPUTS 1
 #endif
@@ -199,12 +202,21 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     // ~step^2/gap).  Three steps in the common case; pathological windows
     // (lam/n not small) take longer.
     double l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
-    for (int it = 0; it < 64; ++it) {
-      const double G = fma(fma(fma(l - q3, l, q2), l, -q1), l, q0);
-      const double dG = fma(fma(fma(4.0, l, -3.0 * q3), l, 2.0 * q2), l, -q1);
-      const double step = G * rcp_approx(dG);
-      l -= step;
-      if (!(fabs(step) > 1e-9 * l)) break;
+    auto newton = [&](double x) {
+      const double x2 = x * x;
+      const double G = fma(fma(x - q3, x, q2), x2, fma(-q1, x, q0));
+      const double dG = fma(fma(fma(4.0, x, -3.0 * q3), x, 2.0 * q2), x, -q1);
+      return G * rcp_approx(dG);
+    };
+    // from e0 <= 1e-4 + lam1/n and a relative gap >= 5%: e3 < 1e-14 (quadratic)
+#pragma unroll
+    for (int it = 0; it < 3; ++it) l -= newton(l);
+    if (grel > 1e-3f) {  // large residual windows (rare): iterate to convergence
+      for (int it = 0; it < 64; ++it) {
+        const double step = newton(l);
+        l -= step;
+        if (!(fabs(step) > 1e-13 * l)) break;
+      }
     }
     lam = l;
     lam2 = (double)g2;
@@ -303,25 +315,38 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     double lk;
     const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
     if (!top) {
-      // Newton from below lam_min (monotone); 1-2 steps when well separated
+      // Newton from below lam_min (monotone): two steps when well separated
       double l = (double)k1 * (1.0 - 1e-5);
-      for (int it = 0; it < 64; ++it) {
-        const double P = fma(fma(t - l, l, -c1), l, det);
-        const double dP = fma(fma(-3.0, l, 2.0 * t), l, -c1);
-        const double step = P * rcp_approx(dP);
-        l -= step;
-        if (!(fabs(step) > 1e-8 * l)) break;
+      auto newton = [&](double x) {
+        const double P = fma(fma(t - x, x, -c1), x, det);
+        const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+        return P * rcp_approx(dP);
+      };
+      l -= newton(l);
+      l -= newton(l);
+      if ((k2 - k1) < 0.05f * k2) {  // close bottom pair (rare): iterate to convergence
+        for (int it = 0; it < 64; ++it) {
+          const double step = newton(l);
+          l -= step;
+          if (!(fabs(step) > 1e-10 * l)) break;
+        }
       }
       lk = l;
     } else {
-      // near-tie at the bottom: Newton from above lam_max, then deflate
+      // near-tie at the bottom: Newton from above lam_max (well separated here),
+      // then deflate; lam_max only needs ~1e-10 for a 1e-5 curvature
       double l = fmin((double)k3 * (1.0 + 1e-5), t);
-      for (int it = 0; it < 64; ++it) {
-        const double P = fma(fma(t - l, l, -c1), l, det);
-        const double dP = fma(fma(-3.0, l, 2.0 * t), l, -c1);
-        const double step = P * rcp_approx(dP);
+      auto newton = [&](double x) {
+        const double P = fma(fma(t - x, x, -c1), x, det);
+        const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+        return P * rcp_approx(dP);
+      };
+      l -= newton(l);
+      l -= newton(l);
+      for (int it = 0; it < 62; ++it) {
+        const double step = newton(l);
         l -= step;
-        if (!(fabs(step) > 1e-14 * l)) break;
+        if (!(fabs(step) > 1e-12 * l)) break;
       }
       const double S = t - l;
       const double Pp = det * rcp_fast(l);
@@ -356,6 +381,12 @@ __device__ __forceinline__ void finish_plane(double a, double b, double c, doubl
 }
 
 // ---- TMA / mbarrier helpers (sm_90+ async proxy; SASS UTMALDG + SYNCS)
+// residue-major column stride of the column-sum buffers (VQ = 4 mod 8 spreads the banks)
+__host__ __device__ __forceinline__ int vq_of(int hw) {
+  int q = (hw + 3) / 4;
+  return q + ((4 - q % 8) + 8) % 8;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -423,14 +454,16 @@ __device__ __forceinline__ double primary_from_u16(unsigned short mm, bool mask_
 // One persistent CTA walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
 // With USE_TMA the raw halo tile of the NEXT tile is fetched by TMA into the
 // other of two shared buffers while this tile's column and row passes run.
-template <int VAR, bool USE_TMA>
+// RT > 0: compile-time window radius (all halo geometry and shared-memory offsets
+// fold to constants); RT == 0: runtime radius P.r.
+template <int VAR, bool USE_TMA, int RT>
 __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     fit_tile_kernel(const KParams P, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   // TMA destinations must be 128-byte aligned: align the dynamic base explicitly
   unsigned char* smem_raw = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_dyn) + 127) & ~uintptr_t(127));
-  const int r = P.r;
+  const int r = RT > 0 ? RT : P.r;
   const int HW_ = TW + 2 * r;  // halo width
   const int HH_ = TH + 2 * r;  // halo height
   constexpr int NVD = VAR == VAR_DF ? 3 : 5;  // fp64 vertical channels
@@ -442,10 +475,14 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   unsigned char* raw0 = smem_raw;
   unsigned char* raw1 = smem_raw + raw_bytes;
   double* prim = reinterpret_cast<double*>(smem_raw + 2 * raw_bytes);  // [HH_][HW_]
-  double* vd = prim + HH_ * HW_;                                         // [NVD][TH][HW_]
-  int* vi = reinterpret_cast<int*>(vd + NVD * TH * HW_);                 // [NVI][TH][HW_]
+  // column sums are stored residue-major: column c at (c % 4) * VQ + c / 4, so the row
+  // pass (threads 4 columns apart) reads consecutive addresses -- no bank conflicts.
+  const int VQ = vq_of(HW_);
+  const int VRS = 4 * VQ;                                                // row stride
+  double* vd = prim + HH_ * HW_;                                         // [NVD][TH][VRS]
+  int* vi = reinterpret_cast<int*>(vd + NVD * TH * VRS);                 // [NVI][TH][VRS]
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(vi + NVI * TH * HW_) + 7) & ~uintptr_t(7));
+      (reinterpret_cast<uintptr_t>(vi + NVI * TH * VRS) + 7) & ~uintptr_t(7));
 
   const int tid = threadIdx.x;
   const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;
@@ -566,12 +603,13 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         double fdy = (double)(o0 - r);
         for (int ii = o0; ii < o0 + 2 * r; ++ii, fdy += 1.0) add(ii, fdy, ii - r, 1.0);
         double fdy_lo = (double)(o0 - r);
+        const int cpos = (col & 3) * VQ + (col >> 2);
         for (int o = o0; o < o1; ++o, fdy += 1.0, fdy_lo += 1.0) {
           add(o + 2 * r, fdy, o + r, 1.0);
 #pragma unroll
-          for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * HW_ + col] = a[k];
+          for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * VRS + cpos] = a[k];
 #pragma unroll
-          for (int k = 0; k < NVI; ++k) vi[(k * TH + o) * HW_ + col] = bb[k];
+          for (int k = 0; k < NVI; ++k) vi[(k * TH + o) * VRS + cpos] = bb[k];
           add(o, fdy_lo, o - r, -1.0);
         }
       }
@@ -588,21 +626,25 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       const double txo = __ldg(P.tan_x + gxs);
       const double tyo = __ldg(P.tan_y + y0);
       const double ifx = P.ifx, ify = P.ify;
-      const double* vrow = vd + orow * HW_;
-      const int* irow = vi + orow * HW_;
-      const int vstride = TH * HW_;
+      const double* vrow = vd + orow * VRS;
+      const int* irow = vi + orow * VRS;
+      const int vstride = TH * VRS;
 
       // running horizontal sums (origin: segment start xs, tile row y0)
       double h[VAR == VAR_DF ? 4 : 9];
-      long long hi[VAR == VAR_DF ? 6 : 1];
+      int hi[VAR == VAR_DF ? 6 : 1];
     #pragma unroll
       for (int k = 0; k < (VAR == VAR_DF ? 4 : 9); ++k) h[k] = 0.0;
     #pragma unroll
       for (int k = 0; k < (VAR == VAR_DF ? 6 : 1); ++k) hi[k] = 0;
 
-      auto accum = [&](int c, double sgn) {
-        const int dx = c - r - xs;
-        const double fdx = __int2double_rn(dx) * sgn;
+      // k: column offset from the segment start xs (xs is a multiple of 4, so the
+      // residue-major position of column xs + k is a compile-time offset from vbase)
+      const int vbase = xs >> 2;
+      auto accum = [&](int k, double sgn) {
+        const int dx = k - r;
+        const int c = vbase + (k & 3) * VQ + (k >> 2);
+        const double fdx = (double)dx * sgn;
         if (VAR == VAR_DF) {
           const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
           const int m = irow[c], my = irow[vstride + c], myy = irow[2 * vstride + c];
@@ -610,13 +652,13 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
           h[1] = fma(sgn, ww, h[1]);   // sum w^2
           h[2] = fma(sgn, yw, h[2]);   // sum dy w
           h[3] = fma(fdx, w, h[3]);    // sum dx w
-          const long long s = sgn > 0 ? 1 : -1;
-          hi[0] += s * m;              // n
-          hi[1] += s * dx * m;         // sum dx
-          hi[2] += s * my;             // sum dy
-          hi[3] += s * dx * dx * m;    // sum dx^2
-          hi[4] += s * dx * my;        // sum dx dy
-          hi[5] += s * myy;            // sum dy^2
+          const int sm = sgn > 0 ? m : -m, smy = sgn > 0 ? my : -my;
+          hi[0] += sm;                 // n
+          hi[1] += dx * sm;            // sum dx
+          hi[2] += smy;                // sum dy
+          hi[3] += dx * dx * sm;       // sum dx^2
+          hi[4] += dx * smy;           // sum dx dy
+          hi[5] += sgn > 0 ? myy : -myy;  // sum dy^2
         } else {
           const double z = vrow[c], z2 = vrow[vstride + c], yz = vrow[2 * vstride + c],
                        yz2 = vrow[3 * vstride + c], y2z2 = vrow[4 * vstride + c];
@@ -630,11 +672,16 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
           h[6] = fma(fdx, z2, h[6]);    // S13 = sum dx Z^2
           h[7] = fma(fdx, yz2, h[7]);   // S12 = sum dx dy Z^2
           h[8] = fma(fdx2, z2, h[8]);   // S11 = sum dx^2 Z^2
-          hi[0] += (sgn > 0 ? 1 : -1) * irow[c];
+          hi[0] += sgn > 0 ? irow[c] : -irow[c];
         }
       };
 
-      for (int c = xs; c <= xs + 2 * r; ++c) accum(c, 1.0);
+      if constexpr (RT > 0) {
+#pragma unroll
+        for (int k = 0; k <= 2 * RT; ++k) accum(k, 1.0);
+      } else {
+        for (int k = 0; k <= 2 * r; ++k) accum(k, 1.0);
+      }
 
     #if RF_STAGE_OUTPUTS
       float o_n[KSEG][3], o_off[KSEG], o_res[KSEG], o_cur[KSEG];
@@ -644,8 +691,8 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     #pragma unroll
       for (int j = 0; j < KSEG; ++j) {
         if (j > 0) {
-          accum(xs + j + 2 * r, 1.0);
-          accum(xs + j - 1, -1.0);
+          accum(j + 2 * r, 1.0);
+          accum(j - 1, -1.0);
         }
         const int gx = gxs + j;
         const double pc = prim[(orow + r) * HW_ + xs + j + r];
@@ -701,7 +748,12 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
             mu2 = q2;
           }
           WindowFit f;
+#if RF_ABLATE == 1
+          f.lam = C.c00 + C.c11; f.u0 = mu0 + C.c01; f.u1 = mu1 + C.c02; f.u2 = mu2 + C.c12; f.s = C.c22;
+          f.kappa = 0.1f; f.degenerate = false;
+#else
           solve_window(C, mu0, mu1, mu2, nd, f);
+#endif
           if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
           else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
           res = fsqrt(fmaxf((float)(f.lam * invn), 0.0f));
@@ -786,8 +838,9 @@ size_t smem_bytes(int var, int r, bool tma, int esz) {
   const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
   const int nvd = var == VAR_DF ? 3 : 5, nvi = var == VAR_DF ? 3 : 1;
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
-  return 2 * raw + sizeof(double) * ((size_t)hh * hw + (size_t)nvd * TH * hw) +
-         sizeof(int) * (size_t)nvi * TH * hw + 8 /* align */ + 2 * sizeof(uint64_t) + 128 /* base align */;
+  const size_t vrs = 4 * (size_t)vq_of(hw);
+  return 2 * raw + sizeof(double) * ((size_t)hh * hw + (size_t)nvd * TH * vrs) +
+         sizeof(int) * (size_t)nvi * TH * vrs + 8 /* align */ + 2 * sizeof(uint64_t) + 128 /* base align */;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
@@ -828,9 +881,9 @@ bool make_depth_tmap(CUtensorMap* m, const void* depth, int dtype, int64_t batch
   return res == CUDA_SUCCESS;
 }
 
-template <int VAR, bool TMA>
+template <int VAR, bool TMA, int RT>
 cudaError_t launch_var(const KParams& P, const CUtensorMap& tmap, size_t sm, int64_t tiles, cudaStream_t s) {
-  auto kern = fit_tile_kernel<VAR, TMA>;
+  auto kern = fit_tile_kernel<VAR, TMA, RT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148, per_sm = 1;
@@ -841,6 +894,21 @@ cudaError_t launch_var(const KParams& P, const CUtensorMap& tmap, size_t sm, int
   const int64_t grid = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
   kern<<<(unsigned)grid, NTHREADS, sm, s>>>(P, tmap);
   return cudaGetLastError();
+}
+
+// compile-time radii for the BASELINE windows 3, 5, 7, 9, 11, 15, 31; others run generic
+template <int VAR>
+cudaError_t launch_radius(const KParams& P, const CUtensorMap& tmap, size_t sm, int64_t tiles, cudaStream_t s) {
+  switch (P.r) {
+    case 1: return launch_var<VAR, true, 1>(P, tmap, sm, tiles, s);
+    case 2: return launch_var<VAR, true, 2>(P, tmap, sm, tiles, s);
+    case 3: return launch_var<VAR, true, 3>(P, tmap, sm, tiles, s);
+    case 4: return launch_var<VAR, true, 4>(P, tmap, sm, tiles, s);
+    case 5: return launch_var<VAR, true, 5>(P, tmap, sm, tiles, s);
+    case 7: return launch_var<VAR, true, 7>(P, tmap, sm, tiles, s);
+    case 15: return launch_var<VAR, true, 15>(P, tmap, sm, tiles, s);
+    default: return launch_var<VAR, true, 0>(P, tmap, sm, tiles, s);
+  }
 }
 
 }  // namespace
@@ -973,9 +1041,9 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     const size_t sm = smem_bytes(var, r, tma, esz);
     cudaError_t e;
     if (var == VAR_STD)
-      e = tma ? launch_var<VAR_STD, true>(P, tmap, sm, tiles, s) : launch_var<VAR_STD, false>(P, tmap, sm, tiles, s);
+      e = tma ? launch_radius<VAR_STD>(P, tmap, sm, tiles, s) : launch_var<VAR_STD, false, 0>(P, tmap, sm, tiles, s);
     else
-      e = tma ? launch_var<VAR_DF, true>(P, tmap, sm, tiles, s) : launch_var<VAR_DF, false>(P, tmap, sm, tiles, s);
+      e = tma ? launch_radius<VAR_DF>(P, tmap, sm, tiles, s) : launch_var<VAR_DF, false, 0>(P, tmap, sm, tiles, s);
     if (e != cudaSuccess) return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   }
   return RF_OK;
