@@ -315,20 +315,25 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     double lk;
     const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
     if (!top) {
-      // Newton from below lam_min (monotone): two steps when well separated
-      double l = (double)k1 * (1.0 - 1e-5);
-      auto newton = [&](double x) {
-        const double P = fma(fma(t - x, x, -c1), x, det);
-        const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
-        return P * rcp_approx(dP);
-      };
-      l -= newton(l);
-      l -= newton(l);
-      if ((k2 - k1) < 0.05f * k2) {  // close bottom pair (rare): iterate to convergence
-        for (int it = 0; it < 64; ++it) {
-          const double step = newton(l);
-          l -= step;
-          if (!(fabs(step) > 1e-10 * l)) break;
+      // Newton from below lam_min (monotone).  With a well separated bottom pair
+      // (relative gap > 20%) the fp32 seed (deflated, ~2e-6 relative) already meets
+      // the 1e-4 curvature tolerance with margin; otherwise polish in fp64.
+      double l = (double)k1;
+      if ((k2 - k1) < 0.2f * k2) {
+        l *= (1.0 - 1e-5);
+        auto newton = [&](double x) {
+          const double P = fma(fma(t - x, x, -c1), x, det);
+          const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+          return P * rcp_approx(dP);
+        };
+        l -= newton(l);
+        l -= newton(l);
+        if ((k2 - k1) < 0.05f * k2) {  // close bottom pair (rare): iterate to convergence
+          for (int it = 0; it < 64; ++it) {
+            const double step = newton(l);
+            l -= step;
+            if (!(fabs(step) > 1e-10 * l)) break;
+          }
         }
       }
       lk = l;
@@ -343,10 +348,12 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
       };
       l -= newton(l);
       l -= newton(l);
-      for (int it = 0; it < 62; ++it) {
-        const double step = newton(l);
-        l -= step;
-        if (!(fabs(step) > 1e-12 * l)) break;
+      if ((k3 - k2) < 0.05f * k3) {  // top pair close too (rare): iterate to convergence
+        for (int it = 0; it < 62; ++it) {
+          const double step = newton(l);
+          l -= step;
+          if (!(fabs(step) > 1e-12 * l)) break;
+        }
       }
       const double S = t - l;
       const double Pp = det * rcp_fast(l);
@@ -516,22 +523,20 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       const unsigned char* raw = b ? raw1 : raw0;
       const int bx = box_x(x0 - r, al), by = max(y0 - r, 0);
       const int sx = (x0 - r) - bx, sy = (y0 - r) - by;  // raw index = tile index + shift
-      for (int row = tid >> 5; row < HH_; row += NTHREADS / 32) {
-        const int y = y0 - r + row;
-        for (int col = tid & 31; col < HW_; col += 32) {
-          double p = 0.0;
-          if (row + sy >= 0 && col + sx >= 0) {
-            bool mask_ok = true;
-            if (P.mask) {
-              const int x = x0 - r + col;
-              mask_ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
-            }
-            const int ri = (row + sy) * HWP + (col + sx);
-            p = esz == 2 ? primary_from_u16<VAR>(reinterpret_cast<const unsigned short*>(raw)[ri], mask_ok)
-                         : primary_from_f32<VAR>(reinterpret_cast<const float*>(raw)[ri], mask_ok);
+      for (int e = tid; e < HH_ * HW_; e += NTHREADS) {
+        const int row = e / HW_, col = e - row * HW_;
+        double p = 0.0;
+        if (row + sy >= 0 && col + sx >= 0) {
+          bool mask_ok = true;
+          if (P.mask) {
+            const int y = y0 - r + row, x = x0 - r + col;
+            mask_ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
           }
-          prim[row * HW_ + col] = p;
+          const int ri = (row + sy) * HWP + (col + sx);
+          p = esz == 2 ? primary_from_u16<VAR>(reinterpret_cast<const unsigned short*>(raw)[ri], mask_ok)
+                       : primary_from_f32<VAR>(reinterpret_cast<const float*>(raw)[ri], mask_ok);
         }
+        prim[e] = p;
       }
       __syncthreads();
       // the other buffer was consumed in the previous iteration: prefetch the next tile into it
