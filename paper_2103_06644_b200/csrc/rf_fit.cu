@@ -567,10 +567,51 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       __syncthreads();
     }
 
-    // ---- 2. vertical running sums.  Each halo column is split into `parts`
-    // row segments so that every thread of the CTA has a column segment; each
-    // segment warms up on its 2r leading rows, then slides down.
-    {
+    // ---- 2. vertical window sums.  Small compile-time radii: every (column,
+    // output row) pair sums its 2r+1 rows directly (short independent chains,
+    // all threads busy).  Otherwise each halo column is split into `parts` row
+    // segments that warm up on their 2r leading rows and then slide down.
+    if constexpr (RT > 0 && RT <= 3) {
+      constexpr int HWc = TW + 2 * RT;
+      for (int e = tid; e < TH * HWc; e += NTHREADS) {
+        const int o = e / HWc, col = e - o * HWc;
+        double a[NVD];
+        int bb[NVI];
+#pragma unroll
+        for (int k = 0; k < NVD; ++k) a[k] = 0.0;
+#pragma unroll
+        for (int k = 0; k < NVI; ++k) bb[k] = 0;
+        const double fo = (double)(o - RT);
+#pragma unroll
+        for (int k = 0; k <= 2 * RT; ++k) {
+          const double p = prim[(o + k) * HWc + col];
+          const double fdy = fo + (double)k;   // dy = (o + k) - r
+          const int dy = o + k - RT;
+          const int v = p > 0.0 ? 1 : 0;
+          if (VAR == VAR_DF) {
+            a[0] += p;
+            a[1] = fma(p, p, a[1]);
+            a[2] = fma(fdy, p, a[2]);
+            bb[0] += v;
+            bb[1] += v * dy;
+            bb[2] += v * dy * dy;
+          } else {
+            const double p2 = p * p;
+            a[0] += p;
+            a[1] += p2;
+            a[2] = fma(fdy, p, a[2]);
+            a[3] = fma(fdy, p2, a[3]);
+            a[4] = fma(fdy * fdy, p2, a[4]);
+            bb[0] += v;
+          }
+        }
+        const int cpos = (col & 3) * VQ + (col >> 2);
+#pragma unroll
+        for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * VRS + cpos] = a[k];
+#pragma unroll
+        for (int k = 0; k < NVI; ++k) vi[(k * TH + o) * VRS + cpos] = bb[k];
+      }
+    } else {
       const int parts = max(1, min(NTHREADS / HW_, TH));
       const int col = tid % HW_;
       const int part = tid / HW_;
