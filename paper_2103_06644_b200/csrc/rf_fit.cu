@@ -794,14 +794,18 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
             mu2 = q2;
           }
           WindowFit f;
-#if RF_ABLATE == 1
+#if RF_ABLATE >= 1
           f.lam = C.c00 + C.c11; f.u0 = mu0 + C.c01; f.u1 = mu1 + C.c02; f.u2 = mu2 + C.c12; f.s = C.c22;
           f.kappa = 0.1f; f.degenerate = false;
 #else
           solve_window(C, mu0, mu1, mu2, nd, f);
 #endif
+#if RF_ABLATE >= 2
+          nx = (float)f.u0; ny = (float)f.u1; nz = (float)f.u2; off = (float)f.s;
+#else
           if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
           else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
+#endif
           res = fsqrt(fmaxf((float)(f.lam * invn), 0.0f));
           cur = f.kappa;
           st |= RF_PIX_FIT;
