@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define RF_ABI_VERSION 1
+#define RF_ABI_VERSION 2
 
 typedef enum rf_status {
   RF_OK = 0,
@@ -44,14 +44,25 @@ typedef enum rf_depth_dtype {
                            (DepthImage.from_millimeters, synth.py:111-114)         */
 } rf_depth_dtype;
 
-/* formulation bits (reference FORMULATIONS, fitting.py:45-49) */
-#define RF_IMPLICIT_STANDARD 1 /* "implicit-standard": monomials [X, Y, Z, 1]       */
-#define RF_IMPLICIT_RGBD 2     /* "implicit-rgbd" (disparity form): [tx, ty, 1, 1/Z] */
+/* formulation ids = positions in the reference's FORMULATIONS tuple (fitting.py:45-49) */
+#define RF_FORM_IMPLICIT_STANDARD 0 /* "implicit-standard": smallest eigvec of [X,Y,Z,1] scatter */
+#define RF_FORM_IMPLICIT_RGBD 1     /* "implicit-rgbd" (disparity form): [tx, ty, 1, 1/Z]       */
+#define RF_FORM_EXPLICIT_STANDARD 2 /* "explicit-standard": Z = aX + bY + c                     */
+#define RF_FORM_EXPLICIT_RGBD 3     /* "explicit-rgbd": 1/Z = a tx + b ty + c                    */
+#define RF_NUM_FORMULATIONS 4
+/* formulation mask bits (1 << id) */
+#define RF_IMPLICIT_STANDARD (1 << RF_FORM_IMPLICIT_STANDARD)
+#define RF_IMPLICIT_RGBD (1 << RF_FORM_IMPLICIT_RGBD)
+#define RF_EXPLICIT_STANDARD (1 << RF_FORM_EXPLICIT_STANDARD)
+#define RF_EXPLICIT_RGBD (1 << RF_FORM_EXPLICIT_RGBD)
+#define RF_ALL_FORMULATIONS 15
 
 /* status bits of the per-pixel status byte */
 #define RF_PIX_INPUT_VALID 1u  /* centre pixel valid (DepthImage.valid)               */
-#define RF_PIX_FIT 2u          /* centre valid and window holds >= MIN_SAMPLES (4)   */
-#define RF_PIX_DEGENERATE 4u   /* FitResult.degenerate (fitting.py:553-554)           */
+#define RF_PIX_FIT 2u          /* centre valid and window holds >= MIN_SAMPLES
+                                  (4 implicit, 3 explicit; fitting.py:55-60)          */
+#define RF_PIX_DEGENERATE 4u   /* FitResult.degenerate (fitting.py:553-554 implicit,
+                                  Cholesky pivot failure fitting.py:584-589 explicit)  */
 
 /* Pinhole intrinsics (reference CameraIntrinsics, camera.py:35-75). */
 typedef struct rf_intrinsics {
@@ -65,7 +76,9 @@ typedef struct rf_tables rf_tables;
 
 /* Caller-owned device output planes for one formulation, each [batch, H, W]
  * (normal is [batch, H, W, 3], xyz interleaved).  Pixels whose status lacks
- * RF_PIX_FIT hold NaN in every float plane. */
+ * RF_PIX_FIT hold NaN in every float plane.  Explicit fits are reported in
+ * implicit form (explicit_to_implicit, fitting.py:729-739) and their residual is
+ * the rms of the explicit objective (fitting.py:590-597). */
 typedef struct rf_pixel_out {
   float* normal;     /* unit normal (a,b,c)/|(a,b,c)|, canonical sign (fitting.py:76-94) */
   float* offset;     /* d/|(a,b,c)|: n.X + offset = 0                                    */
@@ -86,15 +99,17 @@ rf_status rf_tables_destroy(rf_tables* tables);
 /* Replaces, for every pixel of a batch of frames, the reference pipeline
  *   fit_rect(depth, maps, Rect(max(x-r,0), max(y-r,0), min(x+r+1,W), min(y+r+1,H)),
  *            formulation, backend)            (fitting.py:757-786)
- * with window = 2r+1.  depth: device pointer to batch frames of H rows, each
- * row_pitch elements apart (frame stride = H*row_pitch).  mask: optional device
- * uint8 [batch,H,W] (DepthImage(values, valid=mask), synth.py:88-94) or NULL.
- * formulation_mask: RF_IMPLICIT_* bits; out_std / out_rgbd may be NULL when the
- * matching bit is clear.  stream: a cudaStream_t (NULL = legacy default). */
+ * with window = 2r+1, for each formulation whose bit is set in formulation_mask.
+ * depth: device pointer to batch frames of H rows, each row_pitch elements apart
+ * (frame stride = H*row_pitch).  mask: optional device uint8 [batch,H,W]
+ * (DepthImage(values, valid=mask), synth.py:88-94) or NULL.  outs: array of
+ * RF_NUM_FORMULATIONS output sets indexed by RF_FORM_*; only the requested entries
+ * are read.  The implicit and explicit fits of one space share one kernel launch
+ * (one pass over the window moments).  stream: a cudaStream_t (NULL = legacy default). */
 rf_status rf_fit_pixels(const rf_tables* tables, const void* depth, int dtype, int64_t batch,
                         int32_t height, int32_t width, int64_t row_pitch, const uint8_t* mask,
-                        int32_t window, int32_t formulation_mask, const rf_pixel_out* out_std,
-                        const rf_pixel_out* out_rgbd, void* stream);
+                        int32_t window, int32_t formulation_mask, const rf_pixel_out* outs,
+                        void* stream);
 
 /* Number of kernel launches rf_fit_pixels issues for a given formulation mask. */
 int32_t rf_launches_per_call(int32_t formulation_mask);

@@ -30,9 +30,11 @@ def normal_angles(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.arctan2(cross, dot)
 
 
-def compare(gpu: dict, ref: dict) -> dict:
+def compare(gpu: dict, ref: dict, explicit_fit: bool = False) -> dict:
     """gpu/ref: dicts of flat arrays normal (P,3), offset, residual, curvature, status (P,);
-    ref also carries ``scale`` = ||S||_F/n.  Returns metrics and a pass flag."""
+    ref also carries ``scale`` = ||S||_F/n.  Returns metrics and a pass flag.  Explicit fits
+    compute their residual from aggregated sums, sum(b^2) - alpha.rhs, whose cancellation
+    floor the reference documents (fitting.py:592-595): their allowance uses 1e-10."""
     gs = np.asarray(gpu["status"]).astype(np.uint8).ravel()
     rs = np.asarray(ref["status"]).astype(np.uint8).ravel()
     mask_bits = 0b011
@@ -46,7 +48,7 @@ def compare(gpu: dict, ref: dict) -> dict:
     gres = np.asarray(gpu["residual"], np.float64).ravel()[sel]
     rres = np.asarray(ref["residual"], np.float64).ravel()[sel]
     scale = np.asarray(ref["scale"], np.float64).ravel()[sel]
-    res_floor = np.sqrt(LAM_FLOOR_REL * np.abs(scale))
+    res_floor = np.sqrt((1e-10 if explicit_fit else LAM_FLOOR_REL) * np.abs(scale))
     # error in units of the tolerance: <= 1 passes
     res_err = np.abs(gres - rres) / (REL_TOL * np.abs(rres) + res_floor) * REL_TOL
     gc = np.asarray(gpu["curvature"], np.float64).ravel()[sel]

@@ -30,10 +30,13 @@ LIB_PATH = HERE / "_build" / "librf_oracle.so"
 
 STANDARD = 0  # reference "implicit-standard"
 RGBD = 1  # reference "implicit-rgbd" (disparity form)
+EXPLICIT_STANDARD = 2  # reference "explicit-standard"
+EXPLICIT_RGBD = 3  # reference "explicit-rgbd"
 NAIVE = 0
 INTEGRAL = 1
 
-FORMULATION_CODES = {"implicit-standard": STANDARD, "implicit-rgbd": RGBD}
+FORMULATION_CODES = {"implicit-standard": STANDARD, "implicit-rgbd": RGBD,
+                     "explicit-standard": EXPLICIT_STANDARD, "explicit-rgbd": EXPLICIT_RGBD}
 
 _lib = None
 
@@ -112,7 +115,9 @@ def fit_pixels(values, valid, tan_x, tan_y, window, formulation, backend=NAIVE, 
     Returns a dict with ``normal`` (P,3) f32, ``offset``/``residual``/``curvature`` (P,) f32
     and ``status`` (P,) u8, where P = H*W (or len(pixels)), ``scale`` = ||S||_F / n (P,)
     f64 (the rounding floor of lambda); optionally the canonical
-    fp64 coefficient vector ``coef`` (P,4) and smallest eigenvalue ``lam``.
+    fp64 coefficient vector ``coef`` (P,4) and smallest eigenvalue ``lam`` (for the explicit
+    formulations ``coef`` is explicit_to_implicit of the fit and ``lam`` the residual sum
+    of squares sum(b^2) - alpha.rhs).
     """
     if isinstance(formulation, str):
         formulation = FORMULATION_CODES[formulation]

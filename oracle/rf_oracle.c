@@ -23,6 +23,11 @@
  *   - _fit_implicit fitting.py:546-559 (argsort, gap, degenerate flag with
  *       _EIGEN_TIE_REL = 1e-9, rms = sqrt(max(lam,0)/n))
  *   - canonicalize_implicit fitting.py:76-94 (order (c,b,a,d), eps 1e-9)
+ *   - explicit fits: the normal equations read from the same space's scatter
+ *       (accumulate_scatter_naive / scatter_from_integrals, fitting.py:370-381,
+ *       464-476, 523-533), cholesky3 + solve_cholesky3 or _pinv_solve,
+ *       _fit_explicit and explicit_to_implicit (fitting.py:264-322, 582-599,
+ *       729-739), MIN_SAMPLES 3
  * Per-pixel extensions (not in the reference):
  *   - window of pixel (x,y): Rect(max(x-r,0), max(y-r,0), min(x+r+1,W),
  *     min(y+r+1,H)) -- clipped like the segmenter's border tiles
@@ -41,13 +46,17 @@
 #include <stdatomic.h>
 #include <unistd.h>
 
-#define RFO_STANDARD 0
-#define RFO_RGBD 1
+#define RFO_STANDARD 0          /* implicit-standard */
+#define RFO_RGBD 1              /* implicit-rgbd (disparity form) */
+#define RFO_EXPLICIT_STANDARD 2 /* explicit-standard */
+#define RFO_EXPLICIT_RGBD 3     /* explicit-rgbd */
+#define RFO_SPACE(f) ((f) == RFO_STANDARD || (f) == RFO_EXPLICIT_STANDARD ? RFO_STANDARD : RFO_RGBD)
 #define RFO_NAIVE 0
 #define RFO_INTEGRAL 1
 
 static const double CANONICAL_EPS = 1e-9;  /* fitting.py:65 */
 static const double EIGEN_TIE_REL = 1e-9;  /* fitting.py:69 */
+static const double PIVOT_REL = 1e-12;     /* fitting.py:71 */
 
 /* ---- jacobi_eigh, fitting.py:193-253 (returns 0 ok, -1 not converged) ---- */
 static int jacobi_eigh(int n, const double* m, double* values, double* vectors) {
@@ -178,6 +187,96 @@ static void fit_scatter(const double* S, int n, int formulation, fit_out* o) {
   o->curvature = tr > 0.0 ? mn / tr : 0.0;
 }
 
+/* curvature (A17) from an implicit 4x4 scatter of the formulation's space */
+static double curvature_of(const double* S, int space) {
+  int I[3], k;
+  if (space == RFO_STANDARD) { I[0] = 0; I[1] = 1; I[2] = 2; k = 3; }
+  else { I[0] = 0; I[1] = 1; I[2] = 3; k = 2; }
+  double nn = S[k * 4 + k];
+  double C3[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      C3[i * 3 + j] = S[I[i] * 4 + I[j]] - S[I[i] * 4 + k] * S[I[j] * 4 + k] / nn;
+  double cv[3], cvec[9];
+  jacobi_eigh(3, C3, cv, cvec);
+  double mn = cv[0];
+  if (cv[1] < mn) mn = cv[1];
+  if (cv[2] < mn) mn = cv[2];
+  double tr = C3[0] + C3[4] + C3[8];
+  return tr > 0.0 ? mn / tr : 0.0;
+}
+
+/* cholesky3 fitting.py:264-293; returns 0, or -1 for DegenerateFitError */
+static int cholesky3(const double* s, double* L) {
+  double trace = s[0] + s[4] + s[8];
+  double floor = PIVOT_REL * trace;
+  if (!isfinite(trace) || trace <= 0.0) return -1;
+  double p0 = s[0];
+  if (p0 <= floor) return -1;
+  double l00 = sqrt(p0), l10 = s[3] / l00, l20 = s[6] / l00;
+  double p1 = s[4] - l10 * l10;
+  if (p1 <= floor) return -1;
+  double l11 = sqrt(p1), l21 = (s[7] - l20 * l10) / l11;
+  double p2 = s[8] - l20 * l20 - l21 * l21;
+  if (p2 <= floor) return -1;
+  double l22 = sqrt(p2);
+  L[0] = l00; L[1] = l10; L[2] = l11; L[3] = l20; L[4] = l21; L[5] = l22;
+  return 0;
+}
+
+/* _fit_explicit fitting.py:582-599 (+ explicit_to_implicit :729-739, A17 curvature).
+ * S: the implicit 4x4 scatter of the same space, from which the explicit normal
+ * equations are read: standard M = S[{0,1,3}], rhs = S[{0,1,3},2], target Z;
+ * rgbd M = S[{0,1,2}], rhs = S[{0,1,2},3], target 1/Z. */
+static void fit_explicit(const double* S, int n, int space, fit_out* o) {
+  int I[3], tcol;
+  if (space == RFO_STANDARD) { I[0] = 0; I[1] = 1; I[2] = 3; tcol = 2; }
+  else { I[0] = 0; I[1] = 1; I[2] = 2; tcol = 3; }
+  double M[9], rhs[3];
+  for (int i = 0; i < 3; ++i) {
+    rhs[i] = S[I[i] * 4 + tcol];
+    for (int j = 0; j < 3; ++j) M[i * 3 + j] = S[I[i] * 4 + I[j]];
+  }
+  double target_sq = S[tcol * 4 + tcol];
+  double L[6], alpha[3];
+  o->failed = 0;
+  if (cholesky3(M, L) == 0) {
+    /* solve_cholesky3 fitting.py:296-305 */
+    double y0 = rhs[0] / L[0];
+    double y1 = (rhs[1] - L[1] * y0) / L[2];
+    double y2 = (rhs[2] - L[3] * y0 - L[4] * y1) / L[5];
+    alpha[2] = y2 / L[5];
+    alpha[1] = (y1 - L[4] * alpha[2]) / L[2];
+    alpha[0] = (y0 - L[1] * alpha[1] - L[3] * alpha[2]) / L[0];
+    o->degenerate = 0;
+  } else {
+    /* _pinv_solve fitting.py:313-322 */
+    double vals[3], vecs[9];
+    jacobi_eigh(3, M, vals, vecs);
+    double tr = M[0] + M[4] + M[8];
+    double tol = PIVOT_REL * (tr > 0.0 ? tr : 0.0);
+    alpha[0] = alpha[1] = alpha[2] = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      if (vals[i] > tol) {
+        double ub = vecs[0 * 3 + i] * rhs[0] + vecs[1 * 3 + i] * rhs[1] + vecs[2 * 3 + i] * rhs[2];
+        for (int k = 0; k < 3; ++k) alpha[k] += vecs[k * 3 + i] * (ub / vals[i]);
+      }
+    }
+    o->degenerate = 1;
+  }
+  double sq = target_sq - (alpha[0] * rhs[0] + alpha[1] * rhs[1] + alpha[2] * rhs[2]);
+  o->rms = sqrt((sq > 0.0 ? sq : 0.0) / (double)n);
+  o->lam = sq;
+  double imp[4];
+  if (space == RFO_STANDARD) { imp[0] = alpha[0]; imp[1] = alpha[1]; imp[2] = -1.0; imp[3] = alpha[2]; }
+  else { imp[0] = alpha[0]; imp[1] = alpha[1]; imp[2] = alpha[2]; imp[3] = -1.0; }
+  canonicalize(imp, o->coef);
+  double fro2 = 0.0;
+  for (int i = 0; i < 16; ++i) fro2 += S[i] * S[i];
+  o->scale = sqrt(fro2) / (double)n;
+  o->curvature = curvature_of(S, space);
+}
+
 /* ---- naive scatter: gather_window_samples + accumulate_scatter_naive ---- */
 static int naive_scatter(const double* depth, const uint8_t* valid, const double* tan_x,
                          const double* tan_y, int W, int x0, int y0, int x1, int y1,
@@ -301,12 +400,12 @@ static int build_stack(const double* depth, const uint8_t* valid, const double* 
 
 /* scatter_from_integrals, fitting.py:420-521 */
 static int integral_scatter(const sat_stack* st, int x0, int y0, int x1, int y1, int formulation,
-                            double* S) {
+                            int min_samples, double* S) {
   int64_t TS = (int64_t)(st->H + 1) * (st->W + 1);
   int W = st->W;
 #define BOX(c) box(st->t + TS * (c), W, x0, y0, x1, y1)
   int n = (int)llround(BOX(0));
-  if (n < 4) return n;
+  if (n < min_samples) return n;
   if (formulation == RFO_STANDARD) {
     double sx2 = BOX(CH_ST_X2), sxy = BOX(CH_ST_XY), sxz = BOX(CH_ST_XZ), sx = BOX(CH_ST_X);
     double sy2 = BOX(CH_ST_Y2), syz = BOX(CH_ST_YZ), sy = BOX(CH_ST_Y), sz2 = BOX(CH_ST_Z2),
@@ -361,15 +460,18 @@ static void fit_one(job_t* J, int64_t k) {
   uint8_t s = J->valid[idx] ? 1 : 0;
   double S[16];
   int n = 0;
+  const int space = RFO_SPACE(J->formulation);
+  const int explicit_fit = J->formulation >= RFO_EXPLICIT_STANDARD;
+  const int min_samples = explicit_fit ? 3 : 4; /* MIN_SAMPLES fitting.py:55-60 */
   if (s) {
     n = J->backend == RFO_INTEGRAL
-            ? integral_scatter(J->st, x0, y0, x1, y1, J->formulation, S)
-            : naive_scatter(J->depth, J->valid, J->tan_x, J->tan_y, W, x0, y0, x1, y1,
-                            J->formulation, S);
+            ? integral_scatter(J->st, x0, y0, x1, y1, space, min_samples, S)
+            : naive_scatter(J->depth, J->valid, J->tan_x, J->tan_y, W, x0, y0, x1, y1, space, S);
   }
-  if (s && n >= 4) {
+  if (s && n >= min_samples) {
     fit_out o;
-    fit_scatter(S, n, J->formulation, &o);
+    if (explicit_fit) fit_explicit(S, n, space, &o);
+    else fit_scatter(S, n, space, &o);
     if (o.failed) {
       s |= 8;
     } else {
@@ -420,11 +522,11 @@ int rfo_fit_pixels(const double* depth, const uint8_t* valid, const double* tan_
                    float* curvature, uint8_t* status, double* coef, double* lam, double* scale,
                    int nthreads) {
   if (window < 1 || (window & 1) == 0 || H <= 0 || W <= 0) return -1;
-  if (formulation != RFO_STANDARD && formulation != RFO_RGBD) return -1;
+  if (formulation < RFO_STANDARD || formulation > RFO_EXPLICIT_RGBD) return -1;
   sat_stack st;
   st.t = NULL;
   if (backend == RFO_INTEGRAL) {
-    if (build_stack(depth, valid, tan_x, tan_y, H, W, formulation, &st) != 0) return -1;
+    if (build_stack(depth, valid, tan_x, tan_y, H, W, RFO_SPACE(formulation), &st) != 0) return -1;
   }
   job_t J = {depth, tan_x, tan_y, valid, H, W, window / 2, formulation, backend, &st, pix, npix,
              normal, offset, residual, curvature, status, coef, lam, scale, 0};
@@ -450,7 +552,8 @@ int rfo_fit_pixels(const double* depth, const uint8_t* valid, const double* tan_
 int rfo_fit_scatter(const double* S, int n, int formulation, double* coef, double* lam,
                     double* rms, double* curvature, int* degenerate) {
   fit_out o;
-  fit_scatter(S, n, formulation, &o);
+  if (formulation >= RFO_EXPLICIT_STANDARD) fit_explicit(S, n, RFO_SPACE(formulation), &o);
+  else fit_scatter(S, n, formulation, &o);
   memcpy(coef, o.coef, sizeof(o.coef));
   *lam = o.lam;
   *rms = o.rms;

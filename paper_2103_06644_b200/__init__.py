@@ -3,8 +3,12 @@ a drop-in for the fitting hot path of the reference package ``rangefit``
 (arxiv/paper_2103_06644).  See DESIGN.md and include/rangefit_b200.h."""
 
 from .pixels import (
+    EXPLICIT_RGBD,
+    EXPLICIT_STANDARD,
+    FORMULATIONS,
     IMPLICIT_RGBD,
     IMPLICIT_STANDARD,
+    MIN_SAMPLES,
     PIXEL_FORMULATIONS,
     STATUS_DEGENERATE,
     STATUS_FIT,
@@ -18,8 +22,12 @@ from .pixels import (
 )
 
 __all__ = [
+    "EXPLICIT_RGBD",
+    "EXPLICIT_STANDARD",
+    "FORMULATIONS",
     "IMPLICIT_RGBD",
     "IMPLICIT_STANDARD",
+    "MIN_SAMPLES",
     "PIXEL_FORMULATIONS",
     "STATUS_DEGENERATE",
     "STATUS_FIT",

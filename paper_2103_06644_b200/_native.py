@@ -24,8 +24,16 @@ RF_ERR_UNSUPPORTED = 4
 RF_DEPTH_F32_M = 0
 RF_DEPTH_U16_MM = 1
 
-RF_IMPLICIT_STANDARD = 1
-RF_IMPLICIT_RGBD = 2
+RF_FORM_IMPLICIT_STANDARD = 0
+RF_FORM_IMPLICIT_RGBD = 1
+RF_FORM_EXPLICIT_STANDARD = 2
+RF_FORM_EXPLICIT_RGBD = 3
+RF_NUM_FORMULATIONS = 4
+RF_IMPLICIT_STANDARD = 1 << RF_FORM_IMPLICIT_STANDARD
+RF_IMPLICIT_RGBD = 1 << RF_FORM_IMPLICIT_RGBD
+RF_EXPLICIT_STANDARD = 1 << RF_FORM_EXPLICIT_STANDARD
+RF_EXPLICIT_RGBD = 1 << RF_FORM_EXPLICIT_RGBD
+RF_ABI_VERSION = 2
 
 RF_PIX_INPUT_VALID = 1
 RF_PIX_FIT = 2
@@ -87,7 +95,7 @@ def load() -> ctypes.CDLL:
     L.rf_tables_destroy.restype = ctypes.c_int
     L.rf_fit_pixels.argtypes = [
         vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, vp,
-        ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(RfPixelOut), ctypes.POINTER(RfPixelOut), vp,
+        ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(RfPixelOut), vp,
     ]
     L.rf_fit_pixels.restype = ctypes.c_int
     L.rf_launches_per_call.argtypes = [ctypes.c_int32]
@@ -96,6 +104,8 @@ def load() -> ctypes.CDLL:
     L.rf_last_error.restype = ctypes.c_char_p
     L.rf_abi_version.argtypes = []
     L.rf_abi_version.restype = ctypes.c_int32
+    if L.rf_abi_version() != RF_ABI_VERSION:
+        raise NativeLibraryMissing(f"{LIB_PATH} has ABI {L.rf_abi_version()}, expected {RF_ABI_VERSION}: rebuild")
     _lib = L
     return L
 

@@ -48,6 +48,14 @@ constexpr int MAX_RADIUS = 32;
 constexpr int VAR_STD = 0;   // implicit-standard
 constexpr int VAR_DF = 1;    // implicit-rgbd (disparity form)
 
+struct OutPlanes {
+  float* normal;
+  float* offset;
+  float* residual;
+  float* curvature;
+  uint8_t* status;
+};
+
 struct KParams {
   const void* depth;
   const uint8_t* mask;
@@ -59,11 +67,8 @@ struct KParams {
   int64_t out_frame;    // H*W
   int64_t batch;
   int H, W, r, dtype;
-  float* normal;
-  float* offset;
-  float* residual;
-  float* curvature;
-  uint8_t* status;
+  int do_imp, do_exp;  // implicit / explicit fit of this kernel's space requested
+  OutPlanes imp, exp;  // implicit-* / explicit-* output planes of the space
 };
 
 // ------------------------------------------------------------------ helpers
@@ -140,6 +145,116 @@ struct WindowFit {
   float kappa;      // curvature
   bool degenerate;
 };
+
+// Curvature lam_min(C)/tr(C) from the invariants t = tr C,
+// c1 = sum of principal 2x2 minors, det = det C and the fp32 roots k1<=k2<=k3 of
+// l^3 - t l^2 + c1 l - det: fp64 Newton from below, or -- when the bottom pair is
+// close -- Newton from above on lam_max and deflation.
+__device__ __forceinline__ float curvature_from(double t, double c1, double det, float ft, float k1,
+                                                float k2, float k3) {
+  {
+    double lk;
+    const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
+    if (!top) {
+      // Newton from below lam_min (monotone).  With a well separated bottom pair
+      // (relative gap > 20%) the fp32 seed (deflated, ~2e-6 relative) already meets
+      // the 1e-4 curvature tolerance with margin; otherwise polish in fp64.
+      double l = (double)k1;
+      if ((k2 - k1) < 0.2f * k2) {
+        l *= (1.0 - 1e-5);
+        auto newton = [&](double x) {
+          const double P = fma(fma(t - x, x, -c1), x, det);
+          const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+          return P * rcp_approx(dP);
+        };
+        l -= newton(l);
+        l -= newton(l);
+        if ((k2 - k1) < 0.05f * k2) {  // close bottom pair (rare): iterate to convergence
+          for (int it = 0; it < 64; ++it) {
+            const double step = newton(l);
+            l -= step;
+            if (!(fabs(step) > 1e-10 * l)) break;
+          }
+        }
+      }
+      lk = l;
+    } else {
+      // near-tie at the bottom: Newton from above lam_max (well separated here),
+      // then deflate; lam_max only needs ~1e-10 for a 1e-5 curvature
+      double l = fmin((double)k3 * (1.0 + 1e-5), t);
+      auto newton = [&](double x) {
+        const double P = fma(fma(t - x, x, -c1), x, det);
+        const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+        return P * rcp_approx(dP);
+      };
+      l -= newton(l);
+      l -= newton(l);
+      if ((k3 - k2) < 0.05f * k3) {  // top pair close too (rare): iterate to convergence
+        for (int it = 0; it < 62; ++it) {
+          const double step = newton(l);
+          l -= step;
+          if (!(fabs(step) > 1e-12 * l)) break;
+        }
+      }
+      const double S = t - l;
+      const double Pp = det * rcp_fast(l);
+      const double den = S + (double)fsqrt((float)fmax(fma(S, S, -4.0 * Pp), 0.0));
+      lk = den > 0.0 ? 2.0 * Pp * rcp_fast(den) : 0.0;
+    }
+    return t > 0.0 ? (float)lk * frcp(ft) : 0.0f;
+  }
+}
+
+// curvature when no implicit solve runs (explicit fits only)
+__device__ __forceinline__ float curvature_only(const Sym3& C) {
+  const double A00 = C.c11 * C.c22 - C.c12 * C.c12;
+  const double A11 = C.c00 * C.c22 - C.c02 * C.c02;
+  const double A22 = C.c00 * C.c11 - C.c01 * C.c01;
+  const double A01 = C.c02 * C.c12 - C.c01 * C.c22;
+  const double A02 = C.c01 * C.c12 - C.c02 * C.c11;
+  const double t = C.c00 + C.c11 + C.c22;
+  const double c1 = A00 + A11 + A22;
+  const double det = C.c00 * A00 + C.c01 * A01 + C.c02 * A02;
+  float k1, k2, k3;
+  const float ft = (float)t;
+  trig_cubic(ft, (float)c1, (float)det, k1, k2, k3);
+  return curvature_from(t, c1, det, ft, k1, k2, k3);
+}
+
+// Explicit fits (fitting.py:582-621) on the centred moments of the space's monomials
+// (m0, m1, m2) = (X, Y, Z) standard or (tx, ty, 1/Z) rgbd: the target m2 regressed on
+// (m0, m1, 1).  Solved centred ([a b] from the 2x2 covariance, c = mu2 - a mu0 - b mu1),
+// which equals the reference's uncentred normal equations; the residual sum of squares
+// C22 - [a b].[C02 C12] equals its sum(b^2) - alpha.rhs.  degenerate replays the
+// reference's Cholesky pivot test (cholesky3, fitting.py:264-293) on the uncentred
+// matrix [[S00, S01, S0], [S01, S11, S1], [S0, S1, n]].
+struct ExplicitFit {
+  double a, b, c, ss;
+  bool degenerate;
+};
+__device__ __forceinline__ void explicit_solve(const Sym3& C, double m0, double m1, double m2,
+                                               double n, ExplicitFit& out) {
+  const double det2 = fma(C.c00, C.c11, -C.c01 * C.c01);
+  const double idet = det2 > 0.0 ? rcp_fast(det2) : 0.0;
+  out.a = fma(C.c11, C.c02, -C.c01 * C.c12) * idet;
+  out.b = fma(C.c00, C.c12, -C.c01 * C.c02) * idet;
+  out.c = m2 - out.a * m0 - out.b * m1;
+  out.ss = C.c22 - (out.a * C.c02 + out.b * C.c12);
+  // uncentred matrix and its Cholesky pivots
+  const double M00 = fma(n * m0, m0, C.c00), M01 = fma(n * m0, m1, C.c01), M11 = fma(n * m1, m1, C.c11);
+  const double M02 = n * m0, M12 = n * m1;
+  const double trace = M00 + M11 + n;
+  const double fl = 1e-12 * trace;
+  const double p0 = M00;
+  const double l10 = M01 * rcp_fast(M00);
+  const double p1 = fma(-l10, M01, M11);
+  // p2 = n - [M02 M12] M2^-1 [M02 M12]^T = n / (1 + n mu^T C2^-1 mu)
+  const double q = (m0 * fma(C.c11, m0, -C.c01 * m1) + m1 * fma(C.c00, m1, -C.c01 * m0)) * idet;
+  const double p2 = det2 > 0.0 ? n * rcp_fast(fma(n, q, 1.0)) : 0.0;
+  (void)M02;
+  (void)M12;
+  out.degenerate = !(trace > 0.0) || p0 <= fl || p1 <= fl || p2 <= fl;
+}
 
 // Smallest eigenpair of S = [[C + n mu mu^T, n mu], [n mu^T, n]] (the
 // uncentred scatter of [m0, m1, m2, 1], fitting.py:339-381) through the
@@ -311,57 +426,7 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
   }
 
   // curvature: lam_min(C) / tr(C)
-  {
-    double lk;
-    const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
-    if (!top) {
-      // Newton from below lam_min (monotone).  With a well separated bottom pair
-      // (relative gap > 20%) the fp32 seed (deflated, ~2e-6 relative) already meets
-      // the 1e-4 curvature tolerance with margin; otherwise polish in fp64.
-      double l = (double)k1;
-      if ((k2 - k1) < 0.2f * k2) {
-        l *= (1.0 - 1e-5);
-        auto newton = [&](double x) {
-          const double P = fma(fma(t - x, x, -c1), x, det);
-          const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
-          return P * rcp_approx(dP);
-        };
-        l -= newton(l);
-        l -= newton(l);
-        if ((k2 - k1) < 0.05f * k2) {  // close bottom pair (rare): iterate to convergence
-          for (int it = 0; it < 64; ++it) {
-            const double step = newton(l);
-            l -= step;
-            if (!(fabs(step) > 1e-10 * l)) break;
-          }
-        }
-      }
-      lk = l;
-    } else {
-      // near-tie at the bottom: Newton from above lam_max (well separated here),
-      // then deflate; lam_max only needs ~1e-10 for a 1e-5 curvature
-      double l = fmin((double)k3 * (1.0 + 1e-5), t);
-      auto newton = [&](double x) {
-        const double P = fma(fma(t - x, x, -c1), x, det);
-        const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
-        return P * rcp_approx(dP);
-      };
-      l -= newton(l);
-      l -= newton(l);
-      if ((k3 - k2) < 0.05f * k3) {  // top pair close too (rare): iterate to convergence
-        for (int it = 0; it < 62; ++it) {
-          const double step = newton(l);
-          l -= step;
-          if (!(fabs(step) > 1e-12 * l)) break;
-        }
-      }
-      const double S = t - l;
-      const double Pp = det * rcp_fast(l);
-      const double den = S + (double)fsqrt((float)fmax(fma(S, S, -4.0 * Pp), 0.0));
-      lk = den > 0.0 ? 2.0 * Pp * rcp_fast(den) : 0.0;
-    }
-    out.kappa = t > 0.0 ? (float)lk * frcp(ft) : 0.0f;
-  }
+  out.kappa = curvature_from(t, c1, det, ft, k1, k2, k3);
 }
 
 // canonical sign + unit normal / offset (fitting.py:76-94 and SURVEY A18)
@@ -463,7 +528,8 @@ __device__ __forceinline__ double primary_from_u16(unsigned short mm, bool mask_
 // other of two shared buffers while this tile's column and row passes run.
 // RT > 0: compile-time window radius (all halo geometry and shared-memory offsets
 // fold to constants); RT == 0: runtime radius P.r.
-template <int VAR, bool USE_TMA, int RT>
+// EXP: explicit fits compiled in (false keeps the implicit-only kernel lean).
+template <int VAR, bool USE_TMA, int RT, bool EXP>
 __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     fit_tile_kernel(const KParams P, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_dyn[];
@@ -745,7 +811,8 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         uint8_t st = pc > 0.0 ? RF_PIX_INPUT_VALID : 0;
         const int nwin = (int)hi[0];
         float nx = __int_as_float(0x7fc00000), ny = nx, nz = nx, off = nx, res = nx, cur = nx;
-        if (st && nwin >= 4 && gx < P.W) {
+        uint8_t stx = st;  // explicit-fit status (MIN_SAMPLES 3 instead of 4)
+        if (st && nwin >= (EXP ? 3 : 4) && gx < P.W) {
           const double nd = (double)nwin;
           const double invn = rcp_fast(nd);
           Sym3 C;
@@ -793,6 +860,8 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
             mu1 = fma(ify, q1, tyo * q2);
             mu2 = q2;
           }
+          float kap = 0.0f;
+          if (P.do_imp && nwin >= 4) {
           WindowFit f;
 #if RF_ABLATE >= 1
           f.lam = C.c00 + C.c11; f.u0 = mu0 + C.c01; f.u1 = mu1 + C.c02; f.u2 = mu2 + C.c12; f.s = C.c22;
@@ -808,8 +877,39 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
 #endif
           res = fsqrt(fmaxf((float)(f.lam * invn), 0.0f));
           cur = f.kappa;
+          kap = f.kappa;
           st |= RF_PIX_FIT;
           if (f.degenerate) st |= RF_PIX_DEGENERATE;
+          }
+          if (EXP && P.do_exp) {
+            if (!(P.do_imp && nwin >= 4)) kap = curvature_only(C);
+            ExplicitFit e;
+            explicit_solve(C, mu0, mu1, mu2, nd, e);
+            float ex, ey, ez, eo;
+            // explicit_to_implicit (fitting.py:729-739): standard (a, b, -1, c), rgbd (a, b, c, -1)
+            if (VAR == VAR_DF) finish_plane(e.a, e.b, e.c, -1.0, ex, ey, ez, eo);
+            else finish_plane(e.a, e.b, -1.0, e.c, ex, ey, ez, eo);
+            stx |= RF_PIX_FIT | (e.degenerate ? RF_PIX_DEGENERATE : 0);
+            const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
+            P.exp.normal[3 * p + 0] = ex;
+            P.exp.normal[3 * p + 1] = ey;
+            P.exp.normal[3 * p + 2] = ez;
+            P.exp.offset[p] = eo;
+            P.exp.residual[p] = fsqrt(fmaxf((float)(e.ss * invn), 0.0f));
+            P.exp.curvature[p] = kap;
+            P.exp.status[p] = stx;
+          }
+        }
+        if (EXP && P.do_exp && !(stx & RF_PIX_FIT) && gx < P.W) {
+          const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
+          const float qn = __int_as_float(0x7fc00000);
+          P.exp.normal[3 * p + 0] = qn;
+          P.exp.normal[3 * p + 1] = qn;
+          P.exp.normal[3 * p + 2] = qn;
+          P.exp.offset[p] = qn;
+          P.exp.residual[p] = qn;
+          P.exp.curvature[p] = qn;
+          P.exp.status[p] = stx;
         }
     #if RF_STAGE_OUTPUTS
         o_n[j][0] = nx;
@@ -822,43 +922,45 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     #else
         if (gx < P.W) {
           const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
-          P.normal[3 * p + 0] = nx;
-          P.normal[3 * p + 1] = ny;
-          P.normal[3 * p + 2] = nz;
-          P.offset[p] = off;
-          P.residual[p] = res;
-          P.curvature[p] = cur;
-          P.status[p] = st;
+          P.imp.normal[3 * p + 0] = nx;
+          P.imp.normal[3 * p + 1] = ny;
+          P.imp.normal[3 * p + 2] = nz;
+          P.imp.offset[p] = off;
+          P.imp.residual[p] = res;
+          P.imp.curvature[p] = cur;
+          P.imp.status[p] = st;
         }
     #endif
       }
 
     #if RF_STAGE_OUTPUTS
       // ---- stores
+      if (P.do_imp) {
       const int64_t pix0 = frame * P.out_frame + (int64_t)gy * P.W + gxs;
       const bool vec = ((P.W & (KSEG - 1)) == 0) && (gxs + KSEG <= P.W);
       if (vec) {
-        float4* pn = reinterpret_cast<float4*>(P.normal + 3 * pix0);
+        float4* pn = reinterpret_cast<float4*>(P.imp.normal + 3 * pix0);
         pn[0] = make_float4(o_n[0][0], o_n[0][1], o_n[0][2], o_n[1][0]);
         pn[1] = make_float4(o_n[1][1], o_n[1][2], o_n[2][0], o_n[2][1]);
         pn[2] = make_float4(o_n[2][2], o_n[3][0], o_n[3][1], o_n[3][2]);
-        *reinterpret_cast<float4*>(P.offset + pix0) = make_float4(o_off[0], o_off[1], o_off[2], o_off[3]);
-        *reinterpret_cast<float4*>(P.residual + pix0) = make_float4(o_res[0], o_res[1], o_res[2], o_res[3]);
-        *reinterpret_cast<float4*>(P.curvature + pix0) = make_float4(o_cur[0], o_cur[1], o_cur[2], o_cur[3]);
-        *reinterpret_cast<uchar4*>(P.status + pix0) = make_uchar4(o_st[0], o_st[1], o_st[2], o_st[3]);
+        *reinterpret_cast<float4*>(P.imp.offset + pix0) = make_float4(o_off[0], o_off[1], o_off[2], o_off[3]);
+        *reinterpret_cast<float4*>(P.imp.residual + pix0) = make_float4(o_res[0], o_res[1], o_res[2], o_res[3]);
+        *reinterpret_cast<float4*>(P.imp.curvature + pix0) = make_float4(o_cur[0], o_cur[1], o_cur[2], o_cur[3]);
+        *reinterpret_cast<uchar4*>(P.imp.status + pix0) = make_uchar4(o_st[0], o_st[1], o_st[2], o_st[3]);
       } else {
     #pragma unroll
         for (int j = 0; j < KSEG; ++j) {
           if (gxs + j >= P.W) break;
           const int64_t p = pix0 + j;
-          P.normal[3 * p + 0] = o_n[j][0];
-          P.normal[3 * p + 1] = o_n[j][1];
-          P.normal[3 * p + 2] = o_n[j][2];
-          P.offset[p] = o_off[j];
-          P.residual[p] = o_res[j];
-          P.curvature[p] = o_cur[j];
-          P.status[p] = o_st[j];
+          P.imp.normal[3 * p + 0] = o_n[j][0];
+          P.imp.normal[3 * p + 1] = o_n[j][1];
+          P.imp.normal[3 * p + 2] = o_n[j][2];
+          P.imp.offset[p] = o_off[j];
+          P.imp.residual[p] = o_res[j];
+          P.imp.curvature[p] = o_cur[j];
+          P.imp.status[p] = o_st[j];
         }
+      }
       }
     #endif
       }
@@ -933,7 +1035,7 @@ bool make_depth_tmap(CUtensorMap* m, const void* depth, int dtype, int64_t batch
 
 template <int VAR, bool TMA, int RT>
 cudaError_t launch_var(const KParams& P, const CUtensorMap& tmap, size_t sm, int64_t tiles, cudaStream_t s) {
-  auto kern = fit_tile_kernel<VAR, TMA, RT>;
+  auto kern = P.do_exp ? fit_tile_kernel<VAR, TMA, RT, true> : fit_tile_kernel<VAR, TMA, RT, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148, per_sm = 1;
@@ -977,8 +1079,8 @@ int32_t rf_abi_version(void) { return RF_ABI_VERSION; }
 const char* rf_last_error(void) { return g_err; }
 
 int32_t rf_launches_per_call(int32_t formulation_mask) {
-  return ((formulation_mask & RF_IMPLICIT_STANDARD) ? 1 : 0) +
-         ((formulation_mask & RF_IMPLICIT_RGBD) ? 1 : 0);
+  return ((formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) ? 1 : 0) +
+         ((formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) ? 1 : 0);
 }
 
 rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const double* delta_y,
@@ -1035,28 +1137,28 @@ rf_status rf_tables_destroy(rf_tables* t) {
 
 rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_t batch,
                         int32_t H, int32_t W, int64_t row_pitch, const uint8_t* mask,
-                        int32_t window, int32_t fmask, const rf_pixel_out* out_std,
-                        const rf_pixel_out* out_rgbd, void* stream) {
+                        int32_t window, int32_t fmask, const rf_pixel_out* outs, void* stream) {
   if (!t) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null tables%s");
   if (!depth && batch != 0) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null depth%s");
   if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM)
     return fail(RF_ERR_SHAPE, "unknown depth dtype%s %lld", "", dtype);
   if (H != t->intr.height || W != t->intr.width)
     return fail(RF_ERR_SHAPE, "depth %s%lldx%lld does not match the camera tables", "", W, H);
-  if (batch < 0 || batch > 65535) return fail(RF_ERR_ARGUMENT, "batch%s %lld out of range [0, 65535]", "", batch);
+  if (batch < 0) return fail(RF_ERR_ARGUMENT, "batch%s %lld is negative", "", batch);
   if (row_pitch < W) return fail(RF_ERR_ARGUMENT, "row_pitch%s %lld < width", "", row_pitch);
   if (window < 1 || (window & 1) == 0 || window / 2 > MAX_RADIUS)
     return fail(RF_ERR_ARGUMENT, "window%s must be odd and in [1, %lld], got %lld", "",
                 2 * MAX_RADIUS + 1, window);
-  if ((fmask & ~(RF_IMPLICIT_STANDARD | RF_IMPLICIT_RGBD)) != 0 || fmask == 0)
+  if ((fmask & ~RF_ALL_FORMULATIONS) != 0 || fmask == 0)
     return fail(RF_ERR_ARGUMENT, "formulation_mask%s %lld invalid", "", fmask);
   if (batch == 0) return RF_OK;
-  if ((fmask & RF_IMPLICIT_STANDARD) && (!out_std || !out_std->normal || !out_std->offset ||
-                                         !out_std->residual || !out_std->curvature || !out_std->status))
-    return fail(RF_ERR_ARGUMENT, "implicit-standard requested without output buffers%s");
-  if ((fmask & RF_IMPLICIT_RGBD) && (!out_rgbd || !out_rgbd->normal || !out_rgbd->offset ||
-                                     !out_rgbd->residual || !out_rgbd->curvature || !out_rgbd->status))
-    return fail(RF_ERR_ARGUMENT, "implicit-rgbd requested without output buffers%s");
+  if (!outs) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null output array%s");
+  for (int f = 0; f < RF_NUM_FORMULATIONS; ++f) {
+    if (!(fmask & (1 << f))) continue;
+    const rf_pixel_out& o = outs[f];
+    if (!o.normal || !o.offset || !o.residual || !o.curvature || !o.status)
+      return fail(RF_ERR_ARGUMENT, "formulation %s%lld requested without output buffers", "", f);
+  }
   const int r = window / 2;
   const int64_t tiles = (int64_t)((W + TW - 1) / TW) * ((H + TH - 1) / TH) * batch;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1065,10 +1167,14 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   const bool tma = getenv("RF_DISABLE_TMA") == nullptr &&
                    make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
   const int esz = dtype == RF_DEPTH_U16_MM ? 2 : 4;
+  // one launch per space: standard (implicit/explicit-standard), rgbd (implicit/explicit-rgbd)
   for (int var = 0; var < 2; ++var) {
-    const rf_pixel_out* o = var == VAR_STD ? out_std : out_rgbd;
-    if (!(fmask & (var == VAR_STD ? RF_IMPLICIT_STANDARD : RF_IMPLICIT_RGBD))) continue;
+    const int fi = var == VAR_STD ? RF_FORM_IMPLICIT_STANDARD : RF_FORM_IMPLICIT_RGBD;
+    const int fe = var == VAR_STD ? RF_FORM_EXPLICIT_STANDARD : RF_FORM_EXPLICIT_RGBD;
+    const bool di = (fmask >> fi) & 1, de = (fmask >> fe) & 1;
+    if (!di && !de) continue;
     KParams P;
+    memset(&P, 0, sizeof(P));
     P.depth = depth;
     P.mask = mask;
     P.tan_x = t->tan_x;
@@ -1082,11 +1188,10 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     P.W = W;
     P.r = r;
     P.dtype = dtype;
-    P.normal = o->normal;
-    P.offset = o->offset;
-    P.residual = o->residual;
-    P.curvature = o->curvature;
-    P.status = o->status;
+    P.do_imp = di;
+    P.do_exp = de;
+    if (di) P.imp = OutPlanes{outs[fi].normal, outs[fi].offset, outs[fi].residual, outs[fi].curvature, outs[fi].status};
+    if (de) P.exp = OutPlanes{outs[fe].normal, outs[fe].offset, outs[fe].residual, outs[fe].curvature, outs[fe].status};
     P.batch = batch;
     const size_t sm = smem_bytes(var, r, tma, esz);
     cudaError_t e;

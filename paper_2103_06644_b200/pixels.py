@@ -6,7 +6,8 @@ Mirrors the reference's fitting vocabulary (``rangefit``):
   validation; ``delta_x``/``delta_y`` lattices must be zero, see below).
 * :func:`compute_tan_maps` -- reference ``camera.py:124-135``; here it builds
   the per-camera device tables (``rf_tables_create``) once.
-* :func:`fit_pixels` -- the batched per-pixel entry the reference lacks: for
+* :func:`fit_pixels` -- the batched per-pixel entry the reference lacks (all four
+  reference formulations, ``FORMULATIONS``, ``fitting.py:45-49``): for
   every pixel it is ``fit_rect(depth, maps, Rect(max(x-r,0), max(y-r,0),
   min(x+r+1,W), min(y+r+1,H)), formulation, backend)`` (``fitting.py:757-786``)
   followed by the A18 output convention of SURVEY.md: unit normal, offset,
@@ -29,8 +30,13 @@ from . import _native as N
 
 IMPLICIT_STANDARD = "implicit-standard"
 IMPLICIT_RGBD = "implicit-rgbd"
-PIXEL_FORMULATIONS = (IMPLICIT_STANDARD, IMPLICIT_RGBD)
-_FORM_BIT = {IMPLICIT_STANDARD: N.RF_IMPLICIT_STANDARD, IMPLICIT_RGBD: N.RF_IMPLICIT_RGBD}
+EXPLICIT_STANDARD = "explicit-standard"
+EXPLICIT_RGBD = "explicit-rgbd"
+# reference FORMULATIONS order (fitting.py:49); ids index rf_fit_pixels' output array
+FORMULATIONS = (IMPLICIT_STANDARD, IMPLICIT_RGBD, EXPLICIT_STANDARD, EXPLICIT_RGBD)
+PIXEL_FORMULATIONS = (IMPLICIT_STANDARD, IMPLICIT_RGBD)  # the headline pair (north_star)
+MIN_SAMPLES = {IMPLICIT_STANDARD: 4, IMPLICIT_RGBD: 4, EXPLICIT_STANDARD: 3, EXPLICIT_RGBD: 3}
+_FORM_ID = {f: i for i, f in enumerate(FORMULATIONS)}
 
 STATUS_INPUT_VALID = N.RF_PIX_INPUT_VALID
 STATUS_FIT = N.RF_PIX_FIT
@@ -190,8 +196,8 @@ def fit_pixels(
         formulations = (formulations,)
     formulations = tuple(formulations)
     for f in formulations:
-        if f not in _FORM_BIT:
-            raise ValueError(f"unknown formulation {f!r}; expected one of {PIXEL_FORMULATIONS}")
+        if f not in _FORM_ID:
+            raise ValueError(f"unknown formulation {f!r}; expected one of {FORMULATIONS}")
     if not isinstance(depth, torch.Tensor) or not depth.is_cuda:
         raise ValueError("depth must be a CUDA tensor (the sm_100a path has no CPU fallback)")
     squeeze = depth.dim() == 2
@@ -218,17 +224,15 @@ def fit_pixels(
     if out is None:
         out = {f: PixelFits.empty(B, H, W, d.device) for f in formulations}
     fmask = 0
+    outs = (N.RfPixelOut * N.RF_NUM_FORMULATIONS)()
     for f in formulations:
-        fmask |= _FORM_BIT[f]
-    o_std = out[IMPLICIT_STANDARD]._c() if IMPLICIT_STANDARD in formulations else None
-    o_rgbd = out[IMPLICIT_RGBD]._c() if IMPLICIT_RGBD in formulations else None
+        fmask |= 1 << _FORM_ID[f]
+        outs[_FORM_ID[f]] = out[f]._c()
     if stream is None:
         stream = torch.cuda.current_stream(d.device)
     st = N.load().rf_fit_pixels(
         maps.handle, d.data_ptr(), dtype, B, H, W, d.stride(-2), mptr, int(window), fmask,
-        ctypes.byref(o_std) if o_std is not None else None,
-        ctypes.byref(o_rgbd) if o_rgbd is not None else None,
-        ctypes.c_void_p(stream.cuda_stream),
+        outs, ctypes.c_void_p(stream.cuda_stream),
     )
     N.check(st, "fit_pixels")
     if squeeze:
@@ -240,5 +244,5 @@ def fit_pixels(
 def launches_per_call(formulations=PIXEL_FORMULATIONS) -> int:
     fmask = 0
     for f in formulations:
-        fmask |= _FORM_BIT[f]
+        fmask |= 1 << _FORM_ID[f]
     return int(N.load().rf_launches_per_call(fmask))

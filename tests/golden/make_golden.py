@@ -34,13 +34,18 @@ except ImportError:  # pragma: no cover
     sys.path.insert(0, "/root/reference/pkg/src")
     import rangefit as rf
 
-from rangefit.fitting import FIT_BY_FORMULATION, accumulate_scatter_naive, gather_window_samples
+from rangefit.fitting import (FIT_BY_FORMULATION, ExplicitPlane, accumulate_scatter_naive,
+                              explicit_to_implicit, gather_window_samples)
 
-FORMS = ("implicit-rgbd", "implicit-standard")
+FORMS = ("implicit-rgbd", "implicit-standard", "explicit-rgbd", "explicit-standard")
+KEYS = {"implicit-rgbd": "rgbd", "implicit-standard": "std", "explicit-rgbd": "xrgbd",
+        "explicit-standard": "xstd"}
+SPACE = {"implicit-rgbd": "implicit-rgbd", "explicit-rgbd": "implicit-rgbd",
+         "implicit-standard": "implicit-standard", "explicit-standard": "implicit-standard"}
 
 
 def curvature(matrix: np.ndarray, formulation: str) -> float:
-    if formulation == "implicit-standard":
+    if SPACE[formulation] == "implicit-standard":
         I, k = [0, 1, 2], 3
     else:
         I, k = [0, 1, 3], 2
@@ -49,6 +54,17 @@ def curvature(matrix: np.ndarray, formulation: str) -> float:
     ev = np.linalg.eigvalsh(C3)
     tr = float(np.trace(C3))
     return float(ev.min() / tr) if tr > 0 else 0.0
+
+
+def implicit_scatter(samples: np.ndarray, formulation: str) -> np.ndarray:
+    """The space's implicit 4x4 scatter (fitting.py:364-369) without the MIN_SAMPLES
+    check, so explicit fits with n = 3 still get a curvature."""
+    u, v, z = samples[:, 0], samples[:, 1], samples[:, 2]
+    one = np.ones_like(z)
+    m = np.column_stack((u, v, z, one)) if SPACE[formulation] == "implicit-standard" \
+        else np.column_stack((u, v, one, 1.0 / z))
+    g = m.T @ m
+    return (g + g.T) * 0.5
 
 
 def run_case(name, cam, depth_img: "rf.DepthImage", stored, window, dtype):
@@ -81,17 +97,23 @@ def run_case(name, cam, depth_img: "rf.DepthImage", stored, window, dtype):
                     continue
                 res = FIT_BY_FORMULATION[form](scatter)
                 status[i] |= 2 | (4 if res.degenerate else 0)
-                coef[i] = res.plane.coefficients
-                lam[i] = res.eigenvalue
+                if isinstance(res.plane, ExplicitPlane):
+                    coef[i] = explicit_to_implicit(res.plane).coefficients   # fitting.py:729-739
+                    lam[i] = res.rms_residual ** 2 * res.n_points
+                else:
+                    coef[i] = res.plane.coefficients
+                    lam[i] = res.eigenvalue
                 rms[i] = res.rms_residual
                 npts[i] = res.n_points
-                curv[i] = curvature(scatter.matrix, form)
-                fro[i] = float(np.linalg.norm(scatter.matrix)) / res.n_points
-        key = "rgbd" if form == "implicit-rgbd" else "std"
+                # curvature (A17) and the rounding scale come from the space's implicit scatter
+                s4 = scatter.matrix if SPACE[form] == form else implicit_scatter(samples, form)
+                curv[i] = curvature(s4, form)
+                fro[i] = float(np.linalg.norm(s4)) / res.n_points
+        key = KEYS[form]
         out.update({f"{key}_coef": coef, f"{key}_lam": lam, f"{key}_rms": rms, f"{key}_curv": curv,
                     f"{key}_n": npts, f"{key}_status": status, f"{key}_scale": fro})
     np.savez_compressed(HERE / f"{name}.npz", **out)
-    print(name, "fits:", {k: int((out[f"{k}_status"] & 2).sum()) for k in ("rgbd", "std")})
+    print(name, "fits:", {k: int((out[f"{k}_status"] & 2).sum()) for k in KEYS.values()})
 
 
 def random_plane(rng, zlo, zhi):

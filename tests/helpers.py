@@ -8,7 +8,8 @@ import torch
 from oracle import oracle as O
 from oracle.compare import compare
 
-FORM_CODE = {"implicit-standard": O.STANDARD, "implicit-rgbd": O.RGBD}
+FORM_CODE = {"implicit-standard": O.STANDARD, "implicit-rgbd": O.RGBD,
+             "explicit-standard": O.EXPLICIT_STANDARD, "explicit-rgbd": O.EXPLICIT_RGBD}
 
 
 def oracle_frame(depth: torch.Tensor, cam, window: int, formulation: str, pixels=None, mask=None,
@@ -44,7 +45,7 @@ def check_frame(depth_gpu, fits, cam, window, formulation, frame=0, pixels=None,
                        formulation, pixels=pixels,
                        mask=None if mask is None else (mask[frame] if mask.dim() == 3 else mask))
     got = gpu_flat(fits, frame, pixels)
-    return compare(got, ref), got, ref
+    return compare(got, ref, explicit_fit=formulation.startswith("explicit")), got, ref
 
 
 # ------------------------------------------------------------ golden fixtures
@@ -66,7 +67,8 @@ def load_golden(name: str) -> dict:
     cam = Cam(float(z["fx"]), float(z["fy"]), float(z["cx"]), float(z["cy"]), W, H)
     g = {"depth": depth, "cam": cam, "window": int(z["window"]), "dtype": str(z["dtype"]),
          "valid": z["valid"].astype(bool) if "valid" in z.files else None}
-    for key, form in (("rgbd", "implicit-rgbd"), ("std", "implicit-standard")):
+    for key, form in (("rgbd", "implicit-rgbd"), ("std", "implicit-standard"),
+                      ("xrgbd", "explicit-rgbd"), ("xstd", "explicit-standard")):
         coef = z[f"{key}_coef"]
         nrm = np.linalg.norm(coef[:, :3], axis=1)
         with np.errstate(invalid="ignore", divide="ignore"):

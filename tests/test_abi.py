@@ -30,7 +30,7 @@ def test_library_exports_every_symbol():
     lib = N.load()
     for name in header_functions():
         assert hasattr(lib, name), name
-    assert lib.rf_abi_version() == 1
+    assert lib.rf_abi_version() == N.RF_ABI_VERSION
 
 
 def test_launch_count():
@@ -38,6 +38,9 @@ def test_launch_count():
     assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD) == 1
     assert lib.rf_launches_per_call(N.RF_IMPLICIT_RGBD) == 1
     assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_IMPLICIT_RGBD) == 2
+    # the implicit and explicit fits of one space share a launch
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_EXPLICIT_STANDARD) == 1
+    assert lib.rf_launches_per_call(15) == 2
 
 
 @pytest.mark.parametrize("fx,fy,cx,cy,w,h,msg", [
@@ -71,7 +74,7 @@ def test_tables_create_rejects_nonseparable_distortion():
 
 def test_fit_pixels_null_arguments():
     lib = N.load()
-    st = lib.rf_fit_pixels(None, None, 0, 1, 4, 4, 4, None, 5, 3, None, None, None)
+    st = lib.rf_fit_pixels(None, None, 0, 1, 4, 4, 4, None, 5, 3, None, None)
     assert st == N.RF_ERR_ARGUMENT
     with pytest.raises(ValueError):
         N.check(st, "fit_pixels")

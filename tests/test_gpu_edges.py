@@ -127,7 +127,7 @@ def test_argument_errors():
     with pytest.raises(ValueError):
         rf.fit_pixels(d.double(), maps, 5)
     with pytest.raises(ValueError):
-        rf.fit_pixels(d, maps, 5, formulations=("explicit-rgbd",))
+        rf.fit_pixels(d, maps, 5, formulations=("implicit-disparity",))
 
 
 def test_single_formulation_and_stream():

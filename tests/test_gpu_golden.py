@@ -23,11 +23,12 @@ def test_gpu_matches_reference_golden(case):
     depth = torch.from_numpy(g["depth"].astype(np.int32)).to(torch.uint16) if g["dtype"] == "u16" \
         else torch.from_numpy(g["depth"])
     mask = golden_mask(g)
-    out = rf.fit_pixels(depth.cuda(), maps, g["window"],
+    out = rf.fit_pixels(depth.cuda(), maps, g["window"], formulations=rf.FORMULATIONS,
                         mask=None if mask is None else torch.from_numpy(mask.astype(np.uint8)).cuda())
     torch.cuda.synchronize()
-    for form in rf.PIXEL_FORMULATIONS:
-        m = compare(gpu_flat(out[form], 0) if out[form].normal.dim() == 4 else gpu_flat_2d(out[form]), g[form])
+    for form in rf.FORMULATIONS:
+        m = compare(gpu_flat(out[form], 0) if out[form].normal.dim() == 4 else gpu_flat_2d(out[form]), g[form],
+                    explicit_fit=form.startswith("explicit"))
         assert m["ok"], (case, form, m)
 
 

@@ -16,7 +16,7 @@ from tests.helpers import GOLDEN_CASES, golden_mask, load_golden, oracle_frame
 
 
 @pytest.mark.parametrize("case", GOLDEN_CASES)
-@pytest.mark.parametrize("form", ["implicit-rgbd", "implicit-standard"])
+@pytest.mark.parametrize("form", ["implicit-rgbd", "implicit-standard", "explicit-rgbd", "explicit-standard"])
 def test_oracle_matches_reference_golden(case, form):
     g = load_golden(case)
     ref = g[form]
@@ -32,10 +32,14 @@ def test_oracle_matches_reference_golden(case, form):
     assert ang.max(initial=0) <= 1e-6, ang.max()
     # full canonical 4-vectors (sign convention included)
     assert np.abs(got["coef"][ok] - ref["coef"][ok]).max(initial=0) <= 1e-6
-    lam_floor = 1e-11 * ref["scale"][ok] * ref["n"][ok]  # eigenvalues at the rounding level of ||S||_F
+    # implicit: the smallest eigenvalue, rounding level ~eps*||S||_F; explicit: the residual
+    # sum of squares sum(b^2) - alpha.rhs, whose aggregated-sum cancellation floor the
+    # reference itself documents (fitting.py:592-595)
+    explicit_fit = form.startswith("explicit")
+    lam_floor = (1e-10 if explicit_fit else 1e-11) * ref["scale"][ok] * ref["n"][ok]
     lam_err = np.abs(got["lam"][ok] - ref["lam"][ok]) / np.maximum(np.abs(ref["lam"][ok]), lam_floor)
-    assert lam_err.max(initial=0) <= 1e-5
-    m = compare(got, ref)
+    assert lam_err.max(initial=0) <= (1e-4 if explicit_fit else 1e-5)
+    m = compare(got, ref, explicit_fit=explicit_fit)
     assert m["ok"], m
 
 

@@ -16,9 +16,9 @@ for name, window, W, H in cases:
     depth = scenes.render_batch(cfg, frames=1, device="cpu").cuda()
     cam = rf.CameraIntrinsics(cfg.f, cfg.f, cfg.cx, cfg.cy, cfg.width, cfg.height)
     maps = rf.compute_tan_maps(cam)
-    out = rf.fit_pixels(depth, maps, window)
+    out = rf.fit_pixels(depth, maps, window, formulations=rf.FORMULATIONS)
     torch.cuda.synchronize()
-    for form in rf.PIXEL_FORMULATIONS:
+    for form in rf.FORMULATIONS:
         m, got, ref = check_frame(depth, out[form], cam, window, form)
         print(json.dumps({"case": name, "window": window, "form": form, **m}))
         idx, ang = worst_pixels(got, ref, 3)
