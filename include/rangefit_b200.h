@@ -111,6 +111,36 @@ rf_status rf_fit_pixels(const rf_tables* tables, const void* depth, int dtype, i
                         int32_t window, int32_t formulation_mask, const rf_pixel_out* outs,
                         void* stream);
 
+/* One half-open pixel rectangle of one frame (reference Rect, integral.py:50-66). */
+typedef struct rf_rect {
+  int32_t frame, x0, y0, x1, y1;
+} rf_rect;
+
+/* rect status bits */
+#define RF_RECT_FIT 2u            /* n_points >= MIN_SAMPLES (else InsufficientSamplesError) */
+#define RF_RECT_DEGENERATE 4u     /* FitResult.degenerate                                    */
+#define RF_RECT_OUT_OF_BOUNDS 16u /* _check_rect failed (integral.py:131-133, ValueError)    */
+
+/* Per-rect result (reference FitResult, fitting.py:158-174), fp64. */
+typedef struct rf_rect_fit {
+  double coef[4];          /* canonical implicit (a,b,c,d) (ImplicitPlane / explicit_to_implicit) */
+  double explicit_coef[3]; /* ExplicitPlane.coefficients for explicit formulations, else NaN   */
+  double eigenvalue;       /* smallest scatter eigenvalue (implicit), else NaN                */
+  double rms;              /* FitResult.rms_residual                                           */
+  double curvature;        /* SURVEY.md A17 extension                                          */
+  int32_t n_points;        /* valid samples in the rect                                        */
+  int32_t status;          /* RF_RECT_* bits                                                   */
+} rf_rect_fit;
+
+/* Replaces fit_rect(depth, maps, rect, formulation, backend) (fitting.py:757-786)
+ * for a device list of rects of a [batch, H, W] depth tensor; one formulation
+ * (RF_FORM_*) per call; `out` is a device array of nrects results.  Sums are
+ * direct over each rect (the naive backend's numerics, fitting.py:339-402). */
+rf_status rf_fit_rects(const rf_tables* tables, const void* depth, int dtype, int64_t batch,
+                       int32_t height, int32_t width, int64_t row_pitch, const uint8_t* mask,
+                       const rf_rect* rects, int64_t nrects, int32_t formulation,
+                       rf_rect_fit* out, void* stream);
+
 /* Number of kernel launches rf_fit_pixels issues for a given formulation mask. */
 int32_t rf_launches_per_call(int32_t formulation_mask);
 

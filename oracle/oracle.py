@@ -69,6 +69,10 @@ def lib() -> ctypes.CDLL:
         L.rfo_jacobi_eigh.argtypes = [ctypes.c_int, dp, dp, dp]
         L.rfo_jacobi_eigh.restype = ctypes.c_int
         L.rfo_max_threads.restype = ctypes.c_int
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        L.rfo_fit_rects.argtypes = [dp, u8p, dp, dp, ctypes.c_int, ctypes.c_int, i32p, ctypes.c_int64,
+                                    ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, i32p, i32p]
+        L.rfo_fit_rects.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -188,3 +192,28 @@ def jacobi_eigh(matrix):
     rc = lib().rfo_jacobi_eigh(n, _ptr(m, ctypes.c_double), _ptr(vals, ctypes.c_double),
                                _ptr(vecs, ctypes.c_double))
     return vals, vecs, rc == 0
+
+
+def fit_rects(values, valid, tan_x, tan_y, rects, formulation, backend=NAIVE):
+    """fit_rect for a list of (x0, y0, x1, y1) rects of one frame (reference fitting.py:757-786).
+    Returns coef (R,4) canonical implicit, lam, rms, curvature, n (R,), status (R,) with bit1
+    fitted, bit2 degenerate, bit4 out of bounds."""
+    if isinstance(formulation, str):
+        formulation = FORMULATION_CODES[formulation]
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    valid = np.ascontiguousarray(valid, dtype=np.uint8)
+    H, W = values.shape
+    tan_x = np.ascontiguousarray(np.broadcast_to(tan_x, values.shape), dtype=np.float64)
+    tan_y = np.ascontiguousarray(np.broadcast_to(tan_y, values.shape), dtype=np.float64)
+    r = np.ascontiguousarray(np.asarray(rects, dtype=np.int32).reshape(-1, 4))
+    R = r.shape[0]
+    out = {"coef": np.empty((R, 4)), "lam": np.empty(R), "rms": np.empty(R), "curvature": np.empty(R),
+           "n": np.empty(R, np.int32), "status": np.empty(R, np.int32)}
+    rc = lib().rfo_fit_rects(
+        _ptr(values, ctypes.c_double), _ptr(valid, ctypes.c_uint8), _ptr(tan_x, ctypes.c_double),
+        _ptr(tan_y, ctypes.c_double), H, W, _ptr(r, ctypes.c_int32), R, int(formulation), int(backend),
+        _ptr(out["coef"], ctypes.c_double), _ptr(out["lam"], ctypes.c_double), _ptr(out["rms"], ctypes.c_double),
+        _ptr(out["curvature"], ctypes.c_double), _ptr(out["n"], ctypes.c_int32), _ptr(out["status"], ctypes.c_int32))
+    if rc != 0:
+        raise ValueError(f"oracle rfo_fit_rects failed with code {rc}")
+    return out

@@ -547,6 +547,50 @@ int rfo_fit_pixels(const double* depth, const uint8_t* valid, const double* tan_
   return 0;
 }
 
+/*
+ * Arbitrary rects: fit_rect(depth, maps, Rect(x0, y0, x1, y1), formulation, backend)
+ * (fitting.py:757-786) for each of nrects rects (int32 x0, y0, x1, y1 each) of one frame.
+ * status: bit1 fitted, bit2 degenerate, bit4 out of bounds (_check_rect raises).
+ */
+int rfo_fit_rects(const double* depth, const uint8_t* valid, const double* tan_x,
+                  const double* tan_y, int H, int W, const int32_t* rects, int64_t nrects,
+                  int formulation, int backend, double* coef, double* lam, double* rms,
+                  double* curvature, int32_t* npts, int32_t* status) {
+  if (formulation < RFO_STANDARD || formulation > RFO_EXPLICIT_RGBD) return -1;
+  const int space = RFO_SPACE(formulation);
+  const int explicit_fit = formulation >= RFO_EXPLICIT_STANDARD;
+  const int min_samples = explicit_fit ? 3 : 4;
+  sat_stack st;
+  st.t = NULL;
+  if (backend == RFO_INTEGRAL && build_stack(depth, valid, tan_x, tan_y, H, W, space, &st) != 0)
+    return -1;
+  for (int64_t k = 0; k < nrects; ++k) {
+    const int x0 = rects[4 * k], y0 = rects[4 * k + 1], x1 = rects[4 * k + 2], y1 = rects[4 * k + 3];
+    for (int i = 0; i < 4; ++i) coef[4 * k + i] = NAN;
+    lam[k] = rms[k] = curvature[k] = NAN;
+    npts[k] = 0;
+    if (!(0 <= x0 && x0 <= x1 && x1 <= W && 0 <= y0 && y0 <= y1 && y1 <= H)) {
+      status[k] = 16;
+      continue;
+    }
+    double S[16];
+    int n = backend == RFO_INTEGRAL ? integral_scatter(&st, x0, y0, x1, y1, space, min_samples, S)
+                                    : naive_scatter(depth, valid, tan_x, tan_y, W, x0, y0, x1, y1, space, S);
+    npts[k] = n;
+    if (n < min_samples) { status[k] = 0; continue; }
+    fit_out o;
+    if (explicit_fit) fit_explicit(S, n, space, &o);
+    else fit_scatter(S, n, space, &o);
+    status[k] = 2 | (o.degenerate ? 4 : 0) | (o.failed ? 8 : 0);
+    memcpy(coef + 4 * k, o.coef, sizeof(o.coef));
+    lam[k] = o.lam;
+    rms[k] = o.rms;
+    curvature[k] = o.curvature;
+  }
+  free(st.t);
+  return 0;
+}
+
 /* Single-window fit on a caller-supplied 4x4 scatter (for unit tests of the
  * restated Jacobi / canonicalisation).  Returns 0, or -1 if not converged. */
 int rfo_fit_scatter(const double* S, int n, int formulation, double* coef, double* lam,

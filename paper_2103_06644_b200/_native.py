@@ -44,6 +44,7 @@ EXPORTED_SYMBOLS = (
     "rf_tables_create",
     "rf_tables_destroy",
     "rf_fit_pixels",
+    "rf_fit_rects",
     "rf_launches_per_call",
     "rf_last_error",
     "rf_abi_version",
@@ -98,6 +99,11 @@ def load() -> ctypes.CDLL:
         ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(RfPixelOut), vp,
     ]
     L.rf_fit_pixels.restype = ctypes.c_int
+    L.rf_fit_rects.argtypes = [
+        vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, vp,
+        vp, ctypes.c_int64, ctypes.c_int32, vp, vp,
+    ]
+    L.rf_fit_rects.restype = ctypes.c_int
     L.rf_launches_per_call.argtypes = [ctypes.c_int32]
     L.rf_launches_per_call.restype = ctypes.c_int32
     L.rf_last_error.argtypes = []

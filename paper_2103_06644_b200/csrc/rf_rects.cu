@@ -1,0 +1,286 @@
+// rf_rects.cu -- batched arbitrary-rectangle fits ("K5"):
+// the reference's per-window entry fit_rect(depth, maps, rect, formulation,
+// backend) (fitting.py:757-786) evaluated for a list of rects on the device.
+//
+// One CTA per rect.  Threads stride over the rect's pixels (row-major, so warps
+// read contiguous runs of a row), accumulate the rect's raw moments in local
+// coordinates about the rect centre (exact integer geometry, fp64 depth moments
+// -- the naive backend's direct sums, fitting.py:339-402, never an image-global
+// summed-area table), reduce them across the CTA, and thread 0 solves with the
+// same device code as the per-pixel kernels (rf_solve.cuh).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/rangefit_b200.h"
+#include "rf_internal.h"
+#include "rf_solve.cuh"
+
+namespace {
+using namespace rf_dev;
+
+constexpr int RT_THREADS = 128;
+
+struct RectParams {
+  const void* depth;
+  const uint8_t* mask;
+  const double* tan_x;
+  const double* tan_y;
+  double ifx, ify;
+  int64_t row_pitch, frame_stride, out_frame, batch;
+  int H, W, dtype, formulation;
+  const rf_rect* rects;
+  int64_t nrects;
+  rf_rect_fit* out;
+};
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < RT_THREADS / 32; ++w) t += red[w];
+  return t;  // valid on thread 0
+}
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  long long t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < RT_THREADS / 32; ++w) t += red[w];
+  return t;
+}
+
+// canonicalize_implicit (fitting.py:76-94) in fp64
+__device__ void canonical4(double a, double b, double c, double d, double* out) {
+  const double nrm = sqrt(a * a + b * b + c * c + d * d);
+  double u[4] = {a / nrm, b / nrm, c / nrm, d / nrm};
+  double sign = 1.0;
+  const int order[4] = {2, 1, 0, 3};
+  for (int k = 0; k < 4; ++k) {
+    if (fabs(u[order[k]]) > 1e-9) {
+      sign = u[order[k]] > 0.0 ? 1.0 : -1.0;
+      break;
+    }
+  }
+  for (int k = 0; k < 4; ++k) out[k] = sign * u[k];
+}
+
+__global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams P) {
+  __shared__ double redd[RT_THREADS / 32];
+  __shared__ long long redl[RT_THREADS / 32];
+  const int64_t ri = blockIdx.x;
+  if (ri >= P.nrects) return;
+  const rf_rect R = P.rects[ri];
+  rf_rect_fit* o = P.out + ri;
+  const bool space_std = P.formulation == RF_FORM_IMPLICIT_STANDARD || P.formulation == RF_FORM_EXPLICIT_STANDARD;
+  const bool explicit_fit = P.formulation >= RF_FORM_EXPLICIT_STANDARD;
+  // _check_rect (integral.py:131-133): 0 <= x0 <= x1 <= W, 0 <= y0 <= y1 <= H
+  if (!(R.frame >= 0 && R.frame < P.batch && 0 <= R.x0 && R.x0 <= R.x1 && R.x1 <= P.W && 0 <= R.y0 &&
+        R.y0 <= R.y1 && R.y1 <= P.H)) {
+    if (threadIdx.x == 0) {
+      memset(o, 0, sizeof(*o));
+      o->status = RF_RECT_OUT_OF_BOUNDS;
+      o->n_points = 0;
+    }
+    return;
+  }
+  const int rw = R.x1 - R.x0, rh = R.y1 - R.y0;
+  const int ox = R.x0 + rw / 2, oy = R.y0 + rh / 2;  // local origin near the centre
+  const int64_t area = (int64_t)rw * rh;
+  // moments: q = (dx, dy, w) disparity form / (dx Z, dy Z, Z) standard
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0, s7 = 0, s8 = 0;
+  long long n = 0, gx = 0, gy = 0, gxx = 0, gxy = 0, gyy = 0;
+  for (int64_t e = threadIdx.x; e < area; e += RT_THREADS) {
+    const int yy = (int)(e / rw), xx = (int)(e - (int64_t)yy * rw);
+    const int y = R.y0 + yy, x = R.x0 + xx;
+    const int64_t off = (int64_t)R.frame * P.frame_stride + (int64_t)y * P.row_pitch + x;
+    double z;
+    bool valid;
+    if (P.dtype == RF_DEPTH_U16_MM) {
+      const unsigned short mm = __ldg(reinterpret_cast<const unsigned short*>(P.depth) + off);
+      valid = mm > 0;
+      z = __ddiv_rn((double)mm, 1000.0);
+    } else {
+      const float zf = __ldg(reinterpret_cast<const float*>(P.depth) + off);
+      valid = (zf > 0.0f) && (zf <= 3.402823466e38f);
+      z = (double)zf;
+    }
+    if (P.mask) valid = valid && __ldg(P.mask + (int64_t)R.frame * P.out_frame + (int64_t)y * P.W + x) != 0;
+    if (!valid) continue;
+    const int dx = x - ox, dy = y - oy;
+    const double fdx = (double)dx, fdy = (double)dy;
+    if (!space_std) {
+      const double w = rcp_fast(z);
+      s0 += w;
+      s1 = fma(w, w, s1);
+      s2 = fma(fdx, w, s2);
+      s3 = fma(fdy, w, s3);
+      n += 1;
+      gx += dx;
+      gy += dy;
+      gxx += (long long)dx * dx;
+      gxy += (long long)dx * dy;
+      gyy += (long long)dy * dy;
+    } else {
+      const double z2 = z * z, xz = fdx * z, yz = fdy * z;
+      s0 += z;                   // S3
+      s1 += z2;                  // S33
+      s2 += xz;                  // S1
+      s3 += yz;                  // S2
+      s4 = fma(xz, xz, s4);      // S11
+      s5 = fma(xz, yz, s5);      // S12
+      s6 = fma(yz, yz, s6);      // S22
+      s7 = fma(fdx, z2, s7);     // S13
+      s8 = fma(fdy, z2, s8);     // S23
+      n += 1;
+    }
+  }
+  s0 = block_sum(s0, redd);
+  s1 = block_sum(s1, redd);
+  s2 = block_sum(s2, redd);
+  s3 = block_sum(s3, redd);
+  if (space_std) {
+    s4 = block_sum(s4, redd);
+    s5 = block_sum(s5, redd);
+    s6 = block_sum(s6, redd);
+    s7 = block_sum(s7, redd);
+    s8 = block_sum(s8, redd);
+  }
+  n = block_sum_ll(n, redl);
+  if (!space_std) {
+    gx = block_sum_ll(gx, redl);
+    gy = block_sum_ll(gy, redl);
+    gxx = block_sum_ll(gxx, redl);
+    gxy = block_sum_ll(gxy, redl);
+    gyy = block_sum_ll(gyy, redl);
+  }
+  if (threadIdx.x != 0) return;
+
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  rf_rect_fit res;
+  for (int k = 0; k < 4; ++k) res.coef[k] = qnan;
+  for (int k = 0; k < 3; ++k) res.explicit_coef[k] = qnan;
+  res.eigenvalue = res.rms = res.curvature = qnan;
+  res.n_points = (int32_t)n;
+  res.status = 0;
+  const int min_samples = explicit_fit ? 3 : 4;  // MIN_SAMPLES fitting.py:55-60
+  if (n >= min_samples) {
+    const double txo = P.tan_x[ox], tyo = P.tan_y[oy];
+    const double ifx = P.ifx, ify = P.ify;
+    const double nd = (double)n, invn = 1.0 / nd;
+    Sym3 C;
+    double mu0, mu1, mu2;
+    if (!space_std) {
+      // geometry moments about the rect centre (|gx|, |gy| small relative to gxx, gyy)
+      const double fgx = (double)gx, fgy = (double)gy;
+      const double cq00 = fma(-fgx, fgx * invn, (double)gxx);
+      const double cq01 = fma(-fgx, fgy * invn, (double)gxy);
+      const double cq11 = fma(-fgy, fgy * invn, (double)gyy);
+      const double mw = s0 * invn;
+      C.c00 = cq00 * (ifx * ifx);
+      C.c01 = cq01 * (ifx * ify);
+      C.c11 = cq11 * (ify * ify);
+      C.c02 = fma(-(double)gx, mw, s2) * ifx;
+      C.c12 = fma(-(double)gy, mw, s3) * ify;
+      C.c22 = fma(-s0, mw, s1);
+      mu0 = fma((double)gx * invn, ifx, txo);
+      mu1 = fma((double)gy * invn, ify, tyo);
+      mu2 = mw;
+    } else {
+      const double q0 = s2 * invn, q1 = s3 * invn, q2 = s0 * invn;
+      const double k00 = fma(-s2, q0, s4), k01 = fma(-s2, q1, s5), k02 = fma(-s2, q2, s7);
+      const double k11 = fma(-s3, q1, s6), k12 = fma(-s3, q2, s8), k22 = fma(-s0, q2, s1);
+      const double r00 = fma(ifx, k00, txo * k02), r01 = fma(ifx, k01, txo * k12), r02 = fma(ifx, k02, txo * k22);
+      const double r11 = fma(ify, k11, tyo * k12), r12 = fma(ify, k12, tyo * k22);
+      C.c00 = fma(ifx, r00, txo * r02);
+      C.c01 = fma(ify, r01, tyo * r02);
+      C.c02 = r02;
+      C.c11 = fma(ify, r11, tyo * r12);
+      C.c12 = r12;
+      C.c22 = k22;
+      mu0 = fma(ifx, q0, txo * q2);
+      mu1 = fma(ify, q1, tyo * q2);
+      mu2 = q2;
+    }
+    if (!explicit_fit) {
+      WindowFit f;
+      solve_window(C, mu0, mu1, mu2, nd, f);
+      if (space_std) canonical4(f.u0, f.u1, f.u2, f.s, res.coef);
+      else canonical4(f.u0, f.u1, f.s, f.u2, res.coef);
+      res.eigenvalue = f.lam;
+      res.rms = sqrt(fmax(f.lam, 0.0) / nd);
+      res.curvature = f.kappa;
+      res.status = RF_RECT_FIT | (f.degenerate ? RF_RECT_DEGENERATE : 0);
+    } else {
+      ExplicitFit e;
+      explicit_solve(C, mu0, mu1, mu2, nd, e);
+      res.explicit_coef[0] = e.a;
+      res.explicit_coef[1] = e.b;
+      res.explicit_coef[2] = e.c;
+      // explicit_to_implicit (fitting.py:729-739)
+      if (space_std) canonical4(e.a, e.b, -1.0, e.c, res.coef);
+      else canonical4(e.a, e.b, e.c, -1.0, res.coef);
+      res.rms = sqrt(fmax(e.ss, 0.0) / nd);
+      res.curvature = curvature_only(C);
+      res.status = RF_RECT_FIT | (e.degenerate ? RF_RECT_DEGENERATE : 0);
+    }
+  }
+  *o = res;
+}
+
+}  // namespace
+
+extern "C" {
+
+rf_status rf_fit_rects(const rf_tables* t, const void* depth, int dtype, int64_t batch, int32_t H,
+                       int32_t W, int64_t row_pitch, const uint8_t* mask, const rf_rect* rects,
+                       int64_t nrects, int32_t formulation, rf_rect_fit* out, void* stream) {
+  if (!t) return rf_set_error(RF_ERR_ARGUMENT, "rf_fit_rects: null tables");
+  if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM)
+    return rf_set_error(RF_ERR_SHAPE, "rf_fit_rects: unknown depth dtype");
+  if (H != t->intr.height || W != t->intr.width)
+    return rf_set_error(RF_ERR_SHAPE, "rf_fit_rects: depth size does not match the camera tables");
+  if (formulation < 0 || formulation >= RF_NUM_FORMULATIONS)
+    return rf_set_error(RF_ERR_ARGUMENT, "rf_fit_rects: unknown formulation");
+  if (batch < 0 || nrects < 0 || row_pitch < W)
+    return rf_set_error(RF_ERR_ARGUMENT, "rf_fit_rects: bad batch / rect count / row pitch");
+  if (nrects == 0) return RF_OK;
+  if (!depth || !rects || !out || nrects > 0x7fffffff)
+    return rf_set_error(RF_ERR_ARGUMENT, "rf_fit_rects: null depth / rects / out");
+  RectParams P;
+  P.depth = depth;
+  P.mask = mask;
+  P.tan_x = t->tan_x;
+  P.tan_y = t->tan_y;
+  P.ifx = 1.0 / t->intr.fx;
+  P.ify = 1.0 / t->intr.fy;
+  P.row_pitch = row_pitch;
+  P.frame_stride = row_pitch * H;
+  P.out_frame = (int64_t)H * W;
+  P.batch = batch;
+  P.H = H;
+  P.W = W;
+  P.dtype = dtype;
+  P.formulation = formulation;
+  P.rects = rects;
+  P.nrects = nrects;
+  P.out = out;
+  fit_rects_kernel<<<(unsigned)nrects, RT_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(P);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return rf_set_error(RF_ERR_CUDA, cudaGetErrorString(e));
+  return RF_OK;
+}
+
+}  // extern "C"

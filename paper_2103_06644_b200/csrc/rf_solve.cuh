@@ -1,0 +1,397 @@
+// rf_solve.cuh -- per-window solve shared by the per-pixel (rf_fit.cu) and the
+// per-rect (rf_rects.cu) kernels: fp32/fp64 helpers, the smallest eigenpair of
+// the uncentred implicit scatter, the explicit fits, curvature and the canonical
+// output form.  See DESIGN.md section 4.4 for the derivation.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+namespace rf_dev {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double rcp_approx(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+// reciprocal to ~1 ulp: approximate seed + two Newton steps (no IEEE fixup)
+__device__ __forceinline__ double rcp_fast(double x) {
+  double y = rcp_approx(x);
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+__device__ __forceinline__ float frcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float fsqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// acos on [-1, 1], |error| <= 2e-8 rad (Abramowitz & Stegun 4.4.46)
+__device__ __forceinline__ float facos(float x) {
+  const float ax = fabsf(x);
+  float p = fmaf(ax, -0.0012624911f, 0.0066700901f);
+  p = fmaf(ax, p, -0.0170881256f);
+  p = fmaf(ax, p, 0.0308918810f);
+  p = fmaf(ax, p, -0.0501743046f);
+  p = fmaf(ax, p, 0.0889789874f);
+  p = fmaf(ax, p, -0.2145988016f);
+  p = fmaf(ax, p, 1.5707963050f);
+  const float r = fsqrt(fmaxf(1.0f - ax, 0.0f)) * p;
+  return x < 0.0f ? 3.14159265358979f - r : r;
+}
+
+// Roots l1 <= l2 <= l3 of l^3 - a2 l^2 + a1 l - a0 (three real roots), fp32
+// seeds for the fp64 refinement.  l3 by the trigonometric formula, l1/l2 by
+// deflation (product a0/l3, sum (a1 - l1 l2)/l3) so that small roots keep
+// their relative accuracy.  Fast approximate intrinsics throughout (~1e-6).
+__device__ __forceinline__ void trig_cubic(float a2, float a1, float a0, float& l1, float& l2,
+                                           float& l3) {
+  const float q = a2 * (1.0f / 3.0f);
+  const float p = fmaxf(fmaf(q, q, -a1 * (1.0f / 3.0f)), 1e-37f);
+  const float isp = rsqrtf(p);
+  const float sp = p * isp;
+  const float h = fmaf(q * q - 0.5f * a1, q, 0.5f * a0);
+  const float c = fminf(fmaxf(h * isp * isp * isp, -1.0f), 1.0f);
+  const float phi = facos(c) * (1.0f / 3.0f);
+  l3 = fmaxf(fmaf(2.0f * sp, __cosf(phi), q), 1e-37f);
+  const float il3 = frcp(l3);
+  const float P = a0 * il3;
+  const float S = (a1 - P) * il3;
+  const float sd = S + fsqrt(fmaxf(fmaf(S, S, -4.0f * P), 0.0f));
+  l2 = 0.5f * sd;
+  l1 = sd > 0.0f ? 2.0f * P * frcp(sd) : 0.0f;
+}
+
+struct Sym3 {
+  double c00, c01, c02, c11, c12, c22;
+};
+
+struct WindowFit {
+  double lam;       // smallest eigenvalue of the 4x4 scatter
+  double u0, u1, u2;  // coefficients of the three non-constant monomials
+  double s;         // coefficient of the constant monomial
+  float kappa;      // curvature
+  bool degenerate;
+};
+
+// Curvature lam_min(C)/tr(C) from the invariants t = tr C,
+// c1 = sum of principal 2x2 minors, det = det C and the fp32 roots k1<=k2<=k3 of
+// l^3 - t l^2 + c1 l - det: fp64 Newton from below, or -- when the bottom pair is
+// close -- Newton from above on lam_max and deflation.
+__device__ __forceinline__ float curvature_from(double t, double c1, double det, float ft, float k1,
+                                                float k2, float k3) {
+  {
+    double lk;
+    const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
+    if (!top) {
+      // Newton from below lam_min (monotone).  With a well separated bottom pair
+      // (relative gap > 20%) the fp32 seed (deflated, ~2e-6 relative) already meets
+      // the 1e-4 curvature tolerance with margin; otherwise polish in fp64.
+      double l = (double)k1;
+      if ((k2 - k1) < 0.2f * k2) {
+        l *= (1.0 - 1e-5);
+        auto newton = [&](double x) {
+          const double P = fma(fma(t - x, x, -c1), x, det);
+          const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+          return P * rcp_approx(dP);
+        };
+        l -= newton(l);
+        l -= newton(l);
+        if ((k2 - k1) < 0.05f * k2) {  // close bottom pair (rare): iterate to convergence
+          for (int it = 0; it < 64; ++it) {
+            const double step = newton(l);
+            l -= step;
+            if (!(fabs(step) > 1e-10 * l)) break;
+          }
+        }
+      }
+      lk = l;
+    } else {
+      // near-tie at the bottom: Newton from above lam_max (well separated here),
+      // then deflate; lam_max only needs ~1e-10 for a 1e-5 curvature
+      double l = fmin((double)k3 * (1.0 + 1e-5), t);
+      auto newton = [&](double x) {
+        const double P = fma(fma(t - x, x, -c1), x, det);
+        const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+        return P * rcp_approx(dP);
+      };
+      l -= newton(l);
+      l -= newton(l);
+      if ((k3 - k2) < 0.05f * k3) {  // top pair close too (rare): iterate to convergence
+        for (int it = 0; it < 62; ++it) {
+          const double step = newton(l);
+          l -= step;
+          if (!(fabs(step) > 1e-12 * l)) break;
+        }
+      }
+      const double S = t - l;
+      const double Pp = det * rcp_fast(l);
+      const double den = S + (double)fsqrt((float)fmax(fma(S, S, -4.0 * Pp), 0.0));
+      lk = den > 0.0 ? 2.0 * Pp * rcp_fast(den) : 0.0;
+    }
+    return t > 0.0 ? (float)lk * frcp(ft) : 0.0f;
+  }
+}
+
+// curvature when no implicit solve runs (explicit fits only)
+__device__ __forceinline__ float curvature_only(const Sym3& C) {
+  const double A00 = C.c11 * C.c22 - C.c12 * C.c12;
+  const double A11 = C.c00 * C.c22 - C.c02 * C.c02;
+  const double A22 = C.c00 * C.c11 - C.c01 * C.c01;
+  const double A01 = C.c02 * C.c12 - C.c01 * C.c22;
+  const double A02 = C.c01 * C.c12 - C.c02 * C.c11;
+  const double t = C.c00 + C.c11 + C.c22;
+  const double c1 = A00 + A11 + A22;
+  const double det = C.c00 * A00 + C.c01 * A01 + C.c02 * A02;
+  float k1, k2, k3;
+  const float ft = (float)t;
+  trig_cubic(ft, (float)c1, (float)det, k1, k2, k3);
+  return curvature_from(t, c1, det, ft, k1, k2, k3);
+}
+
+// Explicit fits (fitting.py:582-621) on the centred moments of the space's monomials
+// (m0, m1, m2) = (X, Y, Z) standard or (tx, ty, 1/Z) rgbd: the target m2 regressed on
+// (m0, m1, 1).  Solved centred ([a b] from the 2x2 covariance, c = mu2 - a mu0 - b mu1),
+// which equals the reference's uncentred normal equations; the residual sum of squares
+// C22 - [a b].[C02 C12] equals its sum(b^2) - alpha.rhs.  degenerate replays the
+// reference's Cholesky pivot test (cholesky3, fitting.py:264-293) on the uncentred
+// matrix [[S00, S01, S0], [S01, S11, S1], [S0, S1, n]].
+struct ExplicitFit {
+  double a, b, c, ss;
+  bool degenerate;
+};
+__device__ __forceinline__ void explicit_solve(const Sym3& C, double m0, double m1, double m2,
+                                               double n, ExplicitFit& out) {
+  const double det2 = fma(C.c00, C.c11, -C.c01 * C.c01);
+  const double idet = det2 > 0.0 ? rcp_fast(det2) : 0.0;
+  out.a = fma(C.c11, C.c02, -C.c01 * C.c12) * idet;
+  out.b = fma(C.c00, C.c12, -C.c01 * C.c02) * idet;
+  out.c = m2 - out.a * m0 - out.b * m1;
+  out.ss = C.c22 - (out.a * C.c02 + out.b * C.c12);
+  // uncentred matrix and its Cholesky pivots
+  const double M00 = fma(n * m0, m0, C.c00), M01 = fma(n * m0, m1, C.c01), M11 = fma(n * m1, m1, C.c11);
+  const double M02 = n * m0, M12 = n * m1;
+  const double trace = M00 + M11 + n;
+  const double fl = 1e-12 * trace;
+  const double p0 = M00;
+  const double l10 = M01 * rcp_fast(M00);
+  const double p1 = fma(-l10, M01, M11);
+  // p2 = n - [M02 M12] M2^-1 [M02 M12]^T = n / (1 + n mu^T C2^-1 mu)
+  const double q = (m0 * fma(C.c11, m0, -C.c01 * m1) + m1 * fma(C.c00, m1, -C.c01 * m0)) * idet;
+  const double p2 = det2 > 0.0 ? n * rcp_fast(fma(n, q, 1.0)) : 0.0;
+  (void)M02;
+  (void)M12;
+  out.degenerate = !(trace > 0.0) || p0 <= fl || p1 <= fl || p2 <= fl;
+}
+
+// Smallest eigenpair of S = [[C + n mu mu^T, n mu], [n mu^T, n]] (the
+// uncentred scatter of [m0, m1, m2, 1], fitting.py:339-381) through the
+// Schur complement on the constant monomial: C u = lam (I + beta mu mu^T) u,
+// beta = n/(n - lam), s = -beta mu.u.  det(S - l I) is the quartic
+//   l^4 - q3 l^3 + q2 l^2 - q1 l + q0   with
+//   q3 = n + t + n nu, q2 = n t + c1 + n (t nu - mu.C.mu),
+//   q1 = n c1 + det C + n mu.adj(C).mu,  q0 = n det C.
+// lam1 is found by fp64 Newton from a lower bound (fp32 trigonometric seeds
+// of the beta=1 cubic), or -- when lam1 ~ lam2 (near-tie) -- by exact
+// backward deflation of the quartic's two largest roots and the remaining
+// quadratic.  The eigenvector is the
+// dominant column of adj(C - lam (I + beta mu mu^T)).
+// Curvature lam_min(C)/tr(C) uses the same seeds/Newton/
+// deflation on det(C - l I).
+__device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1, double m2,
+                                             double n, WindowFit& out) {
+  const double c00 = C.c00, c01 = C.c01, c02 = C.c02, c11 = C.c11, c12 = C.c12, c22 = C.c22;
+  const double A00 = c11 * c22 - c12 * c12;
+  const double A11 = c00 * c22 - c02 * c02;
+  const double A22 = c00 * c11 - c01 * c01;
+  const double A01 = c02 * c12 - c01 * c22;
+  const double A02 = c01 * c12 - c02 * c11;
+  const double A12 = c01 * c02 - c00 * c12;
+  const double t = c00 + c11 + c22;
+  const double c1 = A00 + A11 + A22;
+  const double det = c00 * A00 + c01 * A01 + c02 * A02;
+  const double nu = m0 * m0 + m1 * m1 + m2 * m2;
+  const double Cm0 = c00 * m0 + c01 * m1 + c02 * m2;
+  const double Cm1 = c01 * m0 + c11 * m1 + c12 * m2;
+  const double Cm2 = c02 * m0 + c12 * m1 + c22 * m2;
+  const double mm = m0 * Cm0 + m1 * Cm1 + m2 * Cm2;
+  const double Am0 = A00 * m0 + A01 * m1 + A02 * m2;
+  const double Am1 = A01 * m0 + A11 * m1 + A12 * m2;
+  const double Am2 = A02 * m0 + A12 * m1 + A22 * m2;
+  const double aa = m0 * Am0 + m1 * Am1 + m2 * Am2;
+  const double q3 = n + t + n * nu;
+  const double q2 = fma(n, t, c1) + n * (t * nu - mm);
+  const double q1 = fma(n, c1, det) + n * aa;
+  const double q0 = n * det;
+
+  // fp32 seeds: roots g1 <= g2 <= g3 of the pencil's cubic at beta = 1,
+  //   (1 + nu) l^3 - (t + t nu - mu.C.mu) l^2 + (c1 + mu.adj(C).mu) l - det C.
+  // lam1(beta) decreases with beta and d lam/d beta >= -lam/beta, so with
+  // beta(lam1) <= n/(n - g1):  g1 (1 - g1/n) <= lam1 <= g1.
+  float g1, g2, g3, k1, k2, k3;
+  const float ft = (float)t, fc1 = (float)c1, fdet = (float)det, fnu = (float)nu, fn = (float)n;
+  {
+    const float inv = frcp(1.0f + fnu);
+    trig_cubic((float)(t + t * nu - mm) * inv, (float)(c1 + aa) * inv, fdet * inv, g1, g2, g3);
+    trig_cubic(ft, fc1, fdet, k1, k2, k3);
+  }
+  const float grel = g1 * frcp(fn);
+
+  double lam, lam2;
+  const bool tie = (g2 - g1) < 0.05f * g2;
+  if (!tie) {
+    // (A) Newton on the quartic from the lower bound: monotone convergence,
+    // stop once the step is below 1e-9 relative (the remaining error is then
+    // ~step^2/gap).  Three steps in the common case; pathological windows
+    // (lam/n not small) take longer.
+    double l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
+    auto newton = [&](double x) {
+      const double x2 = x * x;
+      const double G = fma(fma(x - q3, x, q2), x2, fma(-q1, x, q0));
+      const double dG = fma(fma(fma(4.0, x, -3.0 * q3), x, 2.0 * q2), x, -q1);
+      return G * rcp_approx(dG);
+    };
+    // quadratic convergence, e_{k+1} ~ e_k^2 / (relative gap >= 5%): from
+    // e0 <= 1e-4 + lam1/n two steps leave < 1e-11 when lam1/n <= 1e-4, three when <= 1e-3
+    l -= newton(l);
+    l -= newton(l);
+    if (grel > 1e-4f) l -= newton(l);
+    if (grel > 1e-3f) {  // large residual windows (rare): iterate to convergence
+      for (int it = 0; it < 64; ++it) {
+        const double step = newton(l);
+        l -= step;
+        if (!(fabs(step) > 1e-13 * l)) break;
+      }
+    }
+    lam = l;
+    lam2 = (double)g2;
+  } else {
+    // (B) near-tie lam1 ~ lam2: exact deflation of the quartic.  lam4 (the
+    // largest root, ~n(1+nu)) and then lam3 are found by Newton from above
+    // (upper bounds q3 and lam1+lam2+lam3), each divided out by backward
+    // deflation (stable for the largest root); the quadratic left over has
+    // roots lam1 <= lam2, solved in the cancellation-free form.
+    double l4 = q3;
+    for (int it = 0; it < 64; ++it) {
+      const double G = fma(fma(fma(l4 - q3, l4, q2), l4, -q1), l4, q0);
+      const double dG = fma(fma(fma(4.0, l4, -3.0 * q3), l4, 2.0 * q2), l4, -q1);
+      const double step = G * rcp_approx(dG);
+      l4 -= step;
+      if (!(fabs(step) > 1e-15 * l4)) break;
+    }
+    const double i4 = rcp_fast(l4);
+    const double h0 = -q0 * i4;             // -lam1 lam2 lam3
+    const double h1 = (q1 + h0) * i4;       // lam1 lam2 + lam1 lam3 + lam2 lam3
+    const double h2 = (h1 - q2) * i4;       // -(lam1 + lam2 + lam3)
+    double l3 = -h2;
+    for (int it = 0; it < 64; ++it) {
+      const double H = fma(fma(l3 + h2, l3, h1), l3, h0);
+      const double dH = fma(fma(3.0, l3, 2.0 * h2), l3, h1);
+      const double step = H * rcp_approx(dH);
+      l3 -= step;
+      if (!(fabs(step) > 1e-15 * l3)) break;
+    }
+    const double i3 = rcp_fast(l3);
+    const double e0 = -h0 * i3;             // lam1 lam2
+    const double e1 = (e0 - h1) * i3;       // -(lam1 + lam2)
+    const double disc = (double)fsqrt((float)fmax(fma(e1, e1, -4.0 * e0), 0.0));
+    const double den = disc - e1;           // 2 lam2
+    lam = den > 0.0 ? 2.0 * e0 * rcp_fast(den) : 0.0;
+    lam2 = 0.5 * den;
+  }
+
+  // eigenvector: dominant column of adj(C - lam B), B = I + beta mu mu^T
+  const double beta = n * rcp_fast(n - lam);
+  const double gam = lam * beta;
+  const double E00 = c00 - lam - gam * m0 * m0;
+  const double E11 = c11 - lam - gam * m1 * m1;
+  const double E22 = c22 - lam - gam * m2 * m2;
+  const double E01 = c01 - gam * m0 * m1;
+  const double E02 = c02 - gam * m0 * m2;
+  const double E12 = c12 - gam * m1 * m2;
+  const double B00 = E11 * E22 - E12 * E12;
+  const double B11 = E00 * E22 - E02 * E02;
+  const double B22 = E00 * E11 - E01 * E01;
+  double u0, u1, u2;
+  {
+    const double a0 = fabs(B00), a1 = fabs(B11), a2 = fabs(B22);
+    if (a0 >= a1 && a0 >= a2) {
+      u0 = B00;
+      u1 = E02 * E12 - E01 * E22;
+      u2 = E01 * E12 - E02 * E11;
+    } else if (a1 >= a2) {
+      u0 = E02 * E12 - E01 * E22;
+      u1 = B11;
+      u2 = E01 * E02 - E00 * E12;
+    } else {
+      u0 = E01 * E12 - E02 * E11;
+      u1 = E01 * E02 - E00 * E12;
+      u2 = B22;
+    }
+    if (a0 == 0.0 && a1 == 0.0 && a2 == 0.0) {  // rank <= 1: any null vector
+      u0 = 0.0;
+      u1 = 0.0;
+      u2 = 1.0;
+    }
+  }
+  out.u0 = u0;
+  out.u1 = u1;
+  out.u2 = u2;
+  out.s = -beta * (m0 * u0 + m1 * u1 + m2 * u2);
+  out.lam = lam;
+
+  // degenerate: gap <= 1e-9 ||S||_F (fitting.py:552-554);
+  // ||S||_F^2 = ||C||_F^2 + 2 n mu.C.mu + n^2 (1 + nu)^2
+  // (trace(S)/2 <= ||S||_F <= trace(S) = q3 for PSD S: only near-ties need the norm)
+  {
+    const double gap = lam2 - lam;
+    if (gap > 1e-9 * q3) {
+      out.degenerate = false;
+    } else {
+      const double fc = c00 * c00 + c11 * c11 + c22 * c22 + 2.0 * (c01 * c01 + c02 * c02 + c12 * c12);
+      const double np1 = n * (1.0 + nu);
+      const double fro2 = fc + 2.0 * n * mm + np1 * np1;
+      out.degenerate = gap <= 0.0 || gap * gap <= 1e-18 * fro2;
+    }
+  }
+
+  // curvature: lam_min(C) / tr(C)
+  out.kappa = curvature_from(t, c1, det, ft, k1, k2, k3);
+}
+
+// canonical sign + unit normal / offset (fitting.py:76-94 and SURVEY A18)
+__device__ __forceinline__ void finish_plane(double a, double b, double c, double d, float& nx,
+                                             float& ny, float& nz, float& off) {
+  // exact power-of-two rescale so the fp32 conversion neither over- nor underflows
+  const int hm = max(max(__double2hiint(a) & 0x7ff00000, __double2hiint(b) & 0x7ff00000),
+                     max(__double2hiint(c) & 0x7ff00000, __double2hiint(d) & 0x7ff00000));
+  const int e = hm >> 20;
+  const double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023 - e)
+  const float fa = (float)(a * sc), fb = (float)(b * sc), fc = (float)(c * sc),
+              fd = (float)(d * sc);
+  const float n4 = rsqrtf(fa * fa + fb * fb + fc * fc + fd * fd);
+  float sign = 1.0f;
+  if (fabsf(fc * n4) > 1e-9f) sign = fc > 0.0f ? 1.0f : -1.0f;
+  else if (fabsf(fb * n4) > 1e-9f) sign = fb > 0.0f ? 1.0f : -1.0f;
+  else if (fabsf(fa * n4) > 1e-9f) sign = fa > 0.0f ? 1.0f : -1.0f;
+  else if (fd < 0.0f) sign = -1.0f;
+  const float in3 = sign * rsqrtf(fa * fa + fb * fb + fc * fc);
+  nx = fa * in3;
+  ny = fb * in3;
+  nz = fc * in3;
+  off = fd * in3;
+}
+
+// ---- TMA / mbarrier helpers (sm_90+ async proxy; SASS UTMALDG + SYNCS)
+
+}  // namespace rf_dev

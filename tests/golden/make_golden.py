@@ -128,6 +128,51 @@ def random_plane(rng, zlo, zhi):
     return rf.GroundTruthPlane(np.array([*n, -n[2] * z0]))
 
 
+def run_rects(name, cam, depth_img, stored, dtype, rng, count=60):
+    """Reference fit_rect (naive backend) on random rects, incl. frame-sized and tiny ones."""
+    maps = rf.compute_tan_maps(cam)
+    W, H = cam.width, cam.height
+    rects = [(0, 0, W, H), (0, 0, 2, 2), (W - 3, H - 1, W, H)]
+    while len(rects) < count:
+        x0, y0 = int(rng.integers(0, W - 1)), int(rng.integers(0, H - 1))
+        rects.append((x0, y0, int(rng.integers(x0 + 1, W + 1)), int(rng.integers(y0 + 1, H + 1))))
+    out = {"depth": stored, "fx": cam.fx, "fy": cam.fy, "cx": cam.cx, "cy": cam.cy, "dtype": dtype,
+           "rects": np.array(rects, np.int32)}
+    for form in FORMS:
+        coef = np.full((len(rects), 4), np.nan)
+        xcoef = np.full((len(rects), 3), np.nan)
+        rms = np.full(len(rects), np.nan)
+        lam = np.full(len(rects), np.nan)
+        curv = np.full(len(rects), np.nan)
+        npts = np.zeros(len(rects), np.int32)
+        status = np.zeros(len(rects), np.int32)
+        scale = np.full(len(rects), np.nan)
+        for k, (x0, y0, x1, y1) in enumerate(rects):
+            samples = gather_window_samples(depth_img, maps, rf.Rect(x0, y0, x1, y1), form)
+            npts[k] = samples.shape[0]
+            try:
+                res = rf.fit_rect(depth_img, maps, rf.Rect(x0, y0, x1, y1), form, "naive")
+            except rf.InsufficientSamplesError:
+                continue
+            status[k] = 2 | (4 if res.degenerate else 0)
+            if isinstance(res.plane, ExplicitPlane):
+                coef[k] = explicit_to_implicit(res.plane).coefficients
+                xcoef[k] = res.plane.coefficients
+                lam[k] = res.rms_residual ** 2 * res.n_points
+            else:
+                coef[k] = res.plane.coefficients
+                lam[k] = res.eigenvalue
+            rms[k] = res.rms_residual
+            s4 = implicit_scatter(samples, form)
+            curv[k] = curvature(s4, form)
+            scale[k] = float(np.linalg.norm(s4)) / res.n_points
+        key = KEYS[form]
+        out.update({f"{key}_coef": coef, f"{key}_xcoef": xcoef, f"{key}_rms": rms, f"{key}_lam": lam,
+                    f"{key}_curv": curv, f"{key}_n": npts, f"{key}_status": status, f"{key}_scale": scale})
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, "rects:", len(rects))
+
+
 def main():
     # 1. noisy three-plane scene, 10% dropout, float32 metres (small_camera of the reference tests)
     cam = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=31.5, cy=23.5, width=64, height=48)
@@ -138,6 +183,9 @@ def main():
     z32 = np.where(d.valid, d.values, 0.0).astype(np.float32)
     for w in (3, 5):
         run_case(f"planes_f32_w{w}", cam, rf.DepthImage(values=z32.astype(np.float64)), z32, w, "f32")
+
+    run_rects("rects_planes_f32", cam, rf.DepthImage(values=z32.astype(np.float64)), z32, "f32",
+              np.random.default_rng(21))
 
     # 1b. explicit validity mask: DepthImage(values, valid=mask) (synth.py:88-94)
     mask = np.random.default_rng(5).random(z32.shape) > 0.2

@@ -88,3 +88,16 @@ def golden_mask(g: dict):
     if g["valid"] is None or np.array_equal(g["valid"], derived):
         return None
     return g["valid"]
+
+
+def load_golden_rects(name: str = "rects_planes_f32") -> dict:
+    """Reference fit_rect results on random rects (tests/golden/make_golden.py:run_rects)."""
+    z = np.load(GOLDEN_DIR / f"{name}.npz")
+    depth = z["depth"]
+    H, W = depth.shape
+    g = {"depth": depth, "cam": Cam(float(z["fx"]), float(z["fy"]), float(z["cx"]), float(z["cy"]), W, H),
+         "rects": z["rects"], "dtype": str(z["dtype"])}
+    for key, form in (("rgbd", "implicit-rgbd"), ("std", "implicit-standard"),
+                      ("xrgbd", "explicit-rgbd"), ("xstd", "explicit-standard")):
+        g[form] = {k: z[f"{key}_{k}"] for k in ("coef", "xcoef", "rms", "lam", "curv", "n", "status", "scale")}
+    return g

@@ -157,3 +157,21 @@ def test_pixel_subset_matches_full_frame():
     sub = O.fit_pixels(v, valid, tx, ty, 5, "implicit-standard", pixels=pix)
     np.testing.assert_array_equal(sub["status"], full["status"][pix])
     np.testing.assert_array_equal(np.nan_to_num(sub["normal"]), np.nan_to_num(full["normal"][pix]))
+
+
+@pytest.mark.parametrize("form", ["implicit-rgbd", "implicit-standard", "explicit-rgbd", "explicit-standard"])
+def test_oracle_rects_match_reference(form):
+    """rfo_fit_rects vs the reference's fit_rect (naive) on random rects incl. the whole frame."""
+    from tests.helpers import load_golden_rects
+
+    g = load_golden_rects()
+    ref = g[form]
+    tx, ty = O.tan_maps(g["cam"].fx, g["cam"].fy, g["cam"].cx, g["cam"].cy, g["cam"].width, g["cam"].height)
+    v, valid = O.depth_from_meters(g["depth"])
+    got = O.fit_rects(v, valid, tx, ty, g["rects"], form)
+    np.testing.assert_array_equal(got["status"], ref["status"])
+    np.testing.assert_array_equal(got["n"], ref["n"])
+    ok = (ref["status"] & 2) != 0
+    assert np.abs(got["coef"][ok] - ref["coef"][ok]).max() <= 1e-6
+    np.testing.assert_allclose(got["rms"][ok], ref["rms"][ok], rtol=1e-5,
+                               atol=float(np.sqrt(1e-10 * np.nanmax(ref["scale"]))))
