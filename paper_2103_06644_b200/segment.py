@@ -1,0 +1,222 @@
+"""Quadtree planar segmentation on the batched GPU rect fits.
+
+Same behaviour as the reference's ``segment()`` (``segment.py:327-431``): the frame is
+cut into a square grid, each tile is fitted, tiles whose fit is degenerate or whose
+rms residual exceeds the threshold split into four children up to ``max_depth``,
+tiles with too few valid pixels are rejected, and k-means over the fitted tiles'
+plane features groups coplanar tiles.
+
+B200 design: the quadtree is evaluated **level-synchronously** -- every pending tile
+of a level is fitted in ONE ``rf_fit_rects`` launch (one CTA per tile, direct sums)
+instead of one Python ``fit_rect`` per tile.  Each tile's decision depends only on
+its own fit, so the leaf set equals the reference's; the leaves are then listed in
+the reference's LIFO traversal order so that k-means (which seeds by sample index)
+sees the same sequence.  k-means runs on the host: it clusters a few hundred
+4-vectors and must reproduce the reference's numpy ``default_rng`` seeding.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import fitting as F
+from .pixels import EXPLICIT_RGBD, EXPLICIT_STANDARD, FORMULATIONS, IMPLICIT_RGBD, IMPLICIT_STANDARD, TanAngleMaps
+
+UNLABELED = -1
+MIN_TILE_EDGE = 2  # segment.py:62-64: a 2x2 tile still holds 4 samples
+DEFAULT_THRESHOLDS = {IMPLICIT_STANDARD: 8e-3, IMPLICIT_RGBD: 8e-3, EXPLICIT_STANDARD: 0.02, EXPLICIT_RGBD: 8e-3}
+
+
+class TileStatus(enum.Enum):
+    FITTED = "fitted"
+    TOO_INVALID = "too_invalid"
+    HIGH_ERROR = "high_error_leaf"
+
+
+@dataclass(frozen=True)
+class SegConfig:
+    """Segmentation knobs (reference segment.py:81-130); backend is always the device."""
+
+    formulation: str = IMPLICIT_RGBD
+    backend: str = "b200"
+    initial_tile: int = 64
+    max_depth: int = 3
+    rms_threshold: float | None = None
+    min_valid_fraction: float = 0.5
+    k: int = 8
+    seed: int = 0
+    d_scale: float = 5.0
+    error_metric: str = "rms"
+
+    def __post_init__(self) -> None:
+        if self.formulation not in FORMULATIONS:
+            raise ValueError(f"unknown formulation {self.formulation!r}")
+        if self.backend != "b200":
+            raise ValueError(f"unknown backend {self.backend!r}")
+        if self.max_depth < 0:
+            raise ValueError("max_depth must be non-negative")
+        if self.initial_tile < (1 << self.max_depth) * MIN_TILE_EDGE:
+            raise ValueError(f"initial_tile {self.initial_tile} cannot survive {self.max_depth} subdivisions")
+        if self.threshold <= 0:
+            raise ValueError("rms_threshold must be positive")
+        if not 0.0 <= self.min_valid_fraction <= 1.0:
+            raise ValueError("min_valid_fraction must be in [0, 1]")
+        if self.k < 1:
+            raise ValueError("k must be at least 1")
+        if self.d_scale <= 0:
+            raise ValueError("d_scale must be positive")
+        if self.error_metric != "rms":
+            raise NotImplementedError("error_metric='max' is not implemented on the device path")
+
+    @property
+    def threshold(self) -> float:
+        return self.rms_threshold if self.rms_threshold is not None else DEFAULT_THRESHOLDS[self.formulation]
+
+
+@dataclass
+class Tile:
+    rect: F.Rect
+    status: TileStatus
+    level: int
+    result: F.FitResult | None = None
+    cluster: int = UNLABELED
+
+
+@dataclass
+class Segmentation:
+    tiles: list
+    labels: torch.Tensor
+    centroids: np.ndarray
+    n_fitted: int
+    n_too_invalid: int
+    n_high_error: int
+    warnings: list = field(default_factory=list)
+
+
+def tile_features(result: F.FitResult, d_scale: float = 5.0) -> np.ndarray:
+    """Plane scaled to a unit normal with offset >= 0, offset / d_scale (segment.py:199-214)."""
+    coef = (F.explicit_to_implicit(result.plane).coefficients if isinstance(result.plane, F.ExplicitPlane)
+            else result.plane.coefficients).copy()
+    norm = float(np.linalg.norm(coef[:3]))
+    if norm == 0:
+        raise ValueError("fit has a degenerate normal")
+    coef /= norm
+    flip = coef[3] < 0
+    if coef[3] == 0:
+        for v in (coef[2], coef[1], coef[0]):
+            if abs(v) > 1e-12:
+                flip = v < 0
+                break
+    if flip:
+        coef = -coef
+    return np.array([coef[0], coef[1], coef[2], coef[3] / d_scale])
+
+
+def kmeans(features: np.ndarray, k: int, seed: int = 0, max_iter: int = 100):
+    """Lloyd's k-means, k-means++ seeding from numpy default_rng(seed) (segment.py:224-269)."""
+    x = np.asarray(features, dtype=np.float64)
+    if x.ndim != 2 or x.shape[0] == 0:
+        raise ValueError(f"features must be a non-empty (n, d) array, got {x.shape}")
+    n = x.shape[0]
+    if k < 1:
+        raise ValueError("k must be at least 1")
+    k = min(k, n)
+    rng = np.random.default_rng(seed)
+    cent = np.empty((k, x.shape[1]))
+    cent[0] = x[rng.integers(n)]
+    for i in range(1, k):
+        d2 = ((x[:, None, :] - cent[None, :i, :]) ** 2).sum(axis=2).min(axis=1)
+        tot = float(d2.sum())
+        if tot == 0.0:
+            cent[i:] = x[rng.integers(n, size=k - i)]
+            break
+        cent[i] = x[rng.choice(n, p=d2 / tot)]
+    labels = np.full(n, -1)
+    for _ in range(max_iter):
+        dist = ((x[:, None, :] - cent[None, :, :]) ** 2).sum(axis=2)
+        new = dist.argmin(axis=1)
+        if np.array_equal(new, labels):
+            break
+        labels = new
+        for j in range(k):
+            members = x[labels == j]
+            cent[j] = members.mean(axis=0) if len(members) else x[int(dist.min(axis=1).argmax())]
+    return labels, cent
+
+
+def _grid(width: int, height: int, tile: int):
+    return [F.Rect(x, y, min(x + tile, width), min(y + tile, height))
+            for y in range(0, height, tile) for x in range(0, width, tile)]
+
+
+def _children(r: F.Rect):
+    xm, ym = r.x0 + (r.x1 - r.x0) // 2, r.y0 + (r.y1 - r.y0) // 2
+    return [F.Rect(r.x0, r.y0, xm, ym), F.Rect(xm, r.y0, r.x1, ym),
+            F.Rect(r.x0, ym, xm, r.y1), F.Rect(xm, ym, r.x1, r.y1)]
+
+
+def segment(depth, maps: TanAngleMaps, config: SegConfig, frame: int = 0, mask=None) -> Segmentation:
+    """Segment one frame of a depth tensor ([H,W] or [B,H,W] on the device)."""
+    d = F._as_depth_tensor(depth, torch.device("cuda", maps.device))
+    H, W = d.shape[-2:]
+    if W < MIN_TILE_EDGE or H < MIN_TILE_EDGE:
+        raise ValueError(f"image {W}x{H} is smaller than one fittable tile")
+    decided = {}   # rect -> (kind, result); kind in {"fit", "invalid", "split", "high"}
+    level_rects = [(r, 0) for r in _grid(W, H, config.initial_tile)]
+    while level_rects:
+        rows = F.fit_rects(d, maps, [tuple(r) for r, _ in level_rects], config.formulation,
+                           frames=frame, mask=mask)
+        nxt = []
+        for (r, lev), row in zip(level_rects, rows):
+            n_valid = int(row["n_points"])
+            if n_valid < config.min_valid_fraction * r.area or n_valid == 0 or not row["status"] & F.RECT_FIT:
+                decided[r] = ("invalid", None)
+                continue
+            res = F._result(row, config.formulation)
+            err = np.inf if res.rms_residual is None else res.rms_residual
+            if not res.degenerate and err <= config.threshold:
+                decided[r] = ("fit", res)
+            elif lev < config.max_depth and r.x1 - r.x0 >= 2 * MIN_TILE_EDGE and r.y1 - r.y0 >= 2 * MIN_TILE_EDGE:
+                decided[r] = ("split", res)
+                nxt.extend((c, lev + 1) for c in _children(r))
+            else:
+                decided[r] = ("high", res)
+        level_rects = nxt
+    # leaves in the reference's LIFO order (pending.pop() / pending.extend(children))
+    tiles = []
+    stack = [(r, 0) for r in _grid(W, H, config.initial_tile)]
+    while stack:
+        r, lev = stack.pop()
+        kind, res = decided[r]
+        if kind == "split":
+            stack.extend((c, lev + 1) for c in _children(r))
+        elif kind == "fit":
+            tiles.append(Tile(r, TileStatus.FITTED, lev, res))
+        elif kind == "high":
+            tiles.append(Tile(r, TileStatus.HIGH_ERROR, lev, res))
+        else:
+            tiles.append(Tile(r, TileStatus.TOO_INVALID, lev))
+    warnings = []
+    fitted = [t for t in tiles if t.status is TileStatus.FITTED]
+    if fitted:
+        feats = np.stack([tile_features(t.result, config.d_scale) for t in fitted])
+        k = config.k
+        if k > len(fitted):
+            warnings.append(f"k={k} exceeds {len(fitted)} fitted tiles; clamped")
+            k = len(fitted)
+        labels, centroids = kmeans(feats, k, seed=config.seed)
+        for t, lab in zip(fitted, labels):
+            t.cluster = int(lab)
+    else:
+        centroids = np.zeros((0, 4))
+        warnings.append("no tiles were fitted")
+    lab = torch.full((H, W), UNLABELED, dtype=torch.int16, device=d.device)
+    for t in fitted:
+        lab[t.rect.y0:t.rect.y1, t.rect.x0:t.rect.x1] = t.cluster
+    return Segmentation(tiles, lab, centroids, len(fitted),
+                        sum(t.status is TileStatus.TOO_INVALID for t in tiles),
+                        sum(t.status is TileStatus.HIGH_ERROR for t in tiles), warnings)

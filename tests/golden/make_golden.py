@@ -173,6 +173,24 @@ def run_rects(name, cam, depth_img, stored, dtype, rng, count=60):
     print(name, "rects:", len(rects))
 
 
+def run_segment(name, cam, depth_img, stored, formulations=FORMS):
+    """Reference quadtree segmentation (segment.py:327-431), naive backend (direct sums)."""
+    from rangefit.segment import SegConfig, segment
+
+    maps = rf.compute_tan_maps(cam)
+    out = {"depth": stored, "fx": cam.fx, "fy": cam.fy, "cx": cam.cx, "cy": cam.cy}
+    for form in formulations:
+        cfg = SegConfig(formulation=form, backend="naive", initial_tile=32, max_depth=3, k=6, seed=3)
+        seg = segment(depth_img, maps, cfg)
+        key = KEYS[form]
+        out[f"{key}_rects"] = np.array([tuple(t.rect) for t in seg.tiles], np.int32)
+        out[f"{key}_status"] = np.array([t.status.value for t in seg.tiles])
+        out[f"{key}_cluster"] = np.array([t.cluster for t in seg.tiles], np.int32)
+        out[f"{key}_labels"] = seg.labels
+        print(name, form, "tiles", len(seg.tiles), "fitted", seg.n_fitted)
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+
+
 def main():
     # 1. noisy three-plane scene, 10% dropout, float32 metres (small_camera of the reference tests)
     cam = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=31.5, cy=23.5, width=64, height=48)
@@ -186,6 +204,18 @@ def main():
 
     run_rects("rects_planes_f32", cam, rf.DepthImage(values=z32.astype(np.float64)), z32, "f32",
               np.random.default_rng(21))
+
+    # quadtree segmentation of a Voronoi-like multi-plane frame
+    cam_s = rf.CameraIntrinsics(fx=120.0, fy=120.0, cx=63.5, cy=47.5, width=128, height=96)
+    maps_s = rf.compute_tan_maps(cam_s)
+    planes = []
+    for (x0, y0, x1, y1) in ((0, 0, 64, 48), (64, 0, 128, 48), (0, 48, 70, 96), (70, 48, 128, 96)):
+        p = random_plane(rng, 1.0, 3.5)
+        planes.append(rf.GroundTruthPlane(p.coefficients, mask_rect=(x0, y0, x1, y1)))
+    d_s, _ = rf.render_scene(rf.SyntheticScene(tuple(planes)), maps_s, noise=rf.NoiseModel(), seed=8,
+                             dropout=0.03)
+    z_s = np.where(d_s.valid, d_s.values, 0.0).astype(np.float32)
+    run_segment("segment_planes", cam_s, rf.DepthImage(values=z_s.astype(np.float64)), z_s)
 
     # 1b. explicit validity mask: DepthImage(values, valid=mask) (synth.py:88-94)
     mask = np.random.default_rng(5).random(z32.shape) > 0.2

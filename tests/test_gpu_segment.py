@@ -1,0 +1,32 @@
+"""Level-synchronous quadtree segmentation on the GPU rect fits vs the reference's
+own segment() (golden: tests/golden/make_golden.py:run_segment): same leaf tiles in
+the same order, same statuses, same k-means clusters and label lattice."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2103_06644_b200 as rf
+from paper_2103_06644_b200 import segment as S
+from tests.helpers import GOLDEN_DIR
+
+pytestmark = pytest.mark.gpu
+
+KEYS = {"implicit-rgbd": "rgbd", "implicit-standard": "std", "explicit-rgbd": "xrgbd", "explicit-standard": "xstd"}
+
+
+@pytest.mark.parametrize("form", list(rf.FORMULATIONS))
+def test_segment_matches_reference(form):
+    z = np.load(GOLDEN_DIR / "segment_planes.npz")
+    depth = torch.from_numpy(z["depth"]).cuda()
+    H, W = depth.shape
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(float(z["fx"]), float(z["fy"]), float(z["cx"]),
+                                                   float(z["cy"]), W, H))
+    seg = S.segment(depth, maps, S.SegConfig(formulation=form, initial_tile=32, max_depth=3, k=6, seed=3))
+    key = KEYS[form]
+    np.testing.assert_array_equal(np.array([tuple(t.rect) for t in seg.tiles]), z[f"{key}_rects"])
+    assert [t.status.value for t in seg.tiles] == list(z[f"{key}_status"])
+    np.testing.assert_array_equal(np.array([t.cluster for t in seg.tiles]), z[f"{key}_cluster"])
+    np.testing.assert_array_equal(seg.labels.cpu().numpy(), z[f"{key}_labels"])
