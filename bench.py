@@ -325,6 +325,12 @@ def run_ours(args, world, rank, local):
 
     launches = rf.launches_per_call(forms) * args.steps
 
+    sweep = None
+    if rank == 0 and not args.no_sweep:
+        del host_in, host_out, dev_in
+        torch.cuda.empty_cache()
+        sweep = config_sweep(dev, peak)
+
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu:
         frames_host = depth[:4].cpu()
@@ -347,18 +353,58 @@ def run_ours(args, world, rank, local):
                     "note": "pinned host buffers, 8-chunk H2D/fit/D2H pipeline on two streams"},
             "gpu_launches": launches,
             "clocks": clocks,
+            "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
+
+
+def config_sweep(dev, peak):
+    """Informational: steady-state throughput of every BASELINE config shape on this GPU
+    (both implicit fits, CUDA events over repeated passes of a representative chunk of
+    frames; the bench line above is config 2 at window 5)."""
+    import paper_2103_06644_b200 as rf
+    from paper_2103_06644_b200 import scenes
+
+    plan = [("C1", 1, (5,)), ("C2", 64, (3, 5, 7, 11, 15)), ("C3", 32, (9,)), ("C4", 16, (15,)), ("C5", 4, (31,))]
+    res = {}
+    stream = torch.cuda.current_stream(dev)
+    for name, frames, windows in plan:
+        cfg = scenes.CONFIGS[name]
+        depth = scenes.render_batch(cfg, frames=frames, device=dev)
+        maps = rf.compute_tan_maps(rf.CameraIntrinsics(cfg.f, cfg.f, cfg.cx, cfg.cy, cfg.width, cfg.height), dev)
+        out = {f: rf.PixelFits.empty(frames, cfg.height, cfg.width, dev) for f in rf.PIXEL_FORMULATIONS}
+        for w in windows:
+            for _ in range(3):
+                rf.fit_pixels(depth, maps, w, out=out, stream=stream)
+            reps = 20 if name in ("C1", "C2") else 5
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                rf.fit_pixels(depth, maps, w, out=out, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            px = frames * cfg.width * cfg.height
+            in_b = 2 if cfg.u16 else 4
+            res[f"{name}_w{w}"] = {
+                "frames": frames, "ms_per_pass": ms, "Mpixel_fits_per_s": 2 * px / (ms * 1e-3) / 1e6,
+                "frames_per_s": frames / (ms * 1e-3),
+                "hbm_frac": 2 * px * (in_b + BYTES_OUT) / (ms * 1e-3) / 1e9 / peak,
+                "full_batch_ms_extrapolated": ms * cfg.frames / frames}
+        del depth, out
+        torch.cuda.empty_cache()
+    return res
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the informational per-config sweep")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     try:
