@@ -88,59 +88,57 @@ struct WindowFit {
 // c1 = sum of principal 2x2 minors, det = det C and the fp32 roots k1<=k2<=k3 of
 // l^3 - t l^2 + c1 l - det: fp64 Newton from below, or -- when the bottom pair is
 // close -- Newton from above on lam_max and deflation.
+// fp64 polish of the curvature eigenvalue (close bottom pair, or a bottom near-tie
+// handled from the top): out of line, the common case never enters it.
+static __device__ __noinline__ float curvature_slow(double t, double c1, double det, float ft, float k1, float k2,
+                                             float k3, bool top) {
+  auto newton = [&](double x) {
+    const double P = fma(fma(t - x, x, -c1), x, det);
+    const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+    return P * rcp_approx(dP);
+  };
+  double lk;
+  if (!top) {
+    // Newton from below lam_min (monotone)
+    double l = (double)k1 * (1.0 - 1e-5);
+    l -= newton(l);
+    l -= newton(l);
+    if ((k2 - k1) < 0.05f * k2) {  // close bottom pair: iterate to convergence
+      for (int it = 0; it < 64; ++it) {
+        const double step = newton(l);
+        l -= step;
+        if (!(fabs(step) > 1e-10 * l)) break;
+      }
+    }
+    lk = l;
+  } else {
+    // near-tie at the bottom: Newton from above lam_max (well separated here), then
+    // deflate; lam_max only needs ~1e-10 for a 1e-5 curvature
+    double l = fmin((double)k3 * (1.0 + 1e-5), t);
+    l -= newton(l);
+    l -= newton(l);
+    if ((k3 - k2) < 0.05f * k3) {  // top pair close too: iterate to convergence
+      for (int it = 0; it < 62; ++it) {
+        const double step = newton(l);
+        l -= step;
+        if (!(fabs(step) > 1e-12 * l)) break;
+      }
+    }
+    const double S = t - l;
+    const double Pp = det * rcp_fast(l);
+    const double den = S + (double)fsqrt((float)fmax(fma(S, S, -4.0 * Pp), 0.0));
+    lk = den > 0.0 ? 2.0 * Pp * rcp_fast(den) : 0.0;
+  }
+  return t > 0.0 ? (float)lk * frcp(ft) : 0.0f;
+}
+
 __device__ __forceinline__ float curvature_from(double t, double c1, double det, float ft, float k1,
                                                 float k2, float k3) {
-  {
-    double lk;
-    const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
-    if (!top) {
-      // Newton from below lam_min (monotone).  With a well separated bottom pair
-      // (relative gap > 20%) the fp32 seed (deflated, ~2e-6 relative) already meets
-      // the 1e-4 curvature tolerance with margin; otherwise polish in fp64.
-      double l = (double)k1;
-      if ((k2 - k1) < 0.2f * k2) {
-        l *= (1.0 - 1e-5);
-        auto newton = [&](double x) {
-          const double P = fma(fma(t - x, x, -c1), x, det);
-          const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
-          return P * rcp_approx(dP);
-        };
-        l -= newton(l);
-        l -= newton(l);
-        if ((k2 - k1) < 0.05f * k2) {  // close bottom pair (rare): iterate to convergence
-          for (int it = 0; it < 64; ++it) {
-            const double step = newton(l);
-            l -= step;
-            if (!(fabs(step) > 1e-10 * l)) break;
-          }
-        }
-      }
-      lk = l;
-    } else {
-      // near-tie at the bottom: Newton from above lam_max (well separated here),
-      // then deflate; lam_max only needs ~1e-10 for a 1e-5 curvature
-      double l = fmin((double)k3 * (1.0 + 1e-5), t);
-      auto newton = [&](double x) {
-        const double P = fma(fma(t - x, x, -c1), x, det);
-        const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
-        return P * rcp_approx(dP);
-      };
-      l -= newton(l);
-      l -= newton(l);
-      if ((k3 - k2) < 0.05f * k3) {  // top pair close too (rare): iterate to convergence
-        for (int it = 0; it < 62; ++it) {
-          const double step = newton(l);
-          l -= step;
-          if (!(fabs(step) > 1e-12 * l)) break;
-        }
-      }
-      const double S = t - l;
-      const double Pp = det * rcp_fast(l);
-      const double den = S + (double)fsqrt((float)fmax(fma(S, S, -4.0 * Pp), 0.0));
-      lk = den > 0.0 ? 2.0 * Pp * rcp_fast(den) : 0.0;
-    }
-    return t > 0.0 ? (float)lk * frcp(ft) : 0.0f;
-  }
+  const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
+  // With a well separated bottom pair (relative gap > 20%) the fp32 seed (deflated,
+  // ~2e-6 relative) already meets the 1e-4 curvature tolerance with margin.
+  if (!top && (k2 - k1) >= 0.2f * k2) return t > 0.0 ? k1 * frcp(ft) : 0.0f;
+  return curvature_slow(t, c1, det, ft, k1, k2, k3, top);
 }
 
 // curvature when no implicit solve runs (explicit fits only)
@@ -192,6 +190,54 @@ __device__ __forceinline__ void explicit_solve(const Sym3& C, double m0, double 
   (void)M02;
   (void)M12;
   out.degenerate = !(trace > 0.0) || p0 <= fl || p1 <= fl || p2 <= fl;
+}
+
+// Newton on the quartic from below until the step is below 1e-13 relative (out of line).
+static __device__ __noinline__ double newton_converge(double q3, double q2, double q1, double q0, double l) {
+  for (int it = 0; it < 64; ++it) {
+    const double x2 = l * l;
+    const double G = fma(fma(l - q3, l, q2), x2, fma(-q1, l, q0));
+    const double dG = fma(fma(fma(4.0, l, -3.0 * q3), l, 2.0 * q2), l, -q1);
+    const double step = G * rcp_approx(dG);
+    l -= step;
+    if (!(fabs(step) > 1e-13 * l)) break;
+  }
+  return l;
+}
+
+// Near-tie lam1 ~ lam2 (rare): exact deflation of the quartic.  lam4 (the largest
+// root, ~n(1+nu)) and then lam3 are found by Newton from above (upper bounds q3 and
+// lam1+lam2+lam3), each divided out by backward deflation (stable for the largest
+// root); the quadratic left over has roots lam1 <= lam2, solved cancellation-free.
+static __device__ __noinline__ void tie_deflation(double q3, double q2, double q1, double q0, double& lam,
+                                           double& lam2) {
+  double l4 = q3;
+  for (int it = 0; it < 64; ++it) {
+    const double G = fma(fma(fma(l4 - q3, l4, q2), l4, -q1), l4, q0);
+    const double dG = fma(fma(fma(4.0, l4, -3.0 * q3), l4, 2.0 * q2), l4, -q1);
+    const double step = G * rcp_approx(dG);
+    l4 -= step;
+    if (!(fabs(step) > 1e-15 * l4)) break;
+  }
+  const double i4 = rcp_fast(l4);
+  const double h0 = -q0 * i4;             // -lam1 lam2 lam3
+  const double h1 = (q1 + h0) * i4;       // lam1 lam2 + lam1 lam3 + lam2 lam3
+  const double h2 = (h1 - q2) * i4;       // -(lam1 + lam2 + lam3)
+  double l3 = -h2;
+  for (int it = 0; it < 64; ++it) {
+    const double H = fma(fma(l3 + h2, l3, h1), l3, h0);
+    const double dH = fma(fma(3.0, l3, 2.0 * h2), l3, h1);
+    const double step = H * rcp_approx(dH);
+    l3 -= step;
+    if (!(fabs(step) > 1e-15 * l3)) break;
+  }
+  const double i3 = rcp_fast(l3);
+  const double e0 = -h0 * i3;             // lam1 lam2
+  const double e1 = (e0 - h1) * i3;       // -(lam1 + lam2)
+  const double disc = (double)fsqrt((float)fmax(fma(e1, e1, -4.0 * e0), 0.0));
+  const double den = disc - e1;           // 2 lam2
+  lam = den > 0.0 ? 2.0 * e0 * rcp_fast(den) : 0.0;
+  lam2 = 0.5 * den;
 }
 
 // Smallest eigenpair of S = [[C + n mu mu^T, n mu], [n mu^T, n]] (the
@@ -266,48 +312,11 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     l -= newton(l);
     l -= newton(l);
     if (grel > 1e-4f) l -= newton(l);
-    if (grel > 1e-3f) {  // large residual windows (rare): iterate to convergence
-      for (int it = 0; it < 64; ++it) {
-        const double step = newton(l);
-        l -= step;
-        if (!(fabs(step) > 1e-13 * l)) break;
-      }
-    }
+    if (grel > 1e-3f) l = newton_converge(q3, q2, q1, q0, l);  // large-residual windows (rare)
     lam = l;
     lam2 = (double)g2;
   } else {
-    // (B) near-tie lam1 ~ lam2: exact deflation of the quartic.  lam4 (the
-    // largest root, ~n(1+nu)) and then lam3 are found by Newton from above
-    // (upper bounds q3 and lam1+lam2+lam3), each divided out by backward
-    // deflation (stable for the largest root); the quadratic left over has
-    // roots lam1 <= lam2, solved in the cancellation-free form.
-    double l4 = q3;
-    for (int it = 0; it < 64; ++it) {
-      const double G = fma(fma(fma(l4 - q3, l4, q2), l4, -q1), l4, q0);
-      const double dG = fma(fma(fma(4.0, l4, -3.0 * q3), l4, 2.0 * q2), l4, -q1);
-      const double step = G * rcp_approx(dG);
-      l4 -= step;
-      if (!(fabs(step) > 1e-15 * l4)) break;
-    }
-    const double i4 = rcp_fast(l4);
-    const double h0 = -q0 * i4;             // -lam1 lam2 lam3
-    const double h1 = (q1 + h0) * i4;       // lam1 lam2 + lam1 lam3 + lam2 lam3
-    const double h2 = (h1 - q2) * i4;       // -(lam1 + lam2 + lam3)
-    double l3 = -h2;
-    for (int it = 0; it < 64; ++it) {
-      const double H = fma(fma(l3 + h2, l3, h1), l3, h0);
-      const double dH = fma(fma(3.0, l3, 2.0 * h2), l3, h1);
-      const double step = H * rcp_approx(dH);
-      l3 -= step;
-      if (!(fabs(step) > 1e-15 * l3)) break;
-    }
-    const double i3 = rcp_fast(l3);
-    const double e0 = -h0 * i3;             // lam1 lam2
-    const double e1 = (e0 - h1) * i3;       // -(lam1 + lam2)
-    const double disc = (double)fsqrt((float)fmax(fma(e1, e1, -4.0 * e0), 0.0));
-    const double den = disc - e1;           // 2 lam2
-    lam = den > 0.0 ? 2.0 * e0 * rcp_fast(den) : 0.0;
-    lam2 = 0.5 * den;
+    tie_deflation(q3, q2, q1, q0, lam, lam2);
   }
 
   // eigenvector: dominant column of adj(C - lam B), B = I + beta mu mu^T
