@@ -177,12 +177,15 @@ def run_reference(args, world, rank):
     from oracle import oracle as O
 
     O.build() if not O.LIB_PATH.exists() else None
+    # each step is a bounded sample (whole frames, >= 1) sized so that the whole
+    # --steps K --warmup W run stays within about two minutes of wall time
+    budget = min(2.0, 100.0 / max(args.steps + args.warmup, 1))
     for _ in range(max(args.warmup, 0)):
         cpu_reference_rate(frames, cfg, 0.0)
     rates = []
     total = 0.0
     for _ in range(args.steps):
-        r, cores, el, sample = cpu_reference_rate(frames, cfg, 2.0)
+        r, cores, el, sample = cpu_reference_rate(frames, cfg, budget)
         rates.append(r)
         total += el
     value = statistics.median(rates) / 1e6
@@ -406,6 +409,12 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the informational per-config sweep")
     args = ap.parse_args()
+    if args.impl == "reference":
+        # the reference arm is the host-CPU restatement: rank 0 alone runs it, no process group
+        rank = int(os.environ.get("RANK", "0"))
+        if rank == 0:
+            run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), 0)
+        return
     world, rank, local = dist_setup()
     try:
         if args.impl == "reference":
