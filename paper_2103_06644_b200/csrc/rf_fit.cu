@@ -160,8 +160,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     fit_tile_kernel(const KParams P, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   // TMA destinations must be 128-byte aligned: align the dynamic base explicitly
-  unsigned char* smem_raw = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_dyn) + 127) & ~uintptr_t(127));
+  // (pointer arithmetic on the __shared__ array, not integer casts, so every derived
+  // pointer stays in the shared window and compiles to LDS/STS rather than generic LD/ST)
+  unsigned char* smem_raw = smem_dyn + ((128u - (smem_u32(smem_dyn) & 127u)) & 127u);
   const int r = RT > 0 ? RT : P.r;
   const int HW_ = TW + 2 * r;  // halo width
   const int HH_ = TH + 2 * r;  // halo height
@@ -180,8 +181,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   const int VRS = 4 * VQ;                                                // row stride
   double* vd = prim + HH_ * HW_;                                         // [NVD][TH][VRS]
   int* vi = reinterpret_cast<int*>(vd + NVD * TH * VRS);                 // [NVI][TH][VRS]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(vi + NVI * TH * VRS) + 7) & ~uintptr_t(7));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(vi + NVI * TH * VRS + ((NVI * TH * VRS) & 1));
 
   const int tid = threadIdx.x;
   const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;

@@ -138,7 +138,30 @@ __device__ __forceinline__ float curvature_from(double t, double c1, double det,
   // With a well separated bottom pair (relative gap > 20%) the fp32 seed (deflated,
   // ~2e-6 relative) already meets the 1e-4 curvature tolerance with margin.
   if (!top && (k2 - k1) >= 0.2f * k2) return t > 0.0 ? k1 * frcp(ft) : 0.0f;
-  return curvature_slow(t, c1, det, ft, k1, k2, k3, top);
+  // all three roots within 5%: iterate to convergence out of line (rare)
+  if (top ? (k3 - k2) < 0.05f * k3 : (k2 - k1) < 0.05f * k2)
+    return curvature_slow(t, c1, det, ft, k1, k2, k3, top);
+  // Common in the standard form (depth noise dominates: lam_max >> lam_2 ~ lam_min):
+  // two fp64 Newton steps on det(C - l I) -- on lam_max from its seed when the top gap
+  // is the better separated one (then deflate: lam_1 + lam_2 = t - lam_max,
+  // lam_1 lam_2 = det / lam_max), else on lam_min from below.  Same instructions on
+  // both sides, so the warp does not diverge.
+  double x = top ? (double)k3 : (double)k1 * (1.0 - 1e-5);
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double P = fma(fma(t - x, x, -c1), x, det);
+    const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+    x -= P * rcp_approx(dP);
+  }
+  float kmin = (float)x;
+  if (top) {
+    const double S = t - x;
+    const double Pp = det * rcp_fast(x);
+    const float D = (float)fma(S, S, -4.0 * Pp);  // (lam_2 - lam_1)^2, cancellation-free in fp64
+    const float fS = (float)S;
+    kmin = 2.0f * (float)Pp * frcp(fS + fsqrt(fmaxf(D, 0.0f)));
+  }
+  return t > 0.0 ? kmin * frcp(ft) : 0.0f;
 }
 
 // curvature when no implicit solve runs (explicit fits only)
