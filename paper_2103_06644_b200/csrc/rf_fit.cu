@@ -137,16 +137,55 @@ __device__ __forceinline__ TileGeom tile_of(int64_t t, int ntx, int nty) {
 
 // depth element -> fp64 primary p (0 = invalid): DepthImage validity (synth.py:84, 111-114)
 template <int VAR>
-__device__ __forceinline__ double primary_from_f32(float zf, bool mask_ok) {
-  const bool valid = mask_ok && (zf > 0.0f) && (zf <= 3.402823466e38f);  // isfinite & > 0
+__device__ __forceinline__ double primary_of(float zf) {
+  const bool valid = (zf > 0.0f) && (zf <= 3.402823466e38f);  // isfinite & > 0
   const double z = (double)zf;
   return valid ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
 }
 template <int VAR>
-__device__ __forceinline__ double primary_from_u16(unsigned short mm, bool mask_ok) {
-  if (!(mask_ok && mm > 0)) return 0.0;
-  const double z = __ddiv_rn((double)mm, 1000.0);  // mm / 1000.0 exactly as the reference
-  return VAR == VAR_DF ? rcp_fast(z) : z;
+__device__ __forceinline__ double primary_of(unsigned short mm) {
+  // mm / 1000.0 correctly rounded, as the reference divides: q = mm * RN(1/1000) and one
+  // exact-remainder correction (fma(-q, 1000, mm) is exact); checked for all 65535 codes
+  const double m = (double)mm;
+  const double q0 = m * 1e-3;
+  const double z = fma(fma(-q0, 1000.0, m), 1e-3, q0);
+  return mm > 0 ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
+}
+template <int VAR, typename T>
+__device__ __forceinline__ double primary_masked(T v, bool mask_ok) {
+  return mask_ok ? primary_of<VAR>(v) : 0.0;
+}
+
+// Halo tile (raw TMA box, element (row, col) at raw[(row + sy) * HWP + col + sx]) ->
+// prim[row * HW_ + col].  The plain loop covers interior tiles without a mask; image
+// edges (negative shift: rows/columns left of or above the image) and masks take the
+// checked loop.
+template <int VAR, typename T>
+__device__ __forceinline__ void convert_halo(double* prim, const T* raw, int HW_, int HH_, int HWP, int sx,
+                                             int sy, const KParams& P, int64_t frame, int x0, int y0, int r,
+                                             int tid) {
+  const int n = HH_ * HW_;
+  if (!P.mask && (sx | sy) >= 0) {
+#pragma unroll 2
+    for (int e = tid; e < n; e += NTHREADS) {
+      const int row = e / HW_, col = e - row * HW_;
+      prim[e] = primary_of<VAR>(raw[(row + sy) * HWP + col + sx]);
+    }
+  } else {
+    for (int e = tid; e < n; e += NTHREADS) {
+      const int row = e / HW_, col = e - row * HW_;
+      double p = 0.0;
+      if (row + sy >= 0 && col + sx >= 0) {
+        bool mask_ok = true;
+        if (P.mask) {
+          const int y = y0 - r + row, x = x0 - r + col;
+          mask_ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
+        }
+        p = primary_masked<VAR>(raw[(row + sy) * HWP + col + sx], mask_ok);
+      }
+      prim[e] = p;
+    }
+  }
 }
 
 // One persistent CTA walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
@@ -168,6 +207,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   const int HH_ = TH + 2 * r;  // halo height
   constexpr int NVD = VAR == VAR_DF ? 3 : 5;  // fp64 vertical channels
   constexpr int NVI = VAR == VAR_DF ? 3 : 1;  // int vertical channels
+  // small compile-time radii: direct column sums with dy centred on each output row;
+  // otherwise running column sums with dy relative to the tile's first row
+  constexpr bool CENTRED = RT > 0 && RT <= 3;
   const int esz = P.dtype == RF_DEPTH_U16_MM ? 2 : 4;
   const int al = 16 / esz;  // TMA box x origin must be 16-byte aligned
   const int HWP = (HW_ + al - 1 + 7) & ~7;  // TMA box width (covers the alignment shift)
@@ -215,21 +257,12 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       const unsigned char* raw = b ? raw1 : raw0;
       const int bx = box_x(x0 - r, al), by = max(y0 - r, 0);
       const int sx = (x0 - r) - bx, sy = (y0 - r) - by;  // raw index = tile index + shift
-      for (int e = tid; e < HH_ * HW_; e += NTHREADS) {
-        const int row = e / HW_, col = e - row * HW_;
-        double p = 0.0;
-        if (row + sy >= 0 && col + sx >= 0) {
-          bool mask_ok = true;
-          if (P.mask) {
-            const int y = y0 - r + row, x = x0 - r + col;
-            mask_ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
-          }
-          const int ri = (row + sy) * HWP + (col + sx);
-          p = esz == 2 ? primary_from_u16<VAR>(reinterpret_cast<const unsigned short*>(raw)[ri], mask_ok)
-                       : primary_from_f32<VAR>(reinterpret_cast<const float*>(raw)[ri], mask_ok);
-        }
-        prim[e] = p;
-      }
+      if (esz == 2)
+        convert_halo<VAR>(prim, reinterpret_cast<const unsigned short*>(raw), HW_, HH_, HWP, sx, sy, P, frame,
+                          x0, y0, r, tid);
+      else
+        convert_halo<VAR>(prim, reinterpret_cast<const float*>(raw), HW_, HH_, HWP, sx, sy, P, frame, x0, y0,
+                          r, tid);
       __syncthreads();
       // the other buffer was consumed in the previous iteration: prefetch the next tile into it
       if (tid == 0 && t + gridDim.x < total) {
@@ -250,8 +283,8 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
             const int64_t off = frame * P.frame_stride + (int64_t)y * P.row_pitch + x;
             const bool mask_ok =
                 !P.mask || __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
-            p = esz == 2 ? primary_from_u16<VAR>(__ldg(reinterpret_cast<const unsigned short*>(P.depth) + off), mask_ok)
-                         : primary_from_f32<VAR>(__ldg(reinterpret_cast<const float*>(P.depth) + off), mask_ok);
+            p = esz == 2 ? primary_masked<VAR>(__ldg(reinterpret_cast<const unsigned short*>(P.depth) + off), mask_ok)
+                         : primary_masked<VAR>(__ldg(reinterpret_cast<const float*>(P.depth) + off), mask_ok);
           }
           prim[row * HW_ + col] = p;
         }
@@ -266,39 +299,64 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     // output row) pair sums its 2r+1 rows directly (short independent chains,
     // all threads busy).  Otherwise each halo column is split into `parts` row
     // segments that warm up on their 2r leading rows and then slide down.
-    if constexpr (RT > 0 && RT <= 3) {
+    if constexpr (CENTRED) {
+      // dy is centred on the output row (dy = k - RT, compile-time): the dy-weighted
+      // sums fold into symmetric differences d * (p[RT + d] - p[RT - d]).
       constexpr int HWc = TW + 2 * RT;
+      constexpr int K = 2 * RT + 1;
       for (int e = tid; e < TH * HWc; e += NTHREADS) {
         const int o = e / HWc, col = e - o * HWc;
+        double p[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) p[k] = prim[(o + k) * HWc + col];
         double a[NVD];
         int bb[NVI];
+        int m = 0;
+        double s0 = p[0];
 #pragma unroll
-        for (int k = 0; k < NVD; ++k) a[k] = 0.0;
+        for (int k = 0; k < K; ++k) {
+          m += p[k] > 0.0 ? 1 : 0;
+          if (k > 0) s0 += p[k];
+        }
+        double s2 = p[RT + 1] - p[RT - 1];
 #pragma unroll
-        for (int k = 0; k < NVI; ++k) bb[k] = 0;
-        const double fo = (double)(o - RT);
+        for (int d = 2; d <= RT; ++d) s2 = fma((double)d, p[RT + d] - p[RT - d], s2);
+        if (VAR == VAR_DF) {
+          double s1 = p[0] * p[0];
 #pragma unroll
-        for (int k = 0; k <= 2 * RT; ++k) {
-          const double p = prim[(o + k) * HWc + col];
-          const double fdy = fo + (double)k;   // dy = (o + k) - r
-          const int dy = o + k - RT;
-          const int v = p > 0.0 ? 1 : 0;
-          if (VAR == VAR_DF) {
-            a[0] += p;
-            a[1] = fma(p, p, a[1]);
-            a[2] = fma(fdy, p, a[2]);
-            bb[0] += v;
-            bb[1] += v * dy;
-            bb[2] += v * dy * dy;
-          } else {
-            const double p2 = p * p;
-            a[0] += p;
-            a[1] += p2;
-            a[2] = fma(fdy, p, a[2]);
-            a[3] = fma(fdy, p2, a[3]);
-            a[4] = fma(fdy * fdy, p2, a[4]);
-            bb[0] += v;
+          for (int k = 1; k < K; ++k) s1 = fma(p[k], p[k], s1);
+          int my = 0, myy = 0;
+#pragma unroll
+          for (int d = 1; d <= RT; ++d) {
+            const int vp = p[RT + d] > 0.0 ? 1 : 0, vm = p[RT - d] > 0.0 ? 1 : 0;
+            my += d * (vp - vm);
+            myy += d * d * (vp + vm);
           }
+          a[0] = s0;
+          a[1] = s1;
+          a[2] = s2;
+          bb[0] = m;
+          bb[1] = my;
+          bb[2] = myy;
+        } else {
+          double q[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) q[k] = p[k] * p[k];
+          double s1 = q[0];
+#pragma unroll
+          for (int k = 1; k < K; ++k) s1 += q[k];
+          double s3 = q[RT + 1] - q[RT - 1], s4 = q[RT + 1] + q[RT - 1];
+#pragma unroll
+          for (int d = 2; d <= RT; ++d) {
+            s3 = fma((double)d, q[RT + d] - q[RT - d], s3);
+            s4 = fma((double)(d * d), q[RT + d] + q[RT - d], s4);
+          }
+          a[0] = s0;
+          a[1] = s1;
+          a[2] = s2;
+          a[3] = s3;
+          a[4] = s4;
+          bb[0] = m;
         }
         const int cpos = (col & 3) * VQ + (col >> 2);
 #pragma unroll
@@ -365,7 +423,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       const int gxs = x0 + xs;
       if (gy < P.H && gxs < P.W) {
       const double txo = __ldg(P.tan_x + gxs);
-      const double tyo = __ldg(P.tan_y + y0);
+      const double tyo = __ldg(P.tan_y + (CENTRED ? gy : y0));  // origin row of dy
       const double ifx = P.ifx, ify = P.ify;
       const double* vrow = vd + orow * VRS;
       const int* irow = vi + orow * VRS;

@@ -9,7 +9,9 @@ import pytest
 import torch
 
 import paper_2103_06644_b200 as rf
-from paper_2103_06644_b200 import segment as S
+import importlib
+
+S = importlib.import_module("paper_2103_06644_b200.segment")  # the package also exports segment()
 from tests.helpers import GOLDEN_DIR
 
 pytestmark = pytest.mark.gpu

@@ -6,7 +6,9 @@ from __future__ import annotations
 import numpy as np
 import pytest
 
-from paper_2103_06644_b200 import segment as S
+import importlib
+
+S = importlib.import_module("paper_2103_06644_b200.segment")  # the package also exports segment()
 from paper_2103_06644_b200 import fitting as F
 
 
