@@ -36,6 +36,12 @@ __device__ __forceinline__ float fsqrt(float x) {
   return y;
 }
 
+__device__ __forceinline__ float frsqrt(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // acos on [-1, 1], |error| <= 2e-8 rad (Abramowitz & Stegun 4.4.46)
 __device__ __forceinline__ float facos(float x) {
   const float ax = fabsf(x);
@@ -58,7 +64,7 @@ __device__ __forceinline__ void trig_cubic(float a2, float a1, float a0, float& 
                                            float& l3) {
   const float q = a2 * (1.0f / 3.0f);
   const float p = fmaxf(fmaf(q, q, -a1 * (1.0f / 3.0f)), 1e-37f);
-  const float isp = rsqrtf(p);
+  const float isp = frsqrt(p);
   const float sp = p * isp;
   const float h = fmaf(q * q - 0.5f * a1, q, 0.5f * a0);
   const float c = fminf(fmaxf(h * isp * isp * isp, -1.0f), 1.0f);
@@ -132,36 +138,53 @@ static __device__ __noinline__ float curvature_slow(double t, double c1, double 
   return t > 0.0 ? (float)lk * frcp(ft) : 0.0f;
 }
 
-__device__ __forceinline__ float curvature_from(double t, double c1, double det, float ft, float k1,
-                                                float k2, float k3) {
-  const bool top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
-  // With a well separated bottom pair (relative gap > 20%) the fp32 seed (deflated,
-  // ~2e-6 relative) already meets the 1e-4 curvature tolerance with margin.
-  if (!top && (k2 - k1) >= 0.2f * k2) return t > 0.0 ? k1 * frcp(ft) : 0.0f;
-  // all three roots within 5%: iterate to convergence out of line (rare)
-  if (top ? (k3 - k2) < 0.05f * k3 : (k2 - k1) < 0.05f * k2)
-    return curvature_slow(t, c1, det, ft, k1, k2, k3, top);
-  // Common in the standard form (depth noise dominates: lam_max >> lam_2 ~ lam_min):
-  // two fp64 Newton steps on det(C - l I) -- on lam_max from its seed when the top gap
-  // is the better separated one (then deflate: lam_1 + lam_2 = t - lam_max,
-  // lam_1 lam_2 = det / lam_max), else on lam_min from below.  Same instructions on
-  // both sides, so the warp does not diverge.
-  double x = top ? (double)k3 : (double)k1 * (1.0 - 1e-5);
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const double P = fma(fma(t - x, x, -c1), x, det);
-    const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
-    x -= P * rcp_approx(dP);
-  }
-  float kmin = (float)x;
-  if (top) {
-    const double S = t - x;
-    const double Pp = det * rcp_fast(x);
+// Curvature in three pieces so that solve_window can interleave the curvature Newton
+// steps with its own (independent chains, half the latency):
+//  * curv_seed: fast exit (well separated bottom pair: the fp32 seed, deflated, ~2e-6
+//    relative, meets the 1e-4 tolerance), the rare all-close case, and the Newton start.
+//    Common in the standard form (depth noise dominates: lam_max >> lam_2 ~ lam_min): two
+//    fp64 Newton steps on det(C - l I) on lam_max from its seed when the top gap is the
+//    better separated one (then deflate: lam_1 + lam_2 = t - lam_max, lam_1 lam_2 =
+//    det / lam_max), else on lam_min from below.
+struct CurvSeed {
+  bool top, fast, close;
+  double x;
+};
+__device__ __forceinline__ CurvSeed curv_seed(float k1, float k2, float k3) {
+  CurvSeed c;
+  c.top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
+  c.fast = !c.top && (k2 - k1) >= 0.2f * k2;
+  c.close = c.top ? (k3 - k2) < 0.05f * k3 : (k2 - k1) < 0.05f * k2;
+  c.x = c.top ? (double)k3 : (double)k1 * (1.0 - 1e-5);
+  return c;
+}
+__device__ __forceinline__ double curv_newton(double t, double c1, double det, double x) {
+  const double P = fma(fma(t - x, x, -c1), x, det);
+  const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+  return x - P * rcp_approx(dP);
+}
+__device__ __forceinline__ float curv_finish(const CurvSeed& c, double t, double c1, double det, float ft,
+                                             float k1, float k2, float k3) {
+  if (c.fast) return t > 0.0 ? k1 * frcp(ft) : 0.0f;
+  if (c.close) return curvature_slow(t, c1, det, ft, k1, k2, k3, c.top);  // out of line, rare
+  float kmin = (float)c.x;
+  if (c.top) {
+    const double S = t - c.x;
+    const double Pp = det * rcp_fast(c.x);
     const float D = (float)fma(S, S, -4.0 * Pp);  // (lam_2 - lam_1)^2, cancellation-free in fp64
     const float fS = (float)S;
     kmin = 2.0f * (float)Pp * frcp(fS + fsqrt(fmaxf(D, 0.0f)));
   }
   return t > 0.0 ? kmin * frcp(ft) : 0.0f;
+}
+__device__ __forceinline__ float curvature_from(double t, double c1, double det, float ft, float k1,
+                                                float k2, float k3) {
+  CurvSeed c = curv_seed(k1, k2, k3);
+  if (!c.fast && !c.close) {
+    c.x = curv_newton(t, c1, det, c.x);
+    c.x = curv_newton(t, c1, det, c.x);
+  }
+  return curv_finish(c, t, c1, det, ft, k1, k2, k3);
 }
 
 // curvature when no implicit solve runs (explicit fits only)
@@ -318,27 +341,31 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
 
   double lam, lam2;
   const bool tie = (g2 - g1) < 0.05f * g2;
+  // (A) Newton on the quartic from the lower bound: monotone convergence; the
+  // curvature's two Newton steps on det(C - l I) run interleaved with the first two.
+  // Quadratic convergence, e_{k+1} ~ e_k^2 / (relative gap >= 5%): from
+  // e0 <= 1e-4 + lam1/n two steps leave < 1e-11 when lam1/n <= 1e-4, three when
+  // <= 1e-3; pathological windows (lam/n not small) iterate to convergence.
+  auto newton = [&](double x) {
+    const double x2 = x * x;
+    const double G = fma(fma(x - q3, x, q2), x2, fma(-q1, x, q0));
+    const double dG = fma(fma(fma(4.0, x, -3.0 * q3), x, 2.0 * q2), x, -q1);
+    return G * rcp_approx(dG);
+  };
+  CurvSeed cs = curv_seed(k1, k2, k3);
+  double l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    l -= newton(l);
+    cs.x = curv_newton(t, c1, det, cs.x);
+  }
   if (!tie) {
-    // (A) Newton on the quartic from the lower bound: monotone convergence,
-    // stop once the step is below 1e-9 relative (the remaining error is then
-    // ~step^2/gap).  Three steps in the common case; pathological windows
-    // (lam/n not small) take longer.
-    double l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
-    auto newton = [&](double x) {
-      const double x2 = x * x;
-      const double G = fma(fma(x - q3, x, q2), x2, fma(-q1, x, q0));
-      const double dG = fma(fma(fma(4.0, x, -3.0 * q3), x, 2.0 * q2), x, -q1);
-      return G * rcp_approx(dG);
-    };
-    // quadratic convergence, e_{k+1} ~ e_k^2 / (relative gap >= 5%): from
-    // e0 <= 1e-4 + lam1/n two steps leave < 1e-11 when lam1/n <= 1e-4, three when <= 1e-3
-    l -= newton(l);
-    l -= newton(l);
     if (grel > 1e-4f) l -= newton(l);
     if (grel > 1e-3f) l = newton_converge(q3, q2, q1, q0, l);  // large-residual windows (rare)
     lam = l;
     lam2 = (double)g2;
   } else {
+    // (B) near-tie lam1 ~ lam2: exact deflation (rare)
     tie_deflation(q3, q2, q1, q0, lam, lam2);
   }
 
@@ -398,7 +425,7 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
   }
 
   // curvature: lam_min(C) / tr(C)
-  out.kappa = curvature_from(t, c1, det, ft, k1, k2, k3);
+  out.kappa = curv_finish(cs, t, c1, det, ft, k1, k2, k3);
 }
 
 // canonical sign + unit normal / offset (fitting.py:76-94 and SURVEY A18)
@@ -411,13 +438,13 @@ __device__ __forceinline__ void finish_plane(double a, double b, double c, doubl
   const double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023 - e)
   const float fa = (float)(a * sc), fb = (float)(b * sc), fc = (float)(c * sc),
               fd = (float)(d * sc);
-  const float n4 = rsqrtf(fa * fa + fb * fb + fc * fc + fd * fd);
+  const float n4 = frsqrt(fa * fa + fb * fb + fc * fc + fd * fd);
   float sign = 1.0f;
   if (fabsf(fc * n4) > 1e-9f) sign = fc > 0.0f ? 1.0f : -1.0f;
   else if (fabsf(fb * n4) > 1e-9f) sign = fb > 0.0f ? 1.0f : -1.0f;
   else if (fabsf(fa * n4) > 1e-9f) sign = fa > 0.0f ? 1.0f : -1.0f;
   else if (fd < 0.0f) sign = -1.0f;
-  const float in3 = sign * rsqrtf(fa * fa + fb * fb + fc * fc);
+  const float in3 = sign * frsqrt(fa * fa + fb * fb + fc * fc);
   nx = fa * in3;
   ny = fb * in3;
   nz = fc * in3;
