@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define RF_ABI_VERSION 2
+#define RF_ABI_VERSION 3
 
 typedef enum rf_status {
   RF_OK = 0,
@@ -40,8 +40,10 @@ typedef enum rf_status {
 /* depth element types (reference DepthImage, synth.py:69-114) */
 typedef enum rf_depth_dtype {
   RF_DEPTH_F32_M = 0,   /* float32 metres; valid = isfinite & > 0 (synth.py:84)     */
-  RF_DEPTH_U16_MM = 1   /* uint16 millimetres; Z = mm / 1000.0, valid = mm > 0
+  RF_DEPTH_U16_MM = 1,  /* uint16 millimetres; Z = mm / 1000.0, valid = mm > 0
                            (DepthImage.from_millimeters, synth.py:111-114)         */
+  RF_DEPTH_F64_M = 2    /* float64 metres (DepthImage.values as held by the reference);
+                           only rf_build_channel accepts it                         */
 } rf_depth_dtype;
 
 /* formulation ids = positions in the reference's FORMULATIONS tuple (fitting.py:45-49) */
@@ -146,6 +148,55 @@ int32_t rf_launches_per_call(int32_t formulation_mask);
 
 /* Thread-local message describing the last non-RF_OK status. */
 const char* rf_last_error(void);
+
+/* ---- the reference's integral backend on the device (8b) ----
+ * Channels of the reference's ChannelStacks (integral.py:36-47, 188-325).  Depth-derived
+ * channels are masked by validity (0 where invalid); the constant tan monomials are not. */
+typedef enum rf_channel {
+  RF_CH_COUNT = 0,      /* validity as 0/1 (the per-frame "count" channel)            */
+  RF_CH_ONES = 1,       /* every pixel (the constant stack's count)                  */
+  RF_CH_X2 = 2, RF_CH_XY = 3, RF_CH_XZ = 4, RF_CH_X = 5, RF_CH_Y2 = 6, RF_CH_YZ = 7,
+  RF_CH_Y = 8, RF_CH_Z2 = 9, RF_CH_Z = 10,            /* X = Z tan_x, Y = Z tan_y   */
+  RF_CH_TX_OVER_Z = 11, RF_CH_TY_OVER_Z = 12, RF_CH_INV_Z = 13, RF_CH_INV_Z2 = 14,
+  RF_CH_TX2 = 15, RF_CH_TXTY = 16, RF_CH_TY2 = 17, RF_CH_TX = 18, RF_CH_TY = 19,
+  RF_CH_M_TX2 = 20, RF_CH_M_TXTY = 21, RF_CH_M_TY2 = 22, RF_CH_M_TX = 23, RF_CH_M_TY = 24
+} rf_channel;
+#define RF_NUM_CHANNELS 25
+#define RF_MAX_BOX_CHANNELS 32
+
+/* Replaces build_integral(channel(depth), valid) (integral.py:136-149) for one channel of
+ * one frame: table is a device [height+1][width+1] fp64 array (row 0 and column 0 zero).
+ * The additions are numpy's (cumsum down each column, then along each row, sequential), so
+ * the table equals the reference's bit for bit.  mask: optional device uint8 [H][W]. */
+rf_status rf_build_channel(const rf_tables* tables, const void* depth, int dtype, int64_t row_pitch,
+                           const uint8_t* mask, int32_t channel, double* table, void* stream);
+
+/* build_integral(src, mask) (integral.py:136-149) for an arbitrary fp64 device channel
+ * [height][src_pitch]; mask optional. */
+rf_status rf_integral(const double* src, int64_t src_pitch, const uint8_t* mask, int32_t height,
+                      int32_t width, double* table, void* stream);
+
+/* _box / box_sum (fitting.py:405-411, integral.py:152-158) of nch tables (a HOST array of
+ * device table pointers, each [height+1][width+1]) over nrects device rects (the frame field
+ * is ignored): out[r][c] = t[y1,x1] - t[y0,x1] - t[y1,x0] + t[y0,x0], evaluated in that
+ * order.  Out-of-bounds rects give NaN (callers check bounds, integral.py:131-133). */
+rf_status rf_box_sums(const double* const* tables, int32_t nch, int32_t height, int32_t width,
+                      const rf_rect* rects, int64_t nrects, double* out, void* stream);
+
+#define RF_RECT_JACOBI_FAILED 8u  /* jacobi_eigh did not converge (DegenerateFitError)  */
+
+/* Replaces FIT_BY_FORMULATION[formulation](scatter) (fitting.py:546-629) for n assembled
+ * systems, all device arrays: matrices [n][16] (row-major 4x4 Scatter4.matrix; explicit: the
+ * 3x3 Scatter3.matrix in the top-left, row stride 4), rhs [n][3] (explicit only, else NULL),
+ * target_sq [n] (explicit, NaN = absent; may be NULL), counts [n] (Scatter*.n).
+ * Implicit: the smallest eigenpair through the same solve as the per-pixel kernels (Schur
+ * complement on the constant monomial; cyclic Jacobi when that entry is not positive).
+ * Explicit: the reference's Cholesky (pivot floor 1e-12 trace) or, when rank-deficient, the
+ * minimum-norm solution from a cyclic Jacobi (fitting.py:264-327).  Results as rf_rect_fit
+ * (rms NaN where the reference returns None). */
+rf_status rf_fit_scatters(const double* matrices, const double* rhs, const double* target_sq,
+                          const int64_t* counts, int64_t n, int32_t formulation, rf_rect_fit* out,
+                          void* stream);
 
 /* RF_ABI_VERSION of the loaded library. */
 int32_t rf_abi_version(void);

@@ -23,6 +23,7 @@ RF_ERR_UNSUPPORTED = 4
 
 RF_DEPTH_F32_M = 0
 RF_DEPTH_U16_MM = 1
+RF_DEPTH_F64_M = 2
 
 RF_FORM_IMPLICIT_STANDARD = 0
 RF_FORM_IMPLICIT_RGBD = 1
@@ -33,11 +34,23 @@ RF_IMPLICIT_STANDARD = 1 << RF_FORM_IMPLICIT_STANDARD
 RF_IMPLICIT_RGBD = 1 << RF_FORM_IMPLICIT_RGBD
 RF_EXPLICIT_STANDARD = 1 << RF_FORM_EXPLICIT_STANDARD
 RF_EXPLICIT_RGBD = 1 << RF_FORM_EXPLICIT_RGBD
-RF_ABI_VERSION = 2
+RF_ABI_VERSION = 3
 
 RF_PIX_INPUT_VALID = 1
 RF_PIX_FIT = 2
 RF_PIX_DEGENERATE = 4
+
+RF_RECT_JACOBI_FAILED = 8
+
+# rf_channel ids (integral.py channel names)
+RF_CHANNELS = {
+    "count": 0, "ones": 1,
+    "x2": 2, "xy": 3, "xz": 4, "x": 5, "y2": 6, "yz": 7, "y": 8, "z2": 9, "z": 10,
+    "tx_over_z": 11, "ty_over_z": 12, "inv_z": 13, "inv_z2": 14,
+    "tx2": 15, "txty": 16, "ty2": 17, "tx": 18, "ty": 19,
+    "m_tx2": 20, "m_txty": 21, "m_ty2": 22, "m_tx": 23, "m_ty": 24,
+}
+RF_MAX_BOX_CHANNELS = 32
 
 # every symbol include/rangefit_b200.h declares
 EXPORTED_SYMBOLS = (
@@ -45,6 +58,10 @@ EXPORTED_SYMBOLS = (
     "rf_tables_destroy",
     "rf_fit_pixels",
     "rf_fit_rects",
+    "rf_build_channel",
+    "rf_integral",
+    "rf_box_sums",
+    "rf_fit_scatters",
     "rf_launches_per_call",
     "rf_last_error",
     "rf_abi_version",
@@ -104,6 +121,15 @@ def load() -> ctypes.CDLL:
         vp, ctypes.c_int64, ctypes.c_int32, vp, vp,
     ]
     L.rf_fit_rects.restype = ctypes.c_int
+    L.rf_build_channel.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int64, vp, ctypes.c_int32, vp, vp]
+    L.rf_build_channel.restype = ctypes.c_int
+    L.rf_integral.argtypes = [vp, ctypes.c_int64, vp, ctypes.c_int32, ctypes.c_int32, vp, vp]
+    L.rf_integral.restype = ctypes.c_int
+    L.rf_box_sums.argtypes = [ctypes.POINTER(vp), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp,
+                              ctypes.c_int64, vp, vp]
+    L.rf_box_sums.restype = ctypes.c_int
+    L.rf_fit_scatters.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int32, vp, vp]
+    L.rf_fit_scatters.restype = ctypes.c_int
     L.rf_launches_per_call.argtypes = [ctypes.c_int32]
     L.rf_launches_per_call.restype = ctypes.c_int32
     L.rf_last_error.argtypes = []

@@ -62,21 +62,6 @@ __device__ __forceinline__ long long block_sum_ll(long long v, long long* red) {
   return t;
 }
 
-// canonicalize_implicit (fitting.py:76-94) in fp64
-__device__ void canonical4(double a, double b, double c, double d, double* out) {
-  const double nrm = sqrt(a * a + b * b + c * c + d * d);
-  double u[4] = {a / nrm, b / nrm, c / nrm, d / nrm};
-  double sign = 1.0;
-  const int order[4] = {2, 1, 0, 3};
-  for (int k = 0; k < 4; ++k) {
-    if (fabs(u[order[k]]) > 1e-9) {
-      sign = u[order[k]] > 0.0 ? 1.0 : -1.0;
-      break;
-    }
-  }
-  for (int k = 0; k < 4; ++k) out[k] = sign * u[k];
-}
-
 __global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams P) {
   __shared__ double redd[RT_THREADS / 32];
   __shared__ long long redl[RT_THREADS / 32];

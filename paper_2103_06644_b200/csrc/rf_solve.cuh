@@ -451,6 +451,20 @@ __device__ __forceinline__ void finish_plane(double a, double b, double c, doubl
   off = fd * in3;
 }
 
-// ---- TMA / mbarrier helpers (sm_90+ async proxy; SASS UTMALDG + SYNCS)
+// canonicalize_implicit (fitting.py:76-94) in fp64
+__device__ __forceinline__ void canonical4(double a, double b, double c, double d, double* out) {
+  const double nrm = sqrt(a * a + b * b + c * c + d * d);
+  double u[4] = {a / nrm, b / nrm, c / nrm, d / nrm};
+  double sign = 1.0;
+  const int order[4] = {2, 1, 0, 3};
+  for (int k = 0; k < 4; ++k) {
+    if (fabs(u[order[k]]) > 1e-9) {
+      sign = u[order[k]] > 0.0 ? 1.0 : -1.0;
+      break;
+    }
+  }
+  for (int k = 0; k < 4; ++k) out[k] = sign * u[k];
+}
+
 
 }  // namespace rf_dev

@@ -7,9 +7,15 @@ Names, signatures and error behaviour follow ``/root/reference/pkg/src/rangefit`
 * ``Rect`` (``integral.py:50-66``), ``canonicalize_implicit``, ``ImplicitPlane``,
   ``ExplicitPlane``, ``FitResult``, ``explicit_to_implicit``, ``normal_angle``
   (``fitting.py:76-174, 729-754``) -- small host-side value types;
-* ``fit_rect(depth, maps, rect, formulation, backend="b200", ...)`` (``fitting.py:757-786``)
-  with a new ``"b200"`` backend (the reference's plugin point), and the batched
-  ``fit_rects`` it is built on (``rf_fit_rects``, one CTA per rect, direct sums).
+* ``Scatter4``, ``Scatter3``, ``scatter_from_integrals``, ``fit_implicit_standard``,
+  ``fit_implicit_rgbd``, ``fit_explicit_standard``, ``fit_explicit_rgbd``,
+  ``FIT_BY_FORMULATION``, ``ExplicitRgbdFitter`` (``fitting.py:135-157, 420-739``): the
+  assembled systems are solved on the device (``rf_fit_scatters``), box sums come from the
+  device summed-area tables of ``integral.py`` (``rf_box_sums``);
+* ``fit_rect(depth, maps, rect, formulation, backend="b200", ...)`` (``fitting.py:757-786``):
+  ``"b200"`` / ``"naive"`` = the batched direct-sum rect kernel (``rf_fit_rects``, one CTA
+  per rect -- the naive backend's numerics), ``"integral"`` = the device integral backend;
+* ``CSV_HEADER`` and ``fit_result_csv_row`` (``fitting.py:73, 789-813``).
 
 The fits themselves always run on the GPU through ``librangefit_b200.so``.
 """
@@ -40,7 +46,10 @@ from .pixels import (
 SPACE_STANDARD = "standard"
 SPACE_RGBD = "rgbd"
 _CANONICAL_EPS = 1e-9
-BACKENDS = ("b200",)
+BACKENDS = ("b200", "naive", "integral")
+CSV_HEADER = "formulation,backend,x0,y0,x1,y1,a,b,c,d,lambda,rms,n_points"
+_EIGEN_TIE_REL = 1e-9
+_PIVOT_REL = 1e-12
 
 
 class InsufficientSamplesError(ValueError):
@@ -217,17 +226,272 @@ def _result(row, formulation: str) -> FitResult:
                      degenerate, float(row["curvature"]))
 
 
+@dataclass(frozen=True)
+class Scatter4:
+    """Symmetric 4x4 scatter matrix (sum of outer products) and sample count (fitting.py:135-140)."""
+
+    matrix: np.ndarray
+    n: int
+
+
+@dataclass(frozen=True)
+class Scatter3:
+    """3x3 normal equations, right-hand side, count, optional sum of squared targets
+    (fitting.py:143-156)."""
+
+    matrix: np.ndarray
+    rhs: np.ndarray
+    n: int
+    target_sq: float | None = None
+
+
+def _check_formulation(formulation: str) -> None:
+    if formulation not in _FORM_ID:
+        raise ValueError(f"unknown formulation {formulation!r}; expected one of {FORMULATIONS}")
+
+
+def _require_n(n: int, minimum: int) -> None:
+    if n < minimum:
+        raise InsufficientSamplesError(f"fit needs at least {minimum} samples, got {n}")
+
+
+def _check_matrix(m: np.ndarray, size: int) -> np.ndarray:
+    """jacobi_eigh's / cholesky3's input checks (fitting.py:201-208, 270-272)."""
+    a = np.asarray(m, dtype=np.float64)
+    if a.shape != (size, size):
+        raise ValueError(f"expected a {size}x{size} matrix, got shape {a.shape}")
+    if size == 4:
+        if not np.all(np.isfinite(a)):
+            raise ValueError("matrix holds non-finite entries")
+        fro = float(np.linalg.norm(a))
+        if float(np.abs(a - a.T).max()) > 1e-12 * max(fro, 1.0):
+            raise ValueError("matrix is not symmetric")
+    return a
+
+
+def fit_scatters(matrices, counts, formulation: str, rhs=None, target_sq=None, device=None) -> np.ndarray:
+    """Solve many assembled systems on the device in one launch (``rf_fit_scatters``).
+
+    matrices [n,4,4] (implicit) or [n,3,3] (explicit), counts [n], rhs [n,3] and target_sq [n]
+    (explicit; NaN = absent).  Returns a structured array of ``RECT_FIT_DTYPE``."""
+    _check_formulation(formulation)
+    explicit_fit = formulation in (EXPLICIT_STANDARD, EXPLICIT_RGBD)
+    m = np.asarray(matrices, dtype=np.float64)
+    size = 3 if explicit_fit else 4
+    m = m.reshape(-1, size, size)
+    n = m.shape[0]
+    full = np.zeros((n, 4, 4))
+    full[:, :size, :size] = m
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+    d_m = torch.from_numpy(full.reshape(n, 16)).to(dev)
+    d_c = torch.from_numpy(np.asarray(counts, dtype=np.int64).reshape(n)).to(dev)
+    d_rhs = d_tq = None
+    if explicit_fit:
+        if rhs is None:
+            raise ValueError("explicit systems need a right-hand side")
+        d_rhs = torch.from_numpy(np.asarray(rhs, dtype=np.float64).reshape(n, 3)).to(dev)
+        tq = np.full(n, np.nan) if target_sq is None else np.asarray(
+            [np.nan if v is None else v for v in np.atleast_1d(np.asarray(target_sq, dtype=object))],
+            dtype=np.float64)
+        d_tq = torch.from_numpy(tq.reshape(n)).to(dev)
+    out = torch.empty((n, RECT_FIT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+    st = N.load().rf_fit_scatters(d_m.data_ptr(), d_rhs.data_ptr() if d_rhs is not None else None,
+                                  d_tq.data_ptr() if d_tq is not None else None, d_c.data_ptr(), n,
+                                  _FORM_ID[formulation], out.data_ptr(),
+                                  ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    N.check(st, "fit_scatters")
+    return out.cpu().numpy().view(RECT_FIT_DTYPE).reshape(-1)
+
+
+RECT_JACOBI_FAILED = N.RF_RECT_JACOBI_FAILED
+
+
+def _scatter_result(row, formulation: str, n: int) -> FitResult:
+    if row["status"] & RECT_JACOBI_FAILED:
+        raise DegenerateFitError("eigen iteration did not converge; ill-posed scatter matrix")
+    degenerate = bool(row["status"] & RECT_DEGENERATE)
+    rms = float(row["rms"])
+    curv = float(row["curvature"])
+    curv = None if math.isnan(curv) else curv
+    if formulation in (IMPLICIT_STANDARD, IMPLICIT_RGBD):
+        return FitResult(ImplicitPlane(row["coef"]), n, rms, float(row["eigenvalue"]), degenerate, curv)
+    space = SPACE_STANDARD if formulation == EXPLICIT_STANDARD else SPACE_RGBD
+    return FitResult(ExplicitPlane(np.array(row["explicit_coef"]), space), n,
+                     None if math.isnan(rms) else rms, None, degenerate, curv)
+
+
+def _fit_implicit(scatter: Scatter4, formulation: str) -> FitResult:
+    _require_n(scatter.n, 4)
+    a = _check_matrix(scatter.matrix, 4)
+    row = fit_scatters(a[None], [scatter.n], formulation)[0]
+    return _scatter_result(row, formulation, scatter.n)
+
+
+def fit_implicit_standard(scatter: Scatter4) -> FitResult:
+    """Implicit fit on [X, Y, Z, 1] monomials: smallest scatter eigenpair (fitting.py:562-568)."""
+    return _fit_implicit(scatter, IMPLICIT_STANDARD)
+
+
+def fit_implicit_rgbd(scatter: Scatter4) -> FitResult:
+    """Implicit fit on [tan_x, tan_y, 1, 1/Z]; the eigenvector is the XYZ plane (fitting.py:571-579)."""
+    return _fit_implicit(scatter, IMPLICIT_RGBD)
+
+
+def _fit_explicit(scatter: Scatter3, formulation: str) -> FitResult:
+    _require_n(scatter.n, 3)
+    a = np.asarray(scatter.matrix, dtype=np.float64)
+    if a.shape != (3, 3):
+        raise ValueError(f"expected a 3x3 matrix, got shape {a.shape}")
+    row = fit_scatters(a[None], [scatter.n], formulation, rhs=np.asarray(scatter.rhs, dtype=np.float64)[None],
+                       target_sq=[scatter.target_sq])[0]
+    return _scatter_result(row, formulation, scatter.n)
+
+
+def fit_explicit_standard(scatter: Scatter3) -> FitResult:
+    """Explicit fit Z = aX + bY + c via the normal equations (fitting.py:602-609)."""
+    return _fit_explicit(scatter, EXPLICIT_STANDARD)
+
+
+def fit_explicit_rgbd(scatter: Scatter3) -> FitResult:
+    """Explicit fit 1/Z = a tan_x + b tan_y + c via the normal equations (fitting.py:612-621)."""
+    return _fit_explicit(scatter, EXPLICIT_RGBD)
+
+
+FIT_BY_FORMULATION = {
+    IMPLICIT_STANDARD: fit_implicit_standard,
+    IMPLICIT_RGBD: fit_implicit_rgbd,
+    EXPLICIT_STANDARD: fit_explicit_standard,
+    EXPLICIT_RGBD: fit_explicit_rgbd,
+}
+
+
+def _require_channels(stack, names, what: str) -> None:
+    missing = [name for name in names if name not in stack.channels]
+    if missing:
+        raise ValueError(f"{what} stack is missing channels: {', '.join(missing)}")
+
+
+def scatter_from_integrals(stack, constant, rect, formulation: str):
+    """Assemble a window's scatter system from device box sums (fitting.py:420-533): same
+    channel choice (camera-constant tan block for hole-free windows, the frame's masked tan
+    channels otherwise), same checks and errors; the box sums run in one device launch."""
+    from . import integral as I
+
+    _check_formulation(formulation)
+    rect = Rect(*rect)
+    I._check_rect(rect, stack.width, stack.height)
+    names = list(stack.channels)
+    tables = [stack.count.table] + [stack.channels[k].table for k in names]
+    cnames = []
+    if constant is not None and formulation in (IMPLICIT_RGBD, EXPLICIT_RGBD):
+        if tuple(constant.count.table.shape) != tuple(stack.count.table.shape):
+            raise ValueError("constant stack dimensions do not match the per-frame stack")
+        cnames = [k for k in ("tx2", "txty", "ty2", "tx", "ty") if k in constant.channels]
+        tables += [constant.channels[k].table for k in cnames]
+    sums = I.box_sums(tables, [rect])[0]
+    n = int(round(float(sums[0])))
+    if n < MIN_SAMPLES[formulation]:
+        raise InsufficientSamplesError(
+            f"window {rect} holds {n} valid samples; {formulation} needs {MIN_SAMPLES[formulation]}")
+    box = dict(zip(names, (float(v) for v in sums[1:1 + len(names)])))
+    cbox = dict(zip(cnames, (float(v) for v in sums[1 + len(names):])))
+    if formulation == IMPLICIT_STANDARD:
+        _require_channels(stack, ("x2", "xy", "xz", "x", "y2", "yz", "y", "z2", "z"), "per-frame")
+        b = box
+        matrix = np.array([[b["x2"], b["xy"], b["xz"], b["x"]],
+                           [b["xy"], b["y2"], b["yz"], b["y"]],
+                           [b["xz"], b["yz"], b["z2"], b["z"]],
+                           [b["x"], b["y"], b["z"], float(n)]])
+        return Scatter4(matrix=matrix, n=n)
+    if formulation == EXPLICIT_STANDARD:
+        _require_channels(stack, ("x2", "xy", "x", "y2", "y", "xz", "yz", "z"), "per-frame")
+        b = box
+        matrix = np.array([[b["x2"], b["xy"], b["x"]], [b["xy"], b["y2"], b["y"]], [b["x"], b["y"], float(n)]])
+        rhs = np.array([b["xz"], b["yz"], b["z"]])
+        return Scatter3(matrix=matrix, rhs=rhs, n=n, target_sq=b.get("z2"))
+    if n == rect.area:
+        if constant is None:
+            raise ValueError(f"{formulation} requires the camera-constant channel stack")
+        _require_channels(constant, ("tx2", "txty", "ty2", "tx", "ty"), "constant")
+        t = cbox
+        stx2, stxty, sty2, stx, sty = t["tx2"], t["txty"], t["ty2"], t["tx"], t["ty"]
+    else:
+        if not stack.hole_corrected:
+            raise ValueError(f"window {rect} contains invalid pixels but the frame stack carries "
+                             "no masked tan channels (was it built from a different frame?)")
+        b = box
+        stx2, stxty, sty2, stx, sty = b["m_tx2"], b["m_txty"], b["m_ty2"], b["m_tx"], b["m_ty"]
+    pixel_count = float(n)
+    b = box
+    if formulation == IMPLICIT_RGBD:
+        _require_channels(stack, ("tx_over_z", "ty_over_z", "inv_z", "inv_z2"), "per-frame")
+        matrix = np.array([[stx2, stxty, stx, b["tx_over_z"]],
+                           [stxty, sty2, sty, b["ty_over_z"]],
+                           [stx, sty, pixel_count, b["inv_z"]],
+                           [b["tx_over_z"], b["ty_over_z"], b["inv_z"], b["inv_z2"]]])
+        return Scatter4(matrix=matrix, n=n)
+    _require_channels(stack, ("tx_over_z", "ty_over_z", "inv_z"), "per-frame")
+    matrix = np.array([[stx2, stxty, stx], [stxty, sty2, sty], [stx, sty, pixel_count]])
+    rhs = np.array([b["tx_over_z"], b["ty_over_z"], b["inv_z"]])
+    return Scatter3(matrix=matrix, rhs=rhs, n=n, target_sq=b.get("inv_z2"))
+
+
+class ExplicitRgbdFitter:
+    """Explicit inverse-depth fits over a camera-constant stack (fitting.py:632-726).
+
+    The reference caches each window's Cholesky factor on the host; on the device the 3x3
+    system is refactored per fit (cheaper than a cache lookup), so ``fit`` is
+    ``fit_explicit_rgbd(scatter_from_integrals(stack, constant, rect, EXPLICIT_RGBD))``."""
+
+    def __init__(self, constant):
+        _require_channels(constant, ("tx2", "txty", "ty2", "tx", "ty"), "constant")
+        self.constant = constant
+
+    def matrix_for(self, rect) -> np.ndarray:
+        from . import integral as I
+
+        rect = Rect(*rect)
+        I._check_rect(rect, self.constant.width, self.constant.height)
+        c = self.constant.channels
+        s = I.box_sums([c["tx2"].table, c["txty"].table, c["ty2"].table, c["tx"].table, c["ty"].table,
+                        self.constant.count.table], [rect])[0]
+        return np.array([[s[0], s[1], s[3]], [s[1], s[2], s[4]], [s[3], s[4], s[5]]])
+
+    def fit(self, stack, rect) -> FitResult:
+        return fit_explicit_rgbd(scatter_from_integrals(stack, self.constant, rect, EXPLICIT_RGBD))
+
+
 def fit_rect(depth, maps: TanAngleMaps, rect: Rect, formulation: str, backend: str = "b200",
              stack=None, constant=None, rgbd_fitter=None) -> FitResult:
-    """One window, reference signature (fitting.py:757-766).  ``backend`` must be ``"b200"``;
-    ``stack``/``constant``/``rgbd_fitter`` are accepted for signature compatibility and unused
-    (the device path sums each rect directly)."""
+    """One window, reference signature (fitting.py:757-786).
+
+    ``"b200"`` and ``"naive"``: direct sums over the rect on the device (``rf_fit_rects``, the
+    naive backend's numerics).  ``"integral"``: the scatter assembled from the device channel
+    stacks (``stack`` required; ``constant`` for the rgbd formulations), solved on the device."""
     if backend not in BACKENDS:
         raise ValueError(f"unknown backend {backend!r}; expected one of {BACKENDS}")
     if formulation not in _FORM_ID:
         raise ValueError(f"unknown formulation {formulation!r}; expected one of {FORMULATIONS}")
+    if backend == "integral":
+        if stack is None:
+            raise ValueError("integral backend requires a per-frame channel stack")
+        if formulation == EXPLICIT_RGBD and rgbd_fitter is not None:
+            return rgbd_fitter.fit(stack, rect)
+        return FIT_BY_FORMULATION[formulation](scatter_from_integrals(stack, constant, rect, formulation))
     x0, y0, x1, y1 = (int(v) for v in rect)
     if not (0 <= x0 <= x1 <= maps.width and 0 <= y0 <= y1 <= maps.height):
         raise ValueError(f"rect {tuple(rect)} out of bounds for {maps.width}x{maps.height} image")
     row = fit_rects(depth, maps, [(x0, y0, x1, y1)], formulation)[0]
     return _result(row, formulation)
+
+
+def fit_result_csv_row(result: FitResult, formulation: str, backend: str, rect) -> str:
+    """One CSV row per fit; explicit fits are reported in implicit form (fitting.py:789-813)."""
+    rect = Rect(*rect)
+    coef = (explicit_to_implicit(result.plane).coefficients if isinstance(result.plane, ExplicitPlane)
+            else result.plane.coefficients)
+    lam = "" if result.eigenvalue is None else repr(result.eigenvalue)
+    rms = "" if result.rms_residual is None else repr(result.rms_residual)
+    fields = [formulation, backend, str(rect.x0), str(rect.y0), str(rect.x1), str(rect.y1),
+              *(repr(float(c)) for c in coef[:4]), lam, rms, str(result.n_points)]
+    return ",".join(fields)

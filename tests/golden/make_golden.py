@@ -191,6 +191,108 @@ def run_segment(name, cam, depth_img, stored, formulations=FORMS):
     np.savez_compressed(HERE / f"{name}.npz", **out)
 
 
+def run_integral(name, cam, depth_img, stored, rng, count=40):
+    """The reference's integral backend (integral.py:136-325, fitting.py:405-739): every
+    channel table of the five stacks, scatter_from_integrals + FIT_BY_FORMULATION on random
+    rects, and fit_implicit_* / fit_explicit_* on hand-made systems (Jacobi fallback,
+    rank-deficient explicit systems)."""
+    from rangefit.fitting import (Scatter3, Scatter4, fit_explicit_rgbd, fit_explicit_standard,
+                                  fit_implicit_rgbd, fit_implicit_standard, scatter_from_integrals)
+    from rangefit.integral import (build_constant_channels, build_rgbd_explicit_channels,
+                                   build_rgbd_implicit_channels, build_standard_explicit_channels,
+                                   build_standard_implicit_channels)
+
+    maps = rf.compute_tan_maps(cam)
+    W, H = cam.width, cam.height
+    out = {"depth": stored, "valid": depth_img.valid, "fx": cam.fx, "fy": cam.fy, "cx": cam.cx, "cy": cam.cy}
+    stacks = {"const": build_constant_channels(maps),
+              "std": build_standard_implicit_channels(depth_img, maps),
+              "rgbd": build_rgbd_implicit_channels(depth_img, maps),
+              "xstd": build_standard_explicit_channels(depth_img, maps),
+              "xrgbd": build_rgbd_explicit_channels(depth_img, maps)}
+    for key, st in stacks.items():
+        out[f"{key}_count"] = st.count.table
+        out[f"{key}_names"] = np.array(list(st.channels))
+        out[f"{key}_hole_corrected"] = st.hole_corrected
+        for cname, img in st.channels.items():
+            out[f"{key}_t_{cname}"] = img.table
+    rects = [(0, 0, W, H), (0, 0, 2, 2), (W - 3, H - 1, W, H), (3, 3, 3, 9)]
+    while len(rects) < count:
+        x0, y0 = int(rng.integers(0, W - 1)), int(rng.integers(0, H - 1))
+        rects.append((x0, y0, int(rng.integers(x0 + 1, min(W, x0 + 12) + 1)),
+                      int(rng.integers(y0 + 1, min(H, y0 + 12) + 1))))
+    out["rects"] = np.array(rects, np.int32)
+    for form in FORMS:
+        key = KEYS[form]
+        st = stacks[key]
+        n_r = len(rects)
+        mats = np.full((n_r, 4, 4), np.nan)
+        rhs = np.full((n_r, 3), np.nan)
+        tq = np.full(n_r, np.nan)
+        npts = np.full(n_r, -1, np.int64)
+        coef = np.full((n_r, 4), np.nan)
+        xcoef = np.full((n_r, 3), np.nan)
+        lam = np.full(n_r, np.nan)
+        rms = np.full(n_r, np.nan)
+        deg = np.zeros(n_r, bool)
+        for k, r in enumerate(rects):
+            try:
+                sc = scatter_from_integrals(st, stacks["const"], rf.Rect(*r), form)
+            except rf.InsufficientSamplesError:
+                continue
+            npts[k] = sc.n
+            m = np.asarray(sc.matrix)
+            mats[k, :m.shape[0], :m.shape[1]] = m
+            if isinstance(sc, Scatter3):
+                rhs[k] = sc.rhs
+                tq[k] = np.nan if sc.target_sq is None else sc.target_sq
+            res = FIT_BY_FORMULATION[form](sc)
+            deg[k] = res.degenerate
+            rms[k] = np.nan if res.rms_residual is None else res.rms_residual
+            if isinstance(res.plane, ExplicitPlane):
+                xcoef[k] = res.plane.coefficients
+                coef[k] = explicit_to_implicit(res.plane).coefficients
+            else:
+                coef[k] = res.plane.coefficients
+                lam[k] = res.eigenvalue
+        out.update({f"{key}_mat": mats, f"{key}_rhs": rhs, f"{key}_tq": tq, f"{key}_n": npts,
+                    f"{key}_coef": coef, f"{key}_xcoef": xcoef, f"{key}_lam": lam, f"{key}_rms": rms,
+                    f"{key}_deg": deg})
+    # hand-made systems: a known answer (diag(4,3,2,1) -> e4, lam 1), a zero constant-monomial
+    # entry (Jacobi path), collinear explicit samples (pinv path, degenerate)
+    special4 = [np.diag([4.0, 3.0, 2.0, 1.0]), np.diag([1.0, 2.0, 3.0, 0.0]),
+                np.array([[5.0, 1.0, 0.5, 2.0], [1.0, 4.0, 0.2, 1.0], [0.5, 0.2, 3.0, 0.5], [2.0, 1.0, 0.5, 6.0]])]
+    for key, fit in (("sp_std", fit_implicit_standard), ("sp_rgbd", fit_implicit_rgbd)):
+        c, l, d = [], [], []
+        for m in special4:
+            res = fit(Scatter4(matrix=m, n=4))
+            c.append(res.plane.coefficients)
+            l.append(res.eigenvalue)
+            d.append(res.degenerate)
+        out[f"{key}_coef"], out[f"{key}_lam"], out[f"{key}_deg"] = np.array(c), np.array(l), np.array(d)
+    out["special4"] = np.array(special4)
+    xs = np.array([0.0, 1.0, 2.0, 3.0])
+    ys = 2.0 * xs + 1.0                   # collinear samples: rank-deficient normal equations
+    zs = 0.5 * xs - 0.25 * ys + 2.0
+    m = np.column_stack((xs, ys, np.ones_like(xs)))
+    special3 = [(m.T @ m, m.T @ zs, float(zs @ zs))]
+    m2 = np.column_stack((xs, xs ** 2, np.ones_like(xs)))
+    special3.append((m2.T @ m2, m2.T @ zs, float(zs @ zs)))
+    for key, fit in (("sp_xstd", fit_explicit_standard), ("sp_xrgbd", fit_explicit_rgbd)):
+        c, d, r = [], [], []
+        for (a, b, t) in special3:
+            res = fit(Scatter3(matrix=a, rhs=b, n=4, target_sq=t))
+            c.append(res.plane.coefficients)
+            d.append(res.degenerate)
+            r.append(res.rms_residual)
+        out[f"{key}_coef"], out[f"{key}_deg"], out[f"{key}_rms"] = np.array(c), np.array(d), np.array(r)
+    out["special3_mat"] = np.array([a for a, _, _ in special3])
+    out["special3_rhs"] = np.array([b for _, b, _ in special3])
+    out["special3_tq"] = np.array([t for _, _, t in special3])
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, "rects:", len(rects))
+
+
 def main():
     # 1. noisy three-plane scene, 10% dropout, float32 metres (small_camera of the reference tests)
     cam = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=31.5, cy=23.5, width=64, height=48)
@@ -204,6 +306,16 @@ def main():
 
     run_rects("rects_planes_f32", cam, rf.DepthImage(values=z32.astype(np.float64)), z32, "f32",
               np.random.default_rng(21))
+
+    # integral backend: a holey frame (hole-corrected rgbd stacks) and a hole-free crop
+    cam_i = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=15.5, cy=11.5, width=32, height=24)
+    z_i = z32[12:36, 16:48].copy()
+    run_integral("integral_holes", cam_i, rf.DepthImage(values=z_i.astype(np.float64)), z_i,
+                 np.random.default_rng(31))
+    d_f, _ = rf.render_scene(scene, rf.compute_tan_maps(cam_i), noise=rf.NoiseModel(), seed=6)
+    z_f = np.where(d_f.valid, d_f.values, 1.5).astype(np.float32)
+    run_integral("integral_full", cam_i, rf.DepthImage(values=z_f.astype(np.float64)), z_f,
+                 np.random.default_rng(32))
 
     # quadtree segmentation of a Voronoi-like multi-plane frame
     cam_s = rf.CameraIntrinsics(fx=120.0, fy=120.0, cx=63.5, cy=47.5, width=128, height=96)

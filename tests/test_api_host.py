@@ -1,0 +1,92 @@
+"""Host-side pieces of the reference-compatible API (no GPU): DepthImage, the scatter
+value types, the argument checks that run before any launch, the CSV row format."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2103_06644_b200 as rf
+from paper_2103_06644_b200 import integral as I
+
+
+def test_depth_image_validity_and_millimetres():
+    d = rf.DepthImage(values=np.array([[1.0, 0.0], [np.nan, -2.0]]))
+    np.testing.assert_array_equal(d.valid, [[True, False], [False, False]])
+    d = rf.DepthImage(values=np.array([[1.0, 2.0]]), valid=np.array([[False, True]]))
+    np.testing.assert_array_equal(d.valid, [[False, True]])
+    mm = np.array([[0, 1500], [65535, 3]], np.uint16)
+    d = rf.DepthImage.from_millimeters(mm)
+    np.testing.assert_array_equal(d.values, mm.astype(np.float64) / 1000.0)
+    np.testing.assert_array_equal(d.valid, mm > 0)
+    np.testing.assert_array_equal(d.to_millimeters(), mm)
+    with pytest.raises(ValueError):
+        rf.DepthImage(values=np.zeros(3))
+    with pytest.raises(ValueError):
+        rf.DepthImage(values=np.ones((2, 2)), valid=np.ones((3, 2), bool))
+
+
+def test_fit_checks_run_before_the_device():
+    with pytest.raises(rf.InsufficientSamplesError):
+        rf.fit_implicit_standard(rf.Scatter4(matrix=np.eye(4), n=3))
+    with pytest.raises(rf.InsufficientSamplesError):
+        rf.fit_explicit_rgbd(rf.Scatter3(matrix=np.eye(3), rhs=np.zeros(3), n=2))
+    m = np.eye(4)
+    m[0, 1] = 1.0
+    with pytest.raises(ValueError, match="not symmetric"):
+        rf.fit_implicit_rgbd(rf.Scatter4(matrix=m, n=4))
+    m = np.eye(4)
+    m[2, 2] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        rf.fit_implicit_standard(rf.Scatter4(matrix=m, n=4))
+    with pytest.raises(ValueError, match="requires a per-frame channel stack"):
+        rf.fit_rect(None, None, rf.Rect(0, 0, 2, 2), "implicit-rgbd", backend="integral")
+    with pytest.raises(ValueError, match="unknown backend"):
+        rf.fit_rect(None, None, rf.Rect(0, 0, 2, 2), "implicit-rgbd", backend="cuda")
+    with pytest.raises(ValueError, match="unknown formulation"):
+        rf.scatter_from_integrals(None, None, rf.Rect(0, 0, 2, 2), "implicit")
+    with pytest.raises(ValueError, match="out of bounds"):
+        I._check_rect(rf.Rect(0, 0, 5, 2), 4, 4)
+
+
+def test_csv_row_matches_reference_format():
+    assert rf.CSV_HEADER == "formulation,backend,x0,y0,x1,y1,a,b,c,d,lambda,rms,n_points"
+    res = rf.FitResult(rf.ImplicitPlane(np.array([0.0, 0.0, 2.0, -6.0])), 25, 0.5, 1.25, False)
+    row = rf.fit_result_csv_row(res, "implicit-standard", "naive", rf.Rect(1, 2, 6, 7))
+    c = 1.0 / np.sqrt(10.0)
+    assert row == ",".join(["implicit-standard", "naive", "1", "2", "6", "7", repr(0.0), repr(0.0),
+                            repr(float(np.float64(2.0) / np.linalg.norm([0, 0, 2.0, -6.0]))),
+                            repr(float(np.float64(-6.0) / np.linalg.norm([0, 0, 2.0, -6.0]))),
+                            "1.25", "0.5", "25"])
+    assert abs(float(row.split(",")[8]) - c) < 1e-15
+    xres = rf.FitResult(rf.ExplicitPlane(np.array([0.5, -0.25, 2.0]), "standard"), 9, None, None, False)
+    xrow = rf.fit_result_csv_row(xres, "explicit-standard", "integral", rf.Rect(0, 0, 3, 3))
+    assert xrow.split(",")[10:] == ["", "", "9"]
+
+
+def test_channel_constants_match_reference_names():
+    assert I.CONSTANT_CHANNELS == ("tx2", "txty", "ty2", "tx", "ty")
+    assert I.STANDARD_IMPLICIT_CHANNELS == ("x2", "xy", "xz", "x", "y2", "yz", "y", "z2", "z")
+    assert I.RGBD_IMPLICIT_CHANNELS == ("tx_over_z", "ty_over_z", "inv_z", "inv_z2")
+    assert I.STANDARD_EXPLICIT_CHANNELS == ("x2", "xy", "x", "y2", "y", "xz", "yz", "z")
+    assert I.RGBD_EXPLICIT_CHANNELS == ("tx_over_z", "ty_over_z", "inv_z")
+    assert I.HOLE_CORRECTION_CHANNELS == ("m_tx2", "m_txty", "m_ty2", "m_tx", "m_ty")
+    from paper_2103_06644_b200 import _native as N
+    for name in (*I.CONSTANT_CHANNELS, *I.STANDARD_IMPLICIT_CHANNELS, *I.RGBD_IMPLICIT_CHANNELS,
+                 *I.HOLE_CORRECTION_CHANNELS, I.COUNT_CHANNEL, "ones"):
+        assert name in N.RF_CHANNELS
+    assert len(set(N.RF_CHANNELS.values())) == len(N.RF_CHANNELS) == 25
+
+
+def test_golden_integral_fixtures_are_consistent():
+    """The committed reference tables: zero first row/column, count corner = valid pixels,
+    and box sums of the count table equal the recorded sample counts."""
+    for case in ("integral_holes", "integral_full"):
+        z = np.load(rf.__path__[0] + f"/../tests/golden/{case}.npz")
+        t = z["std_count"]
+        assert (t[0] == 0).all() and (t[:, 0] == 0).all()
+        assert t[-1, -1] == z["valid"].sum()
+        for k, (x0, y0, x1, y1) in enumerate(z["rects"]):
+            n = int(round(t[y1, x1] - t[y0, x1] - t[y1, x0] + t[y0, x0]))
+            if z["std_n"][k] >= 0:
+                assert n == z["std_n"][k]
