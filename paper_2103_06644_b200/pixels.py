@@ -99,6 +99,21 @@ class TanAngleMaps:
         return self.intrinsics.height
 
     @property
+    def tan_x(self) -> np.ndarray:
+        """The reference's (H, W) lattice ``(x + delta_x - cx) / fx`` (camera.py:131-134), as a
+        read-only broadcast of the one row the device table holds (delta = 0)."""
+        i = self.intrinsics
+        row = (np.arange(i.width, dtype=np.float64)[None, :] + 0.0 - i.cx) / i.fx
+        return np.broadcast_to(row, (i.height, i.width))
+
+    @property
+    def tan_y(self) -> np.ndarray:
+        """The reference's (H, W) lattice ``(y + delta_y - cy) / fy`` (camera.py:131-134)."""
+        i = self.intrinsics
+        col = (np.arange(i.height, dtype=np.float64)[:, None] + 0.0 - i.cy) / i.fy
+        return np.broadcast_to(col, (i.height, i.width))
+
+    @property
     def handle(self) -> ctypes.c_void_p:
         if not self._handle:
             raise ValueError("camera tables were released")

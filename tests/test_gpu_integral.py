@@ -157,3 +157,16 @@ def test_batched_scatter_fits_equal_single_fits():
     for i, m in enumerate(mats):
         single = rf.fit_implicit_standard(rf.Scatter4(matrix=m, n=int(z[f"{key}_n"][ok][i])))
         np.testing.assert_array_equal(rf.ImplicitPlane(rows["coef"][i]).coefficients, single.plane.coefficients)
+
+
+def test_tan_lattices_match_the_reference_formula():
+    z, maps = _load("integral_full")
+    H, W = z["depth"].shape
+    tx = (np.arange(W, dtype=np.float64)[None, :] + np.zeros((H, W)) - float(z["cx"])) / float(z["fx"])
+    ty = (np.arange(H, dtype=np.float64)[:, None] + np.zeros((H, W)) - float(z["cy"])) / float(z["fy"])
+    np.testing.assert_array_equal(maps.tan_x, tx)
+    np.testing.assert_array_equal(maps.tan_y, ty)
+    # the device tables hold the same values: the constant tan_x table's first data row
+    # is the running sum of row 0 of the lattice
+    const = rf.build_constant_channels(maps)
+    np.testing.assert_array_equal(const.channels["tx"].table.cpu().numpy()[1, 1:], np.cumsum(tx[0]))
