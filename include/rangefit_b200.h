@@ -42,8 +42,8 @@ typedef enum rf_depth_dtype {
   RF_DEPTH_F32_M = 0,   /* float32 metres; valid = isfinite & > 0 (synth.py:84)     */
   RF_DEPTH_U16_MM = 1,  /* uint16 millimetres; Z = mm / 1000.0, valid = mm > 0
                            (DepthImage.from_millimeters, synth.py:111-114)         */
-  RF_DEPTH_F64_M = 2    /* float64 metres (DepthImage.values as held by the reference);
-                           only rf_build_channel accepts it                         */
+  RF_DEPTH_F64_M = 2    /* float64 metres (DepthImage.values as held by the reference,
+                           the loss-free RF64 files); valid = isfinite & > 0         */
 } rf_depth_dtype;
 
 /* formulation ids = positions in the reference's FORMULATIONS tuple (fitting.py:45-49) */
@@ -197,6 +197,17 @@ rf_status rf_box_sums(const double* const* tables, int32_t nch, int32_t height, 
 rf_status rf_fit_scatters(const double* matrices, const double* rhs, const double* target_sq,
                           const int64_t* counts, int64_t n, int32_t formulation, rf_rect_fit* out,
                           void* stream);
+
+/* ---- the reference's virtual depth sensor (render_scene, synth.py:137-194) ----
+ * One frame of the camera in `tables`: planes [nplanes][4] (unit-normal a,b,c,d), rects
+ * [nplanes][4] half-open pixel bounds already clipped to the frame (the whole frame for
+ * planes without a mask rect); eps [H][W] standard normals (NULL = no noise), uniforms
+ * [H][W] in [0,1) (NULL = no dropout): nearest positive intersection, Z += k Z^2 eps,
+ * dropout, validity Z > 0.  Outputs depth fp64 [H][W] (0 where invalid), valid and labels
+ * uint8 [H][W] (plane index, 255 = invalid).  All arrays are device memory. */
+rf_status rf_render_planes(const rf_tables* tables, const double* planes, const int32_t* rects, int32_t nplanes,
+                           const double* eps, const double* uniforms, double noise_coefficient, double dropout,
+                           double* depth, uint8_t* valid, uint8_t* labels, void* stream);
 
 /* RF_ABI_VERSION of the loaded library. */
 int32_t rf_abi_version(void);

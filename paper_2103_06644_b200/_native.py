@@ -62,6 +62,7 @@ EXPORTED_SYMBOLS = (
     "rf_integral",
     "rf_box_sums",
     "rf_fit_scatters",
+    "rf_render_planes",
     "rf_launches_per_call",
     "rf_last_error",
     "rf_abi_version",
@@ -130,6 +131,9 @@ def load() -> ctypes.CDLL:
     L.rf_box_sums.restype = ctypes.c_int
     L.rf_fit_scatters.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int32, vp, vp]
     L.rf_fit_scatters.restype = ctypes.c_int
+    L.rf_render_planes.argtypes = [vp, vp, vp, ctypes.c_int32, vp, vp, ctypes.c_double, ctypes.c_double, vp, vp,
+                                   vp, vp]
+    L.rf_render_planes.restype = ctypes.c_int
     L.rf_launches_per_call.argtypes = [ctypes.c_int32]
     L.rf_launches_per_call.restype = ctypes.c_int32
     L.rf_last_error.argtypes = []

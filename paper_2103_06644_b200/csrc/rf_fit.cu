@@ -79,6 +79,11 @@ struct KParams {
 namespace {
 using namespace rf_dev;
 
+// bytes per depth element
+__host__ __device__ __forceinline__ int elem_size(int dtype) {
+  return dtype == RF_DEPTH_U16_MM ? 2 : dtype == RF_DEPTH_F64_M ? 8 : 4;
+}
+
 // residue-major column stride of the column-sum buffers (VQ = 4 mod 8 spreads the banks)
 __host__ __device__ __forceinline__ int vq_of(int hw) {
   int q = (hw + 3) / 4;
@@ -140,6 +145,11 @@ template <int VAR>
 __device__ __forceinline__ double primary_of(float zf) {
   const bool valid = (zf > 0.0f) && (zf <= 3.402823466e38f);  // isfinite & > 0
   const double z = (double)zf;
+  return valid ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
+}
+template <int VAR>
+__device__ __forceinline__ double primary_of(double z) {  // float64 metres (RF64 ingest)
+  const bool valid = (z > 0.0) && (z <= 1.7976931348623157e308);
   return valid ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
 }
 template <int VAR>
@@ -210,7 +220,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   // small compile-time radii: direct column sums with dy centred on each output row;
   // otherwise running column sums with dy relative to the tile's first row
   constexpr bool CENTRED = RT > 0 && RT <= 3;
-  const int esz = P.dtype == RF_DEPTH_U16_MM ? 2 : 4;
+  const int esz = elem_size(P.dtype);
   const int al = 16 / esz;  // TMA box x origin must be 16-byte aligned
   const int HWP = (HW_ + al - 1 + 7) & ~7;  // TMA box width (covers the alignment shift)
   const int raw_bytes = USE_TMA ? ((HH_ * HWP * esz + 127) & ~127) : 0;
@@ -260,6 +270,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       if (esz == 2)
         convert_halo<VAR>(prim, reinterpret_cast<const unsigned short*>(raw), HW_, HH_, HWP, sx, sy, P, frame,
                           x0, y0, r, tid);
+      else if (esz == 8)
+        convert_halo<VAR>(prim, reinterpret_cast<const double*>(raw), HW_, HH_, HWP, sx, sy, P, frame, x0, y0,
+                          r, tid);
       else
         convert_halo<VAR>(prim, reinterpret_cast<const float*>(raw), HW_, HH_, HWP, sx, sy, P, frame, x0, y0,
                           r, tid);
@@ -283,8 +296,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
             const int64_t off = frame * P.frame_stride + (int64_t)y * P.row_pitch + x;
             const bool mask_ok =
                 !P.mask || __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
-            p = esz == 2 ? primary_masked<VAR>(__ldg(reinterpret_cast<const unsigned short*>(P.depth) + off), mask_ok)
-                         : primary_masked<VAR>(__ldg(reinterpret_cast<const float*>(P.depth) + off), mask_ok);
+            p = esz == 2   ? primary_masked<VAR>(__ldg(reinterpret_cast<const unsigned short*>(P.depth) + off), mask_ok)
+                : esz == 8 ? primary_masked<VAR>(__ldg(reinterpret_cast<const double*>(P.depth) + off), mask_ok)
+                           : primary_masked<VAR>(__ldg(reinterpret_cast<const float*>(P.depth) + off), mask_ok);
           }
           prim[row * HW_ + col] = p;
         }
@@ -703,7 +717,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // (hwp, hh, 1), zero fill out of range.  Returns false when TMA cannot address it.
 bool make_depth_tmap(CUtensorMap* m, const void* depth, int dtype, int64_t batch, int H, int W,
                      int64_t row_pitch, int r) {
-  const int esz = dtype == RF_DEPTH_U16_MM ? 2 : 4;
+  const int esz = elem_size(dtype);
   const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
   if (hwp > 256 || hh > 256) return false;
   if ((reinterpret_cast<uintptr_t>(depth) & 15) != 0) return false;
@@ -715,7 +729,10 @@ bool make_depth_tmap(CUtensorMap* m, const void* depth, int dtype, int64_t batch
   const cuuint64_t strides[2] = {(cuuint64_t)(row_pitch * esz), (cuuint64_t)(row_pitch * H * esz)};
   const cuuint32_t box[3] = {(cuuint32_t)hwp, (cuuint32_t)hh, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult res = fn(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+  const CUtensorMapDataType dt = esz == 2   ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                 : esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const CUresult res = fn(m, dt, 3,
                           const_cast<void*>(depth), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -827,7 +844,7 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
                         int32_t window, int32_t fmask, const rf_pixel_out* outs, void* stream) {
   if (!t) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null tables%s");
   if (!depth && batch != 0) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null depth%s");
-  if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM)
+  if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM && dtype != RF_DEPTH_F64_M)
     return fail(RF_ERR_SHAPE, "unknown depth dtype%s %lld", "", dtype);
   if (H != t->intr.height || W != t->intr.width)
     return fail(RF_ERR_SHAPE, "depth %s%lldx%lld does not match the camera tables", "", W, H);
@@ -853,7 +870,7 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   memset(&tmap, 0, sizeof(tmap));
   const bool tma = getenv("RF_DISABLE_TMA") == nullptr &&
                    make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
-  const int esz = dtype == RF_DEPTH_U16_MM ? 2 : 4;
+  const int esz = elem_size(dtype);
   // one launch per space: standard (implicit/explicit-standard), rgbd (implicit/explicit-rgbd)
   for (int var = 0; var < 2; ++var) {
     const int fi = var == VAR_STD ? RF_FORM_IMPLICIT_STANDARD : RF_FORM_IMPLICIT_RGBD;

@@ -97,6 +97,9 @@ __global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams 
       const unsigned short mm = __ldg(reinterpret_cast<const unsigned short*>(P.depth) + off);
       valid = mm > 0;
       z = __ddiv_rn((double)mm, 1000.0);
+    } else if (P.dtype == RF_DEPTH_F64_M) {
+      z = __ldg(reinterpret_cast<const double*>(P.depth) + off);
+      valid = (z > 0.0) && (z <= 1.7976931348623157e308);
     } else {
       const float zf = __ldg(reinterpret_cast<const float*>(P.depth) + off);
       valid = (zf > 0.0f) && (zf <= 3.402823466e38f);
@@ -233,7 +236,7 @@ rf_status rf_fit_rects(const rf_tables* t, const void* depth, int dtype, int64_t
                        int32_t W, int64_t row_pitch, const uint8_t* mask, const rf_rect* rects,
                        int64_t nrects, int32_t formulation, rf_rect_fit* out, void* stream) {
   if (!t) return rf_set_error(RF_ERR_ARGUMENT, "rf_fit_rects: null tables");
-  if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM)
+  if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM && dtype != RF_DEPTH_F64_M)
     return rf_set_error(RF_ERR_SHAPE, "rf_fit_rects: unknown depth dtype");
   if (H != t->intr.height || W != t->intr.width)
     return rf_set_error(RF_ERR_SHAPE, "rf_fit_rects: depth size does not match the camera tables");

@@ -185,9 +185,11 @@ class PixelFits:
 def _depth_dtype(t: torch.Tensor) -> int:
     if t.dtype == torch.float32:
         return N.RF_DEPTH_F32_M
+    if t.dtype == torch.float64:
+        return N.RF_DEPTH_F64_M
     if t.dtype in (torch.uint16, torch.int16):
         return N.RF_DEPTH_U16_MM
-    raise ValueError(f"depth must be float32 metres or uint16 millimetres, got {t.dtype}")
+    raise ValueError(f"depth must be float32/float64 metres or uint16 millimetres, got {t.dtype}")
 
 
 def fit_pixels(

@@ -293,6 +293,40 @@ def run_integral(name, cam, depth_img, stored, rng, count=40):
     print(name, "rects:", len(rects))
 
 
+def run_render(name):
+    """The reference renderer (synth.py:137-194) on small scenes: nearest hit with mask rects,
+    quadratic noise, dropout, per-row seeded streams; plus the interchange files it writes
+    (imageio.py:47-139, synth.py:224-246)."""
+    from rangefit import imageio as rio
+    from rangefit.synth import write_depth
+
+    cam = rf.CameraIntrinsics(fx=50.0, fy=52.0, cx=19.5, cy=14.5, width=40, height=30)
+    maps = rf.compute_tan_maps(cam)
+    planes = (rf.GroundTruthPlane(np.array([0.1, -0.2, -1.0, 2.5])),
+              rf.GroundTruthPlane(np.array([-0.3, 0.1, -1.0, 1.8]), mask_rect=(5, 3, 30, 20)),
+              rf.GroundTruthPlane(np.array([0.0, 0.0, -1.0, 1.2]), mask_rect=(-10, 22, 12, 40)),
+              rf.GroundTruthPlane(np.array([0.9, 0.0, 0.1, 0.5])))
+    scene = rf.SyntheticScene(planes)
+    out = {"fx": cam.fx, "fy": cam.fy, "cx": cam.cx, "cy": cam.cy, "width": cam.width, "height": cam.height,
+           "planes": np.stack([p.coefficients for p in planes]),
+           "rects": np.array([p.mask_rect if p.mask_rect is not None else (-1, -1, -1, -1) for p in planes])}
+    cases = {"plain": dict(noise=None, seed=0, dropout=0.0),
+             "noise": dict(noise=rf.NoiseModel(), seed=7, dropout=0.0),
+             "drop": dict(noise=None, seed=3, dropout=0.2),
+             "both": dict(noise=rf.NoiseModel(slope_coefficient=0.02), seed=11, dropout=0.1)}
+    for key, kw in cases.items():
+        d, labels = rf.render_scene(scene, maps, **kw)
+        out[f"{key}_depth"], out[f"{key}_valid"], out[f"{key}_labels"] = d.values, d.valid, labels
+        out[f"{key}_noise"] = 0.0 if kw["noise"] is None else kw["noise"].slope_coefficient
+        out[f"{key}_seed"], out[f"{key}_dropout"] = kw["seed"], kw["dropout"]
+    d, _ = rf.render_scene(scene, maps, noise=rf.NoiseModel(), seed=7)
+    write_depth(HERE / "io_depth.pgm", d)
+    write_depth(HERE / "io_depth.rf64", d)
+    rio.write_pgm8(HERE / "io_labels.pgm", out["plain_labels"])
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, "render cases:", len(cases))
+
+
 def main():
     # 1. noisy three-plane scene, 10% dropout, float32 metres (small_camera of the reference tests)
     cam = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=31.5, cy=23.5, width=64, height=48)
@@ -306,6 +340,8 @@ def main():
 
     run_rects("rects_planes_f32", cam, rf.DepthImage(values=z32.astype(np.float64)), z32, "f32",
               np.random.default_rng(21))
+
+    run_render("render_planes")
 
     # integral backend: a holey frame (hole-corrected rgbd stacks) and a hole-free crop
     cam_i = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=15.5, cy=11.5, width=32, height=24)

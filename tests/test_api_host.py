@@ -90,3 +90,48 @@ def test_golden_integral_fixtures_are_consistent():
             n = int(round(t[y1, x1] - t[y0, x1] - t[y1, x0] + t[y0, x0]))
             if z["std_n"][k] >= 0:
                 assert n == z["std_n"][k]
+
+
+def test_interchange_files_match_reference_bytes(tmp_path):
+    from paper_2103_06644_b200 import imageio as io
+    from paper_2103_06644_b200 import synth
+    g = rf.__path__[0] + "/../tests/golden/"
+    mm = io.read_pgm16(g + "io_depth.pgm")
+    io.write_pgm16(tmp_path / "a.pgm", mm)
+    assert (tmp_path / "a.pgm").read_bytes() == open(g + "io_depth.pgm", "rb").read()
+    raw = io.read_raw_float(g + "io_depth.rf64")
+    io.write_raw_float(tmp_path / "a.rf64", raw)
+    assert (tmp_path / "a.rf64").read_bytes() == open(g + "io_depth.rf64", "rb").read()
+    lab = io.read_pgm8(g + "io_labels.pgm")
+    io.write_pgm8(tmp_path / "l.pgm", lab)
+    assert (tmp_path / "l.pgm").read_bytes() == open(g + "io_labels.pgm", "rb").read()
+    d = synth.read_depth(g + "io_depth.rf64")
+    assert d.valid.sum() == np.isfinite(raw).sum()
+    synth.write_depth(tmp_path / "b.pgm", d)
+    assert (tmp_path / "b.pgm").read_bytes() == open(g + "io_depth.pgm", "rb").read()
+    np.testing.assert_array_equal(synth.read_depth(tmp_path / "b.pgm").values, mm / 1000.0)
+    rgb = np.arange(2 * 3 * 3, dtype=np.uint8).reshape(2, 3, 3)
+    io.write_ppm(tmp_path / "c.ppm", rgb)
+    np.testing.assert_array_equal(io.read_ppm(tmp_path / "c.ppm"), rgb)
+    (tmp_path / "bad.pgm").write_bytes(b"P5\n# comment\n4 4\n65535\n\x00\x01")
+    with pytest.raises(ValueError, match="truncated"):
+        io.read_pgm16(tmp_path / "bad.pgm")
+    with pytest.raises(ValueError, match="RF64"):
+        io.read_raw_float(tmp_path / "bad.pgm")
+
+
+def test_scene_parsing_and_mask_rect_slices():
+    from paper_2103_06644_b200 import synth
+    sc = synth.parse_scene("# two planes\n0 0 1 -2\n0.1 0 -1 3  5 6 20 30  # masked\n")
+    assert len(sc.planes) == 2 and sc.planes[1].mask_rect == (5, 6, 20, 30)
+    np.testing.assert_allclose(np.linalg.norm(sc.planes[1].normal), 1.0)
+    with pytest.raises(ValueError, match="expected"):
+        synth.parse_scene("1 2 3\n")
+    with pytest.raises(ValueError, match="no planes"):
+        synth.parse_scene("# nothing\n")
+    rects = synth._plane_rects(synth.SyntheticScene((
+        synth.GroundTruthPlane(np.array([0, 0, 1.0, -1])),
+        synth.GroundTruthPlane(np.array([0, 0, 1.0, -1]), mask_rect=(-10, 22, 12, 40)),
+        synth.GroundTruthPlane(np.array([0, 0, 1.0, -1]), mask_rect=(5, -3, 99, 20)))), 40, 30)
+    # numpy slice semantics of masked[y0:y1, x0:x1] (synth.py:145-148)
+    assert rects.tolist() == [[0, 0, 40, 30], [30, 22, 30, 30], [5, 27, 40, 27]]

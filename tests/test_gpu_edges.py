@@ -125,7 +125,7 @@ def test_argument_errors():
     with pytest.raises(ValueError):
         rf.fit_pixels(torch.ones((32, 31), device="cuda"), maps, 5)
     with pytest.raises(ValueError):
-        rf.fit_pixels(d.double(), maps, 5)
+        rf.fit_pixels(d.int(), maps, 5)           # int32 is not a depth type
     with pytest.raises(ValueError):
         rf.fit_pixels(d, maps, 5, formulations=("implicit-disparity",))
 
