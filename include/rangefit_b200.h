@@ -143,6 +143,15 @@ rf_status rf_fit_rects(const rf_tables* tables, const void* depth, int dtype, in
                        const rf_rect* rects, int64_t nrects, int32_t formulation,
                        rf_rect_fit* out, void* stream);
 
+/* Replaces segment.py's _max_residual (segment.py:306-325) for a device list of rects and
+ * planes: out[r] = max |objective| over the rect's valid pixels (0 for none), with coefs
+ * [nrects][4] = the canonical implicit coefficients (implicit formulations) or the
+ * ExplicitPlane (a, b, c) (explicit; 4th entry unused). */
+rf_status rf_max_residuals(const rf_tables* tables, const void* depth, int dtype, int64_t batch,
+                           int32_t height, int32_t width, int64_t row_pitch, const uint8_t* mask,
+                           const rf_rect* rects, int64_t nrects, int32_t formulation, const double* coefs,
+                           double* out, void* stream);
+
 /* Number of kernel launches rf_fit_pixels issues for a given formulation mask. */
 int32_t rf_launches_per_call(int32_t formulation_mask);
 

@@ -63,6 +63,7 @@ EXPORTED_SYMBOLS = (
     "rf_box_sums",
     "rf_fit_scatters",
     "rf_render_planes",
+    "rf_max_residuals",
     "rf_launches_per_call",
     "rf_last_error",
     "rf_abi_version",
@@ -134,6 +135,11 @@ def load() -> ctypes.CDLL:
     L.rf_render_planes.argtypes = [vp, vp, vp, ctypes.c_int32, vp, vp, ctypes.c_double, ctypes.c_double, vp, vp,
                                    vp, vp]
     L.rf_render_planes.restype = ctypes.c_int
+    L.rf_max_residuals.argtypes = [
+        vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, vp,
+        vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp,
+    ]
+    L.rf_max_residuals.restype = ctypes.c_int
     L.rf_launches_per_call.argtypes = [ctypes.c_int32]
     L.rf_launches_per_call.restype = ctypes.c_int32
     L.rf_last_error.argtypes = []

@@ -228,9 +228,132 @@ __global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams 
   *o = res;
 }
 
+// _max_residual (segment.py:306-325): max |objective| over a rect's valid pixels for a
+// given plane, evaluated like the reference's numpy expression (left to right, unfused),
+// one CTA per rect.  coefs: [nrects][4] -- the canonical implicit coefficients (implicit
+// forms) or the explicit (a, b, c, unused).
+struct MaxResParams {
+  RectParams base;
+  const double* coefs;
+  double* out;
+};
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < RT_THREADS / 32; ++w) t = fmax(t, red[w]);
+  return t;
+}
+
+__global__ void __launch_bounds__(RT_THREADS) max_residual_kernel(const MaxResParams M) {
+  __shared__ double red[RT_THREADS / 32];
+  const RectParams& P = M.base;
+  const int64_t ri = blockIdx.x;
+  if (ri >= P.nrects) return;
+  const rf_rect R = P.rects[ri];
+  if (!(R.frame >= 0 && R.frame < P.batch && 0 <= R.x0 && R.x0 <= R.x1 && R.x1 <= P.W && 0 <= R.y0 &&
+        R.y0 <= R.y1 && R.y1 <= P.H)) {
+    if (threadIdx.x == 0) M.out[ri] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  const double c0 = M.coefs[4 * ri], c1 = M.coefs[4 * ri + 1], c2 = M.coefs[4 * ri + 2], c3 = M.coefs[4 * ri + 3];
+  const int rw = R.x1 - R.x0;
+  const int64_t area = (int64_t)rw * (R.y1 - R.y0);
+  double mx = 0.0;  // max of |res| >= 0; an empty rect reports 0 as the reference
+  for (int64_t e = threadIdx.x; e < area; e += RT_THREADS) {
+    const int yy = (int)(e / rw), xx = (int)(e - (int64_t)yy * rw);
+    const int y = R.y0 + yy, x = R.x0 + xx;
+    const int64_t off = (int64_t)R.frame * P.frame_stride + (int64_t)y * P.row_pitch + x;
+    double z;
+    bool valid;
+    if (P.dtype == RF_DEPTH_U16_MM) {
+      const unsigned short mm = __ldg(reinterpret_cast<const unsigned short*>(P.depth) + off);
+      valid = mm > 0;
+      z = __ddiv_rn((double)mm, 1000.0);
+    } else if (P.dtype == RF_DEPTH_F64_M) {
+      z = __ldg(reinterpret_cast<const double*>(P.depth) + off);
+      valid = (z > 0.0) && (z <= 1.7976931348623157e308);
+    } else {
+      const float zf = __ldg(reinterpret_cast<const float*>(P.depth) + off);
+      valid = (zf > 0.0f) && (zf <= 3.402823466e38f);
+      z = (double)zf;
+    }
+    if (P.mask) valid = valid && __ldg(P.mask + (int64_t)R.frame * P.out_frame + (int64_t)y * P.W + x) != 0;
+    if (!valid) continue;
+    const double tx = P.tan_x[x], ty = P.tan_y[y];
+    double r;
+    switch (P.formulation) {
+      case RF_FORM_IMPLICIT_STANDARD:  // c0 z tx + c1 z ty + c2 z + c3
+        r = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(c0, z), tx), __dmul_rn(__dmul_rn(c1, z), ty)),
+                                __dmul_rn(c2, z)), c3);
+        break;
+      case RF_FORM_IMPLICIT_RGBD:  // c0 tx + c1 ty + c2 + c3 / z
+        r = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(c0, tx), __dmul_rn(c1, ty)), c2), __ddiv_rn(c3, z));
+        break;
+      case RF_FORM_EXPLICIT_STANDARD:  // a z tx + b z ty + c - z
+        r = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(c0, z), tx), __dmul_rn(__dmul_rn(c1, z), ty)), c2), z);
+        break;
+      default:  // a tx + b ty + c - 1 / z
+        r = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(c0, tx), __dmul_rn(c1, ty)), c2), __ddiv_rn(1.0, z));
+        break;
+    }
+    mx = fmax(mx, fabs(r));
+  }
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0) M.out[ri] = mx;
+}
+
 }  // namespace
 
 extern "C" {
+
+rf_status rf_max_residuals(const rf_tables* t, const void* depth, int dtype, int64_t batch, int32_t H,
+                           int32_t W, int64_t row_pitch, const uint8_t* mask, const rf_rect* rects,
+                           int64_t nrects, int32_t formulation, const double* coefs, double* out, void* stream) {
+  if (!t) return rf_set_error(RF_ERR_ARGUMENT, "rf_max_residuals: null tables");
+  if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM && dtype != RF_DEPTH_F64_M)
+    return rf_set_error(RF_ERR_SHAPE, "rf_max_residuals: unknown depth dtype");
+  if (H != t->intr.height || W != t->intr.width)
+    return rf_set_error(RF_ERR_SHAPE, "rf_max_residuals: depth size does not match the camera tables");
+  if (formulation < 0 || formulation >= RF_NUM_FORMULATIONS)
+    return rf_set_error(RF_ERR_ARGUMENT, "rf_max_residuals: unknown formulation");
+  if (batch < 0 || nrects < 0 || row_pitch < W)
+    return rf_set_error(RF_ERR_ARGUMENT, "rf_max_residuals: bad batch / rect count / row pitch");
+  if (nrects == 0) return RF_OK;
+  if (!depth || !rects || !coefs || !out || nrects > 0x7fffffff)
+    return rf_set_error(RF_ERR_ARGUMENT, "rf_max_residuals: null pointer");
+  MaxResParams M;
+  RectParams& P = M.base;
+  P.depth = depth;
+  P.mask = mask;
+  P.tan_x = t->tan_x;
+  P.tan_y = t->tan_y;
+  P.ifx = 1.0 / t->intr.fx;
+  P.ify = 1.0 / t->intr.fy;
+  P.row_pitch = row_pitch;
+  P.frame_stride = row_pitch * H;
+  P.out_frame = (int64_t)H * W;
+  P.batch = batch;
+  P.H = H;
+  P.W = W;
+  P.dtype = dtype;
+  P.formulation = formulation;
+  P.rects = rects;
+  P.nrects = nrects;
+  P.out = nullptr;
+  M.coefs = coefs;
+  M.out = out;
+  max_residual_kernel<<<(unsigned)nrects, RT_THREADS, 0, reinterpret_cast<cudaStream_t>(stream)>>>(M);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return rf_set_error(RF_ERR_CUDA, cudaGetErrorString(e));
+  return RF_OK;
+}
 
 rf_status rf_fit_rects(const rf_tables* t, const void* depth, int dtype, int64_t batch, int32_t H,
                        int32_t W, int64_t row_pitch, const uint8_t* mask, const rf_rect* rects,

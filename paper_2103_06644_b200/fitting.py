@@ -169,7 +169,7 @@ def _as_depth_tensor(depth, device) -> torch.Tensor:
     elif hasattr(depth, "values"):
         vals = np.asarray(depth.values)
         valid = np.asarray(getattr(depth, "valid", np.isfinite(vals) & (vals > 0)), dtype=bool)
-        d = torch.from_numpy(np.where(valid, vals, 0.0).astype(np.float32))
+        d = torch.from_numpy(np.where(valid, vals, 0.0).astype(np.float64))  # RF_DEPTH_F64_M: the values as held
     else:
         d = torch.as_tensor(np.asarray(depth))
     if not d.is_cuda:
@@ -434,6 +434,109 @@ def scatter_from_integrals(stack, constant, rect, formulation: str):
     matrix = np.array([[stx2, stxty, stx], [stxty, sty2, sty], [stx, sty, pixel_count]])
     rhs = np.array([b["tx_over_z"], b["ty_over_z"], b["inv_z"]])
     return Scatter3(matrix=matrix, rhs=rhs, n=n, target_sq=b.get("inv_z2"))
+
+
+def fit_rects_integral(stack, constant, rects, formulation: str) -> np.ndarray:
+    """scatter_from_integrals + FIT_BY_FORMULATION for many rects of one frame: one box-sum
+    launch, the systems assembled as the reference assembles them, one fit launch.
+    Returns ``RECT_FIT_DTYPE`` rows; rects below MIN_SAMPLES carry no RECT_FIT bit."""
+    from . import integral as I
+
+    _check_formulation(formulation)
+    rr = [Rect(*r) for r in rects]
+    out = np.zeros(len(rr), dtype=RECT_FIT_DTYPE)
+    if not rr:
+        return out
+    names = list(stack.channels)
+    tables = [stack.count.table] + [stack.channels[k].table for k in names]
+    cnames = []
+    if formulation in (IMPLICIT_RGBD, EXPLICIT_RGBD) and constant is not None:
+        cnames = ["tx2", "txty", "ty2", "tx", "ty"]
+        _require_channels(constant, cnames, "constant")
+        tables += [constant.channels[k].table for k in cnames]
+    sums = I.box_sums(tables, rr)
+    n = np.rint(sums[:, 0]).astype(np.int64)
+    col = {k: sums[:, 1 + i] for i, k in enumerate(names)}
+    ccol = {k: sums[:, 1 + len(names) + i] for i, k in enumerate(cnames)}
+    area = np.array([r.area for r in rr])
+    ok = n >= MIN_SAMPLES[formulation]
+    nf = n.astype(np.float64)
+    size = 4 if formulation in (IMPLICIT_STANDARD, IMPLICIT_RGBD) else 3
+    M = np.zeros((len(rr), size, size))
+    rhs = tq = None
+    if formulation in (IMPLICIT_STANDARD, EXPLICIT_STANDARD):
+        need = ("x2", "xy", "xz", "x", "y2", "yz", "y", "z2", "z") if size == 4 else \
+            ("x2", "xy", "x", "y2", "y", "xz", "yz", "z")
+        _require_channels(stack, need, "per-frame")
+        c = col
+        if size == 4:
+            rows = [[c["x2"], c["xy"], c["xz"], c["x"]], [c["xy"], c["y2"], c["yz"], c["y"]],
+                    [c["xz"], c["yz"], c["z2"], c["z"]], [c["x"], c["y"], c["z"], nf]]
+        else:
+            rows = [[c["x2"], c["xy"], c["x"]], [c["xy"], c["y2"], c["y"]], [c["x"], c["y"], nf]]
+            rhs = np.stack([c["xz"], c["yz"], c["z"]], axis=1)
+            tq = c.get("z2")
+    else:
+        full = n == area
+        if (full & ok).any() and constant is None:
+            raise ValueError(f"{formulation} requires the camera-constant channel stack")
+        if (~full & ok).any() and not stack.hole_corrected:
+            raise ValueError("a window contains invalid pixels but the frame stack carries no masked tan channels")
+        t = {}
+        for k in ("tx2", "txty", "ty2", "tx", "ty"):
+            t[k] = np.where(full, ccol[k] if ccol else 0.0, col[f"m_{k}"] if f"m_{k}" in col else 0.0)
+        c = col
+        need = ("tx_over_z", "ty_over_z", "inv_z", "inv_z2") if size == 4 else ("tx_over_z", "ty_over_z", "inv_z")
+        _require_channels(stack, need, "per-frame")
+        if size == 4:
+            rows = [[t["tx2"], t["txty"], t["tx"], c["tx_over_z"]], [t["txty"], t["ty2"], t["ty"], c["ty_over_z"]],
+                    [t["tx"], t["ty"], nf, c["inv_z"]], [c["tx_over_z"], c["ty_over_z"], c["inv_z"], c["inv_z2"]]]
+        else:
+            rows = [[t["tx2"], t["txty"], t["tx"]], [t["txty"], t["ty2"], t["ty"]], [t["tx"], t["ty"], nf]]
+            rhs = np.stack([c["tx_over_z"], c["ty_over_z"], c["inv_z"]], axis=1)
+            tq = c.get("inv_z2")
+    for a in range(size):
+        for b in range(size):
+            M[:, a, b] = rows[a][b]
+    out["n_points"] = n
+    idx = np.nonzero(ok)[0]
+    if len(idx):
+        res = fit_scatters(M[idx], n[idx], formulation, rhs=None if rhs is None else rhs[idx],
+                           target_sq=None if tq is None else tq[idx], device=stack.count.table.device.index)
+        out[idx] = res
+    return out
+
+
+def max_residuals(depth, maps: TanAngleMaps, rects, formulation: str, coefs, frames=None, mask=None,
+                  stream: torch.cuda.Stream | None = None) -> np.ndarray:
+    """segment.py's _max_residual (segment.py:306-325) for many rects on the device: coefs
+    [n, 4] canonical implicit coefficients, or [n, 3] explicit (a, b, c)."""
+    _check_formulation(formulation)
+    dev = torch.device("cuda", maps.device)
+    d = _as_depth_tensor(depth, dev)
+    if d.stride(-1) != 1 or (d.shape[0] > 1 and d.stride(0) != d.stride(1) * d.shape[1]):
+        d = d.contiguous()
+    B, H, W = d.shape
+    r = np.asarray(rects, dtype=np.int64).reshape(-1, 4)
+    f = np.zeros(len(r), np.int64) if frames is None else np.broadcast_to(np.asarray(frames, np.int64), (len(r),))
+    rr = torch.from_numpy(np.column_stack([f, r]).astype(np.int32)).to(dev)
+    c = np.zeros((len(r), 4))
+    cin = np.asarray(coefs, dtype=np.float64).reshape(len(r), -1)
+    c[:, :cin.shape[1]] = cin
+    dc = torch.from_numpy(c).to(dev)
+    out = torch.empty(len(r), dtype=torch.float64, device=dev)
+    mptr = None
+    if mask is not None:
+        m = mask.unsqueeze(0) if mask.dim() == 2 else mask
+        m = m.to(device=dev, dtype=torch.uint8).contiguous()
+        mptr = m.data_ptr()
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    st = N.load().rf_max_residuals(maps.handle, d.data_ptr(), _depth_dtype(d), B, H, W, d.stride(-2), mptr,
+                                   rr.data_ptr(), len(r), _FORM_ID[formulation], dc.data_ptr(), out.data_ptr(),
+                                   ctypes.c_void_p(stream.cuda_stream))
+    N.check(st, "max_residuals")
+    return out.cpu().numpy()
 
 
 class ExplicitRgbdFitter:

@@ -7,8 +7,11 @@ tiles with too few valid pixels are rejected, and k-means over the fitted tiles'
 plane features groups coplanar tiles.
 
 B200 design: the quadtree is evaluated **level-synchronously** -- every pending tile
-of a level is fitted in ONE ``rf_fit_rects`` launch (one CTA per tile, direct sums)
-instead of one Python ``fit_rect`` per tile.  Each tile's decision depends only on
+of a level is fitted in ONE launch instead of one Python ``fit_rect`` per tile:
+``rf_fit_rects`` (one CTA per tile, direct sums) for the ``"b200"`` / ``"naive"``
+backends, or one ``rf_box_sums`` + one ``rf_fit_scatters`` launch over the frame's device
+channel stack for ``"integral"``; ``error_metric="max"`` adds one ``rf_max_residuals``
+launch per level (``_max_residual``, segment.py:306-325).  Each tile's decision depends only on
 its own fit, so the leaf set equals the reference's; the leaves are then listed in
 the reference's LIFO traversal order so that k-means (which seeds by sample index)
 sees the same sequence.  k-means runs on the host: it clusters a few hundred
@@ -39,7 +42,8 @@ class TileStatus(enum.Enum):
 
 @dataclass(frozen=True)
 class SegConfig:
-    """Segmentation knobs (reference segment.py:81-130); backend is always the device."""
+    """Segmentation knobs (reference segment.py:81-130).  Every backend runs on the device:
+    ``"b200"``/``"naive"`` direct sums per tile, ``"integral"`` the frame's channel stack."""
 
     formulation: str = IMPLICIT_RGBD
     backend: str = "b200"
@@ -55,7 +59,7 @@ class SegConfig:
     def __post_init__(self) -> None:
         if self.formulation not in FORMULATIONS:
             raise ValueError(f"unknown formulation {self.formulation!r}")
-        if self.backend != "b200":
+        if self.backend not in F.BACKENDS:
             raise ValueError(f"unknown backend {self.backend!r}")
         if self.max_depth < 0:
             raise ValueError("max_depth must be non-negative")
@@ -69,8 +73,8 @@ class SegConfig:
             raise ValueError("k must be at least 1")
         if self.d_scale <= 0:
             raise ValueError("d_scale must be positive")
-        if self.error_metric != "rms":
-            raise NotImplementedError("error_metric='max' is not implemented on the device path")
+        if self.error_metric not in ("rms", "max"):
+            raise ValueError(f"unknown error metric {self.error_metric!r}")
 
     @property
     def threshold(self) -> float:
@@ -159,25 +163,74 @@ def _children(r: F.Rect):
             F.Rect(r.x0, ym, xm, r.y1), F.Rect(xm, ym, r.x1, r.y1)]
 
 
-def segment(depth, maps: TanAngleMaps, config: SegConfig, frame: int = 0, mask=None) -> Segmentation:
-    """Segment one frame of a depth tensor ([H,W] or [B,H,W] on the device)."""
+def build_frame_stack(depth, maps: TanAngleMaps, formulation: str):
+    """The per-frame channel stack a formulation needs, with residuals (segment.py:272-285)."""
+    from . import integral as I
+
+    if formulation == IMPLICIT_STANDARD:
+        return I.build_standard_implicit_channels(depth, maps)
+    if formulation == IMPLICIT_RGBD:
+        return I.build_rgbd_implicit_channels(depth, maps)
+    if formulation == EXPLICIT_STANDARD:
+        return I.build_standard_explicit_channels(depth, maps, include_residual=True)
+    if formulation == EXPLICIT_RGBD:
+        return I.build_rgbd_explicit_channels(depth, maps, include_residual=True)
+    raise ValueError(f"unknown formulation {formulation!r}")
+
+
+def segment(depth, maps: TanAngleMaps, config: SegConfig, constant=None, frame: int = 0,
+            mask=None) -> Segmentation:
+    """Segment one frame (reference signature segment.py:327-333; ``depth`` a DepthImage or a
+    device tensor [H,W] / [B,H,W] with ``frame`` selecting the frame)."""
+    from . import integral as I
+
     d = F._as_depth_tensor(depth, torch.device("cuda", maps.device))
     H, W = d.shape[-2:]
+    if W < 1 or H < 1:
+        raise ValueError("empty depth image")
     if W < MIN_TILE_EDGE or H < MIN_TILE_EDGE:
         raise ValueError(f"image {W}x{H} is smaller than one fittable tile")
+    stack = None
+    if config.backend == "integral":
+        if config.formulation in (IMPLICIT_RGBD, EXPLICIT_RGBD) and constant is None:
+            constant = I.build_constant_channels(maps)
+        fd = d[frame]
+        if mask is not None:
+            m = (mask[frame] if mask.dim() == 3 else mask).to(fd.device).bool()
+            fd = torch.where(m, fd, torch.zeros((), dtype=fd.dtype, device=fd.device))
+        stack = build_frame_stack(fd, maps, config.formulation)
+    implicit = config.formulation in (IMPLICIT_STANDARD, IMPLICIT_RGBD)
     decided = {}   # rect -> (kind, result); kind in {"fit", "invalid", "split", "high"}
     level_rects = [(r, 0) for r in _grid(W, H, config.initial_tile)]
     while level_rects:
-        rows = F.fit_rects(d, maps, [tuple(r) for r, _ in level_rects], config.formulation,
-                           frames=frame, mask=mask)
-        nxt = []
-        for (r, lev), row in zip(level_rects, rows):
+        rects = [tuple(r) for r, _ in level_rects]
+        if stack is not None:
+            rows = F.fit_rects_integral(stack, constant, rects, config.formulation)
+        else:
+            rows = F.fit_rects(d, maps, rects, config.formulation, frames=frame, mask=mask)
+        results, fitted_idx = {}, []
+        for i, ((r, lev), row) in enumerate(zip(level_rects, rows)):
             n_valid = int(row["n_points"])
             if n_valid < config.min_valid_fraction * r.area or n_valid == 0 or not row["status"] & F.RECT_FIT:
+                continue
+            results[i] = F._result(row, config.formulation)
+            fitted_idx.append(i)
+        errors = {}
+        if config.error_metric == "max" and fitted_idx:
+            coefs = [results[i].plane.coefficients for i in fitted_idx]
+            mx = F.max_residuals(d, maps, [rects[i] for i in fitted_idx], config.formulation,
+                                 np.stack(coefs) if implicit else np.stack(coefs)[:, :3], frames=frame, mask=mask)
+            errors = dict(zip(fitted_idx, (float(v) for v in mx)))
+        nxt = []
+        for i, (r, lev) in enumerate(level_rects):
+            if i not in results:
                 decided[r] = ("invalid", None)
                 continue
-            res = F._result(row, config.formulation)
-            err = np.inf if res.rms_residual is None else res.rms_residual
+            res = results[i]
+            if config.error_metric == "max":
+                err = errors[i]
+            else:
+                err = np.inf if res.rms_residual is None else res.rms_residual
             if not res.degenerate and err <= config.threshold:
                 decided[r] = ("fit", res)
             elif lev < config.max_depth and r.x1 - r.x0 >= 2 * MIN_TILE_EDGE and r.y1 - r.y0 >= 2 * MIN_TILE_EDGE:
@@ -188,12 +241,12 @@ def segment(depth, maps: TanAngleMaps, config: SegConfig, frame: int = 0, mask=N
         level_rects = nxt
     # leaves in the reference's LIFO order (pending.pop() / pending.extend(children))
     tiles = []
-    stack = [(r, 0) for r in _grid(W, H, config.initial_tile)]
-    while stack:
-        r, lev = stack.pop()
+    pending = [(r, 0) for r in _grid(W, H, config.initial_tile)]
+    while pending:
+        r, lev = pending.pop()
         kind, res = decided[r]
         if kind == "split":
-            stack.extend((c, lev + 1) for c in _children(r))
+            pending.extend((c, lev + 1) for c in _children(r))
         elif kind == "fit":
             tiles.append(Tile(r, TileStatus.FITTED, lev, res))
         elif kind == "high":
@@ -214,9 +267,10 @@ def segment(depth, maps: TanAngleMaps, config: SegConfig, frame: int = 0, mask=N
     else:
         centroids = np.zeros((0, 4))
         warnings.append("no tiles were fitted")
-    lab = torch.full((H, W), UNLABELED, dtype=torch.int16, device=d.device)
+    host = np.full((H, W), UNLABELED, dtype=np.int16)
     for t in fitted:
-        lab[t.rect.y0:t.rect.y1, t.rect.x0:t.rect.x1] = t.cluster
+        host[t.rect.y0:t.rect.y1, t.rect.x0:t.rect.x1] = t.cluster
+    lab = torch.from_numpy(host).to(d.device)  # one upload: the label lattice lives with the depth
     return Segmentation(tiles, lab, centroids, len(fitted),
                         sum(t.status is TileStatus.TOO_INVALID for t in tiles),
                         sum(t.status is TileStatus.HIGH_ERROR for t in tiles), warnings)

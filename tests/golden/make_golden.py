@@ -173,20 +173,26 @@ def run_rects(name, cam, depth_img, stored, dtype, rng, count=60):
     print(name, "rects:", len(rects))
 
 
-def run_segment(name, cam, depth_img, stored, formulations=FORMS):
-    """Reference quadtree segmentation (segment.py:327-431), naive backend (direct sums)."""
+def run_segment(name, cam, depth_img, stored, formulations=FORMS, backend="naive", metric="rms"):
+    """Reference quadtree segmentation (segment.py:327-431) with the given backend and error
+    metric."""
     from rangefit.segment import SegConfig, segment
 
     maps = rf.compute_tan_maps(cam)
-    out = {"depth": stored, "fx": cam.fx, "fy": cam.fy, "cx": cam.cx, "cy": cam.cy}
+    out = {"depth": stored, "fx": cam.fx, "fy": cam.fy, "cx": cam.cx, "cy": cam.cy,
+           "backend": backend, "metric": metric}
+    thresholds = {"implicit-rgbd": 3e-3, "implicit-standard": 3e-2, "explicit-rgbd": 4e-3,
+                  "explicit-standard": 6e-2} if metric == "max" else {}
     for form in formulations:
-        cfg = SegConfig(formulation=form, backend="naive", initial_tile=32, max_depth=3, k=6, seed=3)
+        cfg = SegConfig(formulation=form, backend=backend, initial_tile=32, max_depth=3, k=6, seed=3,
+                        error_metric=metric, rms_threshold=thresholds.get(form))
         seg = segment(depth_img, maps, cfg)
         key = KEYS[form]
         out[f"{key}_rects"] = np.array([tuple(t.rect) for t in seg.tiles], np.int32)
         out[f"{key}_status"] = np.array([t.status.value for t in seg.tiles])
         out[f"{key}_cluster"] = np.array([t.cluster for t in seg.tiles], np.int32)
         out[f"{key}_labels"] = seg.labels
+        out[f"{key}_threshold"] = cfg.threshold
         print(name, form, "tiles", len(seg.tiles), "fitted", seg.n_fitted)
     np.savez_compressed(HERE / f"{name}.npz", **out)
 
@@ -364,6 +370,9 @@ def main():
                              dropout=0.03)
     z_s = np.where(d_s.valid, d_s.values, 0.0).astype(np.float32)
     run_segment("segment_planes", cam_s, rf.DepthImage(values=z_s.astype(np.float64)), z_s)
+    run_segment("segment_planes_integral", cam_s, rf.DepthImage(values=z_s.astype(np.float64)), z_s,
+                backend="integral")
+    run_segment("segment_planes_max", cam_s, rf.DepthImage(values=z_s.astype(np.float64)), z_s, metric="max")
 
     # 1b. explicit validity mask: DepthImage(values, valid=mask) (synth.py:88-94)
     mask = np.random.default_rng(5).random(z32.shape) > 0.2

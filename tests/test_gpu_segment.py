@@ -19,15 +19,25 @@ pytestmark = pytest.mark.gpu
 KEYS = {"implicit-rgbd": "rgbd", "implicit-standard": "std", "explicit-rgbd": "xrgbd", "explicit-standard": "xstd"}
 
 
+CASES = [("segment_planes", "b200"), ("segment_planes", "naive"), ("segment_planes_integral", "integral"),
+         ("segment_planes_max", "b200")]
+
+
+@pytest.mark.parametrize("case,backend", CASES)
 @pytest.mark.parametrize("form", list(rf.FORMULATIONS))
-def test_segment_matches_reference(form):
-    z = np.load(GOLDEN_DIR / "segment_planes.npz")
+def test_segment_matches_reference(form, case, backend):
+    z = np.load(GOLDEN_DIR / f"{case}.npz")
+    key = KEYS[form]
     depth = torch.from_numpy(z["depth"]).cuda()
     H, W = depth.shape
     maps = rf.compute_tan_maps(rf.CameraIntrinsics(float(z["fx"]), float(z["fy"]), float(z["cx"]),
                                                    float(z["cy"]), W, H))
-    seg = S.segment(depth, maps, S.SegConfig(formulation=form, initial_tile=32, max_depth=3, k=6, seed=3))
-    key = KEYS[form]
+    metric = str(z["metric"]) if "metric" in z else "rms"
+    thr = float(z[f"{key}_threshold"]) if f"{key}_threshold" in z else None
+    cfg = S.SegConfig(formulation=form, backend=backend, initial_tile=32, max_depth=3, k=6, seed=3,
+                      error_metric=metric, rms_threshold=thr)
+    src = rf.DepthImage(values=z["depth"].astype(np.float64)) if backend == "integral" else depth
+    seg = S.segment(src, maps, cfg)
     np.testing.assert_array_equal(np.array([tuple(t.rect) for t in seg.tiles]), z[f"{key}_rects"])
     assert [t.status.value for t in seg.tiles] == list(z[f"{key}_status"])
     np.testing.assert_array_equal(np.array([t.cluster for t in seg.tiles]), z[f"{key}_cluster"])

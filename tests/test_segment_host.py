@@ -39,7 +39,9 @@ def test_segconfig_validation():
     with pytest.raises(ValueError):
         S.SegConfig(initial_tile=8, max_depth=3)
     with pytest.raises(ValueError):
-        S.SegConfig(backend="integral")
-    with pytest.raises(NotImplementedError):
-        S.SegConfig(error_metric="max")
+        S.SegConfig(backend="cuda")
+    with pytest.raises(ValueError):
+        S.SegConfig(error_metric="mean")
+    for b in ("b200", "naive", "integral"):
+        assert S.SegConfig(backend=b, error_metric="max").backend == b
     assert S.SegConfig(formulation="explicit-standard").threshold == 0.02
