@@ -68,7 +68,8 @@ def profiled_traffic():
 def link_bandwidth(host_out, out, forms, stream) -> float:
     """Device->host bandwidth of one plain pinned copy of a whole step's outputs (GB/s): the
     ceiling the end-to-end pipeline is held to."""
-    pairs = [(hb, getattr(out[f], k)) for f in forms for k, hb in host_out[f].items()]
+    names = ("normal", "offset", "residual", "curvature", "status")
+    pairs = [(getattr(host_out[f], k), getattr(out[f], k)) for f in forms for k in names]
     nbytes = sum(hb.numel() * hb.element_size() for hb, _ in pairs)
     best = 0.0
     for _ in range(3):
@@ -295,68 +296,30 @@ def run_ours(args, world, rank, local):
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "launch_ms": {f: avg[f] for f in forms}}
 
-    # ---- end to end through the public API with host buffers (pinned)
+    # ---- end to end through the public API with host buffers (pinned): HostPipeline
     host_in = depth.cpu().pin_memory()
-    host_out = {f: {k: torch.empty_like(getattr(out[f], k), device="cpu").pin_memory()
-                    for k in ("normal", "offset", "residual", "curvature", "status")} for f in forms}
-    dev_in = torch.empty_like(depth)
+    pipe = rf.HostPipeline(maps, WINDOW, forms, chunk_frames=8)
     h2d = host_in.numel() * host_in.element_size()
-    d2h = sum(t.numel() * t.element_size() for f in forms for t in host_out[f].values())
-    h2d_stream = torch.cuda.Stream(dev)
-    copy_stream = torch.cuda.Stream(dev)  # D2H (the other copy direction runs concurrently)
-
-    fit_done = {}  # chunk -> event of its last fit (dev_in[chunk] is free again after it)
-
-    def e2e_step(nchunks=8):
-        # chunked 3-stage pipeline: H2D(chunk i+1) || fit(chunk i) || D2H(chunk i-1)
-        cs = B // nchunks
-        done = []
-        for c in range(nchunks):
-            sl = slice(c * cs, (c + 1) * cs)
-            if c in fit_done:
-                h2d_stream.wait_event(fit_done[c])
-            with torch.cuda.stream(h2d_stream):
-                dev_in[sl].copy_(host_in[sl], non_blocking=True)
-                ev_in = torch.cuda.Event()
-                ev_in.record(h2d_stream)
-            stream.wait_event(ev_in)
-            res = rf.fit_pixels(dev_in[sl], maps, WINDOW, forms, stream=stream)
-            ev_fit = torch.cuda.Event()
-            ev_fit.record(stream)
-            fit_done[c] = ev_fit
-            copy_stream.wait_event(ev_fit)
-            with torch.cuda.stream(copy_stream):
-                for f in forms:
-                    for k, hb in host_out[f].items():
-                        src = getattr(res[f], k)
-                        src.record_stream(copy_stream)
-                        hb[sl].copy_(src, non_blocking=True)
-            done.append(res)
-        return done
-
-    for _ in range(2):
-        e2e_step()
+    host_out = pipe.run(host_in)   # warm-up (allocates the pinned outputs and the device ring)
+    d2h = sum(getattr(host_out[f], k).numel() * getattr(host_out[f], k).element_size()
+              for f in forms for k in ("normal", "offset", "residual", "curvature", "status"))
+    pipe.run(host_in)
     torch.cuda.synchronize()
     barrier(world)
     t0 = time.perf_counter()
-    s0 = torch.cuda.Event(enable_timing=True)
-    s1 = torch.cuda.Event(enable_timing=True)
-    s0.record(stream)
     for _ in range(args.steps):
-        e2e_step()
-    copy_stream.synchronize()
-    s1.record(stream)
+        pipe.run(host_in)          # returns once the step's outputs are in host memory
     torch.cuda.synchronize()
-    e2e_ms = max(s0.elapsed_time(s1), (time.perf_counter() - t0) * 1e3)
+    e2e_ms = (time.perf_counter() - t0) * 1e3
     e2e_ms = max_over_ranks(e2e_ms, world)
     e2e_value = world * fits_step * args.steps / (e2e_ms * 1e-3) / 1e6
-    link = link_bandwidth(host_out, out, forms, copy_stream)
+    link = link_bandwidth(host_out, out, forms, pipe.d2h)
 
     launches = rf.launches_per_call(forms) * args.steps
 
     sweep = None
     if rank == 0 and not args.no_sweep:
-        del host_in, host_out, dev_in
+        del host_in, host_out, pipe
         torch.cuda.empty_cache()
         sweep = config_sweep(dev, peak)
 
@@ -379,7 +342,7 @@ def run_ours(args, world, rank, local):
             "roofline": roofline,
             "cpu_baseline": cpu_baseline,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "note": "pinned host buffers, 8-chunk pipeline: H2D, fit and D2H on three streams",
+                    "note": "rf.HostPipeline: pinned host in/out, 8-frame chunks, H2D / fit / D2H on three streams",
                     "d2h_gbs_achieved": d2h * args.steps / (e2e_ms * 1e-3) / 1e9,
                     "d2h_gbs_plain_copy": link,
                     "bound": "PCIe device-to-host copy of the outputs (25 B per pixel-fit)"},

@@ -258,6 +258,88 @@ def fit_pixels(
     return {f: out[f] for f in formulations}
 
 
+class HostPipeline:
+    """Host frames in, host outputs out: the reference-facing call with host buffers.
+
+    Frames stream through the device in chunks of ``chunk_frames``: the H2D copy of chunk
+    i+1, the fit kernels of chunk i and the D2H copies of chunk i-1 run concurrently on three
+    streams (both PCIe directions and the SMs busy at once).  Device buffers are a ring of
+    ``slots`` chunks, so device memory stays bounded for any batch; outputs land in pinned
+    host ``PixelFits`` (allocated once per batch shape and reused).
+    """
+
+    def __init__(self, maps: TanAngleMaps, window: int, formulations=PIXEL_FORMULATIONS, chunk_frames: int = 8,
+                 slots: int = 2):
+        if chunk_frames < 1 or slots < 2:
+            raise ValueError("chunk_frames must be >= 1 and slots >= 2")
+        self.maps, self.window, self.chunk, self.slots = maps, int(window), int(chunk_frames), int(slots)
+        self.formulations = (formulations,) if isinstance(formulations, str) else tuple(formulations)
+        for f in self.formulations:
+            if f not in _FORM_ID:
+                raise ValueError(f"unknown formulation {f!r}; expected one of {FORMULATIONS}")
+        self.device = torch.device("cuda", maps.device)
+        self.h2d = torch.cuda.Stream(self.device)
+        self.compute = torch.cuda.Stream(self.device)
+        self.d2h = torch.cuda.Stream(self.device)
+        self._dev_in = None
+        self._dev_out = None
+        self._host_out = None
+
+    def _buffers(self, B: int, dtype: torch.dtype):
+        H, W, c = self.maps.height, self.maps.width, self.chunk
+        if self._dev_in is None or self._dev_in.dtype != dtype:
+            self._dev_in = torch.empty((self.slots, c, H, W), dtype=dtype, device=self.device)
+            self._dev_out = [{f: PixelFits.empty(c, H, W, self.device) for f in self.formulations}
+                             for _ in range(self.slots)]
+        if self._host_out is None or self._host_out[self.formulations[0]].status.shape[0] != B:
+            pin = dict(pin_memory=True)
+            self._host_out = {f: PixelFits(torch.empty((B, H, W, 3), **pin), torch.empty((B, H, W), **pin),
+                                           torch.empty((B, H, W), **pin), torch.empty((B, H, W), **pin),
+                                           torch.empty((B, H, W), dtype=torch.uint8, **pin))
+                              for f in self.formulations}
+
+    def run(self, depth: torch.Tensor) -> dict:
+        """depth: host tensor [B, H, W] (float32/float64 metres or uint16 mm; pinned for
+        asynchronous copies).  Returns ``{formulation: PixelFits}`` of pinned host tensors,
+        complete when this returns and reused by the next ``run`` of the same batch size."""
+        if depth.is_cuda:
+            raise ValueError("HostPipeline.run takes host frames; use fit_pixels for device tensors")
+        d = depth.unsqueeze(0) if depth.dim() == 2 else depth
+        if d.dim() != 3 or tuple(d.shape[1:]) != (self.maps.height, self.maps.width):
+            raise ValueError(f"depth must be [B, {self.maps.height}, {self.maps.width}], got {tuple(depth.shape)}")
+        _depth_dtype(d)  # validates the element type
+        d = d.contiguous()
+        B = d.shape[0]
+        self._buffers(B, d.dtype)
+        slot_free = [None] * self.slots   # D2H done with the slot's outputs (and the fit with its input)
+        for i, b0 in enumerate(range(0, B, self.chunk)):
+            b1 = min(B, b0 + self.chunk)
+            k = i % self.slots
+            src = self._dev_in[k, :b1 - b0]
+            if slot_free[k] is not None:
+                self.h2d.wait_event(slot_free[k])
+            with torch.cuda.stream(self.h2d):
+                src.copy_(d[b0:b1], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(self.h2d)
+            self.compute.wait_event(ev_in)
+            outs = {f: PixelFits(*(t[:b1 - b0] for t in (o.normal, o.offset, o.residual, o.curvature, o.status)))
+                    for f, o in self._dev_out[k].items()}
+            fit_pixels(src, self.maps, self.window, self.formulations, out=outs, stream=self.compute)
+            ev_fit = torch.cuda.Event()
+            ev_fit.record(self.compute)
+            self.d2h.wait_event(ev_fit)
+            with torch.cuda.stream(self.d2h):
+                for f in self.formulations:
+                    for name in ("normal", "offset", "residual", "curvature", "status"):
+                        getattr(self._host_out[f], name)[b0:b1].copy_(getattr(outs[f], name), non_blocking=True)
+                ev_out = torch.cuda.Event()
+                ev_out.record(self.d2h)
+            slot_free[k] = ev_out
+        self.d2h.synchronize()
+        return self._host_out
+
+
 def launches_per_call(formulations=PIXEL_FORMULATIONS) -> int:
     fmask = 0
     for f in formulations:

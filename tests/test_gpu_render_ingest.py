@@ -88,3 +88,20 @@ def test_batched_ingest(tmp_path):
     for f in rf.PIXEL_FORMULATIONS:
         torch.testing.assert_close(a[f].normal, b[f].normal, rtol=0, atol=0, equal_nan=True)
         torch.testing.assert_close(a[f].status, b[f].status, rtol=0, atol=0)
+
+
+def test_host_pipeline_equals_device_call():
+    from paper_2103_06644_b200 import scenes
+    cfg = scenes.small_config("C2", 160, 120)
+    depth = scenes.render_batch(cfg, frames=11, device="cuda")
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(cfg.f, cfg.f, cfg.cx, cfg.cy, cfg.width, cfg.height))
+    ref = rf.fit_pixels(depth, maps, 5)
+    pipe = rf.HostPipeline(maps, 5, chunk_frames=4, slots=2)   # 3 chunks, the last one short
+    for _ in range(2):                                          # second run reuses the buffers
+        got = pipe.run(depth.cpu().pin_memory())
+        for f in rf.PIXEL_FORMULATIONS:
+            for k in ("normal", "offset", "residual", "curvature", "status"):
+                torch.testing.assert_close(getattr(got[f], k), getattr(ref[f], k).cpu(), rtol=0, atol=0,
+                                           equal_nan=True)
+    with pytest.raises(ValueError):
+        pipe.run(depth)  # device tensors go through fit_pixels
