@@ -868,9 +868,16 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
-  const bool tma = getenv("RF_DISABLE_TMA") == nullptr &&
-                   make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
   const int esz = elem_size(dtype);
+  // TMA double buffers only when both spaces' shared-memory footprint still fits the
+  // opt-in limit (large radii with wide elements fall back to the LDG halo path)
+  int dev = 0, smem_optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const bool tma_fits = smem_bytes(VAR_STD, r, true, esz) <= (size_t)smem_optin &&
+                        smem_bytes(VAR_DF, r, true, esz) <= (size_t)smem_optin;
+  const bool tma = getenv("RF_DISABLE_TMA") == nullptr && tma_fits &&
+                   make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
   // one launch per space: standard (implicit/explicit-standard), rgbd (implicit/explicit-rgbd)
   for (int var = 0; var < 2; ++var) {
     const int fi = var == VAR_STD ? RF_FORM_IMPLICIT_STANDARD : RF_FORM_IMPLICIT_RGBD;

@@ -61,10 +61,17 @@ def test_uint16_millimetres():
             assert m["ok"], (k, f, m)
 
 
-@pytest.mark.parametrize("W,H,window", [(5, 7, 9), (1, 1, 3), (70, 3, 5), (3, 70, 5), (65, 17, 3), (129, 33, 63)])
-def test_odd_sizes_and_large_windows(W, H, window):
+@pytest.mark.parametrize("W,H,window,dtype", [(5, 7, 9, "f32"), (1, 1, 3, "f32"), (70, 3, 5, "f32"),
+                                               (3, 70, 5, "f32"), (65, 17, 3, "f32"), (129, 33, 63, "f32"),
+                                               (128, 32, 63, "f32"), (128, 32, 65, "f32"), (128, 40, 65, "f64"),
+                                               (128, 24, 31, "f64")])
+def test_odd_sizes_and_large_windows(W, H, window, dtype):
+    """Includes 16-byte aligned rows with the largest windows (TMA smem footprint over the
+    opt-in limit -> LDG halo path) and float64 input."""
     cfg = scenes.SceneConfig("C1", 1, W, H, 60.0, (window,), (0.5, 4.0), cells=0, planes=3)
     frame = scenes.render_frame(cfg, 11).cuda()
+    if dtype == "f64":
+        frame = frame.double()
     cam, maps = _maps(cfg)
     out = rf.fit_pixels(frame, maps, window)
     torch.cuda.synchronize()
