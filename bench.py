@@ -386,6 +386,22 @@ def config_sweep(dev, peak):
                 "frames_per_s": frames / (ms * 1e-3),
                 "hbm_frac": 2 * px * (in_b + BYTES_OUT) / (ms * 1e-3) / 1e9 / peak,
                 "full_batch_ms_extrapolated": ms * cfg.frames / frames}
+        if name == "C2":
+            # all four formulations at the headline window (implicit + explicit share each space's pass)
+            out4 = {f: rf.PixelFits.empty(frames, cfg.height, cfg.width, dev) for f in rf.FORMULATIONS}
+            for _ in range(3):
+                rf.fit_pixels(depth, maps, 5, rf.FORMULATIONS, out=out4, stream=stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(20):
+                rf.fit_pixels(depth, maps, 5, rf.FORMULATIONS, out=out4, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 20
+            px = frames * cfg.width * cfg.height
+            res["C2_w5_all4"] = {"frames": frames, "ms_per_pass": ms,
+                                 "Mpixel_fits_per_s": 4 * px / (ms * 1e-3) / 1e6, "formulations": 4}
+            del out4
         del depth, out
         torch.cuda.empty_cache()
     return res
