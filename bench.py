@@ -65,6 +65,29 @@ def profiled_traffic():
         return None
 
 
+def profiled_pipes(kernel: str):
+    """What binds the dominant kernel instead of HBM, from the same committed ncu capture:
+    issue-slot and pipe utilisation (fractions of peak)."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        k = json.loads(p.read_text())["kernels"][kernel]
+    except Exception:
+        return None
+
+    def pct(name):
+        try:
+            return float(str(k[name]).split()[0]) / 100.0
+        except Exception:
+            return None
+
+    return {"bound": "instruction issue under fp64 / MUFU dependency latency",
+            "issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "fp64_pipe": pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+            "xu_pipe": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+            "dram_throughput": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+            "source": "profiles/ncu_summary.json (ncu --set full)"}
+
+
 def link_bandwidth(host_out, out, forms, stream) -> float:
     """Device->host bandwidth of one plain pinned copy of a whole step's outputs (GB/s): the
     ceiling the end-to-end pipeline is held to."""
@@ -294,7 +317,7 @@ def run_ours(args, world, rank, local):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": f"fit_tile_kernel<{dom}>", "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes,
-                "launch_ms": {f: avg[f] for f in forms}}
+                "launch_ms": {f: avg[f] for f in forms}, "binding": profiled_pipes(dom)}
 
     # ---- end to end through the public API with host buffers (pinned): HostPipeline
     host_in = depth.cpu().pin_memory()
