@@ -1,3 +1,4 @@
+"""Diagnostic: a 3-frame batch through the TMA-fed kernels, parity per frame against the oracle."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
