@@ -1,0 +1,95 @@
+"""Randomised parity sweep (seeded, deterministic): frame sizes from 1 pixel to a few tiles
+with ragged edges, every odd window up to 25, the three depth element types, optional
+masks, holes, and hostile values (NaN, +/-inf, negative depths, 1 mm depths among metres)
+-- all four formulations against the oracle, plus the batched-rect kernel on random rects.
+(Subnormal depths are valid input but not a parity case: 1/Z ~ 1e39 puts the disparity
+scatter's entries 80 orders of magnitude apart, where the reference's fp64 Jacobi and any
+other solver return rounding noise.)"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2103_06644_b200 as rf
+from oracle.compare import compare, normal_angles
+from tests.helpers import Cam, gpu_flat, oracle_frame
+
+pytestmark = pytest.mark.gpu
+
+
+def _frame(rng, W, H, dtype):
+    """Planes + noise + holes + hostile values, stored in the requested element type."""
+    fx = float(rng.uniform(0.5, 2.0) * max(W, H))
+    cx, cy = (W - 1) / 2.0, (H - 1) / 2.0
+    tx = (np.arange(W) - cx) / fx
+    ty = (np.arange(H) - cy) / fx
+    n = rng.standard_normal(3)
+    n[2] = -abs(n[2]) - 0.5
+    d0 = rng.uniform(0.4, 6.0)
+    denom = n[0] * tx[None, :] + n[1] * ty[:, None] + n[2]
+    z = -d0 * n[2] / denom
+    z = np.where((z > 0.05) & (z < 30), z, 0.0)
+    z = z + 1.425e-3 * z * z * rng.standard_normal(z.shape)
+    z[rng.random(z.shape) < rng.uniform(0.0, 0.3)] = 0.0
+    if dtype == "u16":
+        mm = np.clip(np.round(z * 1000.0), 0, 65535).astype(np.uint16)
+        return mm, Cam(fx, fx, cx, cy, W, H)
+    hostile = rng.random(z.shape)
+    z = np.where(hostile < 0.01, np.nan, z)
+    z = np.where((hostile >= 0.01) & (hostile < 0.015), np.inf, z)
+    z = np.where((hostile >= 0.015) & (hostile < 0.02), -z - 1.0, z)
+    z = np.where((hostile >= 0.02) & (hostile < 0.022), 1e-3, z)
+    return (z.astype(np.float32) if dtype == "f32" else z.astype(np.float64)), Cam(fx, fx, cx, cy, W, H)
+
+
+CASES = []
+_rng = np.random.default_rng(2103)
+for i in range(48):
+    W = int(_rng.choice([1, 2, 5, 17, 63, 64, 65, 100, 130]))
+    H = int(_rng.choice([1, 3, 15, 16, 17, 40, 71]))
+    window = int(_rng.choice([1, 3, 5, 7, 9, 11, 13, 15, 17, 25]))
+    CASES.append((i, W, H, window, ["f32", "u16", "f64"][i % 3], bool(i % 4 == 1)))
+
+
+@pytest.mark.parametrize("case,W,H,window,dtype,use_mask", CASES)
+def test_random_frames(case, W, H, window, dtype, use_mask):
+    rng = np.random.default_rng(1000 + case)
+    z, cam = _frame(rng, W, H, dtype)
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H))
+    depth = torch.from_numpy(z).cuda()
+    mask = torch.from_numpy(rng.random((H, W)) > 0.15).cuda() if use_mask else None
+    out = rf.fit_pixels(depth, maps, window, rf.FORMULATIONS, mask=mask)
+    torch.cuda.synchronize()
+    for form in rf.FORMULATIONS:
+        ref = oracle_frame(torch.from_numpy(z), cam, window, form, mask=None if mask is None else mask.cpu())
+        m = compare(gpu_flat(out[form]), ref, explicit_fit=form.startswith("explicit"))
+        assert m["ok"], (case, form, {k: m[k] for k in ("status_mismatch", "max_normal_rad", "max_residual_rel",
+                                                         "max_curvature_rel", "nonfit_is_nan")})
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_random_rects(case):
+    rng = np.random.default_rng(500 + case)
+    W, H = int(rng.integers(8, 90)), int(rng.integers(8, 60))
+    dtype = ["f32", "u16", "f64"][case % 3]
+    z, cam = _frame(rng, W, H, dtype)
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H))
+    rects = []
+    for _ in range(40):
+        x0, y0 = int(rng.integers(0, W)), int(rng.integers(0, H))
+        rects.append((x0, y0, int(rng.integers(x0, W + 1)), int(rng.integers(y0, H + 1))))
+    depth = torch.from_numpy(z).cuda()
+    from oracle import oracle as O
+    values, valid = (O.depth_from_millimeters(z) if dtype == "u16" else O.depth_from_meters(z))
+    tx, ty = O.tan_maps(cam.fx, cam.fy, cam.cx, cam.cy, W, H)
+    for form, code in (("implicit-standard", O.STANDARD), ("implicit-rgbd", O.RGBD),
+                       ("explicit-standard", O.EXPLICIT_STANDARD), ("explicit-rgbd", O.EXPLICIT_RGBD)):
+        got = rf.fit_rects(depth, maps, rects, form)
+        ref = O.fit_rects(values, valid, tx, ty, rects, code)
+        np.testing.assert_array_equal(got["n_points"], ref["n"])
+        np.testing.assert_array_equal(got["status"] & 2, ref["status"] & 2)
+        ok = ((ref["status"] & 2) != 0) & ((ref["status"] & 4) == 0) & ((got["status"] & 4) == 0)
+        if ok.any():
+            assert normal_angles(got["coef"][ok, :3], ref["coef"][ok, :3]).max() <= 1e-4, (case, form)
