@@ -79,6 +79,9 @@ struct KParams {
 namespace {
 using namespace rf_dev;
 
+// compile-time radii whose halo tile is not staged as fp64 in shared memory (see NOPRIM)
+__host__ __device__ constexpr bool noprim_radius(int rt) { return rt == 15; }
+
 // bytes per depth element
 __host__ __device__ __forceinline__ int elem_size(int dtype) {
   return dtype == RF_DEPTH_U16_MM ? 2 : dtype == RF_DEPTH_F64_M ? 8 : 4;
@@ -226,12 +229,15 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   const int raw_bytes = USE_TMA ? ((HH_ * HWP * esz + 127) & ~127) : 0;
   unsigned char* raw0 = smem_raw;
   unsigned char* raw1 = smem_raw + raw_bytes;
+  // NOPRIM (large compile-time radius): no converted halo tile in shared memory -- the
+  // column pass converts raw elements as it reads them, so two CTAs fit per SM
+  constexpr bool NOPRIM = noprim_radius(RT) && USE_TMA;
   double* prim = reinterpret_cast<double*>(smem_raw + 2 * raw_bytes);  // [HH_][HW_]
   // column sums are stored residue-major: column c at (c % 4) * VQ + c / 4, so the row
   // pass (threads 4 columns apart) reads consecutive addresses -- no bank conflicts.
-  const int VQ = vq_of(HW_);
+  const int VQ = NOPRIM ? (HW_ + 3) / 4 : vq_of(HW_);
   const int VRS = 4 * VQ;                                                // row stride
-  double* vd = prim + HH_ * HW_;                                         // [NVD][TH][VRS]
+  double* vd = prim + (NOPRIM ? 0 : HH_ * HW_);                          // [NVD][TH][VRS]
   int* vi = reinterpret_cast<int*>(vd + NVD * TH * VRS);                 // [NVI][TH][VRS]
   uint64_t* bars = reinterpret_cast<uint64_t*>(vi + NVI * TH * VRS + ((NVI * TH * VRS) & 1));
 
@@ -260,13 +266,38 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     const int64_t frame = g.frame;
     const int x0 = g.x0, y0 = g.y0;
 
+    // raw halo element (row, col) of this tile -> fp64 primary (NOPRIM path)
+    const unsigned char* raw = (it & 1) ? raw1 : raw0;
+    const int sx = (x0 - r) - box_x(x0 - r, al), sy = (y0 - r) - max(y0 - r, 0);  // raw index shift
+    auto raw_primary = [&](int row, int col) -> double {
+      if (row + sy < 0 || col + sx < 0) return 0.0;  // left / top of the image
+      bool mask_ok = true;
+      if (P.mask) {
+        const int y = y0 - r + row, x = x0 - r + col;
+        mask_ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
+      }
+      const int ri = (row + sy) * HWP + col + sx;
+      return esz == 2   ? primary_masked<VAR>(reinterpret_cast<const unsigned short*>(raw)[ri], mask_ok)
+             : esz == 8 ? primary_masked<VAR>(reinterpret_cast<const double*>(raw)[ri], mask_ok)
+                        : primary_masked<VAR>(reinterpret_cast<const float*>(raw)[ri], mask_ok);
+    };
+
     // ---- 1. halo tile -> primary
-    if (USE_TMA) {
+    if (USE_TMA && NOPRIM) {
       const int b = it & 1;
       mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
-      const unsigned char* raw = b ? raw1 : raw0;
-      const int bx = box_x(x0 - r, al), by = max(y0 - r, 0);
-      const int sx = (x0 - r) - bx, sy = (y0 - r) - by;  // raw index = tile index + shift
+      // the other buffer was consumed by the previous tile (its last reads precede the
+      // end-of-tile barrier): prefetch the next tile into it now
+      if (tid == 0 && t + gridDim.x < total) {
+        const TileGeom gn = tile_of(t + gridDim.x, ntx, nty);
+        unsigned char* dst = b ? raw0 : raw1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bars[b ^ 1], box_bytes);
+        tma_load_tile(dst, &tmap, box_x(gn.x0 - r, al), max(gn.y0 - r, 0), (int)gn.frame, &bars[b ^ 1]);
+      }
+    } else if (USE_TMA) {
+      const int b = it & 1;
+      mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
       if (esz == 2)
         convert_halo<VAR>(prim, reinterpret_cast<const unsigned short*>(raw), HW_, HH_, HWP, sx, sy, P, frame,
                           x0, y0, r, tid);
@@ -392,7 +423,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         for (int k = 0; k < NVI; ++k) bb[k] = 0;
         // dy of input row ii is ii - r (origin: the tile's first output row)
         auto add = [&](int ii, double fdy, int dy, double sg) {
-          const double p = prim[ii * HW_ + col];
+          const double p = NOPRIM ? raw_primary(ii, col) : prim[ii * HW_ + col];
           const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
           if (VAR == VAR_DF) {
             a[0] = fma(sg, p, a[0]);
@@ -510,7 +541,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         }
 #endif
         const int gx = gxs + j;
-        const double pc = prim[(orow + r) * HW_ + xs + j + r];
+        const double pc = NOPRIM ? raw_primary(orow + r, xs + j + r) : prim[(orow + r) * HW_ + xs + j + r];
         uint8_t st = pc > 0.0 ? RF_PIX_INPUT_VALID : 0;
         const int nwin = (int)hi[0];
         float nx = __int_as_float(0x7fc00000), ny = nx, nz = nx, off = nx, res = nx, cur = nx;
@@ -692,9 +723,10 @@ rf_status fail(rf_status s, const char* fmt, const char* a = "", long long b = 0
 size_t smem_bytes(int var, int r, bool tma, int esz) {
   const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
   const int nvd = var == VAR_DF ? 3 : 5, nvi = var == VAR_DF ? 3 : 1;
+  const bool noprim = tma && noprim_radius(r);  // matches the kernel's NOPRIM (RT == r)
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
-  const size_t vrs = 4 * (size_t)vq_of(hw);
-  return 2 * raw + sizeof(double) * ((size_t)hh * hw + (size_t)nvd * TH * vrs) +
+  const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
+  return 2 * raw + sizeof(double) * ((noprim ? 0 : (size_t)hh * hw) + (size_t)nvd * TH * vrs) +
          sizeof(int) * (size_t)nvi * TH * vrs + 8 /* align */ + 2 * sizeof(uint64_t) + 128 /* base align */;
 }
 
