@@ -26,6 +26,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "../../include/rangefit_b200.h"
 #include "rf_internal.h"
 
@@ -803,6 +805,28 @@ cudaError_t launch_radius(const KParams& P, const CUtensorMap& tmap, size_t sm, 
 
 }  // namespace
 
+// Small batches (a few waves of tiles): the two spaces' kernels run concurrently -- the
+// second on a per-device side stream forked from and joined back into the caller's stream --
+// so that each kernel's tail wave overlaps the other's.  The fork/join enqueue is serialised
+// by a mutex so concurrent callers never wait on each other's fork event.
+struct ForkStream {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+ForkStream g_fork[64];
+std::mutex g_fork_mu;
+
+bool fork_stream(int dev, ForkStream*& fs) {
+  if (dev < 0 || dev >= 64) return false;
+  fs = &g_fork[dev];
+  if (!fs->aux) {
+    if (cudaStreamCreateWithFlags(&fs->aux, cudaStreamNonBlocking) != cudaSuccess) return false;
+    if (cudaEventCreateWithFlags(&fs->fork, cudaEventDisableTiming) != cudaSuccess) return false;
+    if (cudaEventCreateWithFlags(&fs->join, cudaEventDisableTiming) != cudaSuccess) return false;
+  }
+  return true;
+}
+
 rf_status rf_set_error(rf_status s, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);
   return s;
@@ -911,6 +935,19 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   const bool tma = getenv("RF_DISABLE_TMA") == nullptr && tma_fits &&
                    make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
   // one launch per space: standard (implicit/explicit-standard), rgbd (implicit/explicit-rgbd)
+  const bool both = (fmask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) &&
+                    (fmask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  ForkStream* fs = nullptr;
+  std::unique_lock<std::mutex> fork_lock(g_fork_mu, std::defer_lock);
+  const bool fork = both && tiles <= (int64_t)8 * nsm && getenv("RF_NO_FORK") == nullptr;
+  if (fork) {
+    fork_lock.lock();
+    if (!fork_stream(dev, fs)) return fail(RF_ERR_CUDA, "side stream creation failed%s");
+    cudaEventRecord(fs->fork, s);
+    cudaStreamWaitEvent(fs->aux, fs->fork, 0);
+  }
   for (int var = 0; var < 2; ++var) {
     const int fi = var == VAR_STD ? RF_FORM_IMPLICIT_STANDARD : RF_FORM_IMPLICIT_RGBD;
     const int fe = var == VAR_STD ? RF_FORM_EXPLICIT_STANDARD : RF_FORM_EXPLICIT_RGBD;
@@ -938,11 +975,22 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     P.batch = batch;
     const size_t sm = smem_bytes(var, r, tma, esz);
     cudaError_t e;
+    const cudaStream_t ls = (fork && var == VAR_DF) ? fs->aux : s;
     if (var == VAR_STD)
-      e = tma ? launch_radius<VAR_STD>(P, tmap, sm, tiles, s) : launch_var<VAR_STD, false, 0>(P, tmap, sm, tiles, s);
+      e = tma ? launch_radius<VAR_STD>(P, tmap, sm, tiles, ls) : launch_var<VAR_STD, false, 0>(P, tmap, sm, tiles, ls);
     else
-      e = tma ? launch_radius<VAR_DF>(P, tmap, sm, tiles, s) : launch_var<VAR_DF, false, 0>(P, tmap, sm, tiles, s);
-    if (e != cudaSuccess) return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+      e = tma ? launch_radius<VAR_DF>(P, tmap, sm, tiles, ls) : launch_var<VAR_DF, false, 0>(P, tmap, sm, tiles, ls);
+    if (e != cudaSuccess) {
+      if (fork) {  // keep the caller's stream joined even on failure
+        cudaEventRecord(fs->join, fs->aux);
+        cudaStreamWaitEvent(s, fs->join, 0);
+      }
+      return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    }
+  }
+  if (fork) {
+    cudaEventRecord(fs->join, fs->aux);
+    cudaStreamWaitEvent(s, fs->join, 0);
   }
   return RF_OK;
 }

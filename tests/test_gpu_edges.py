@@ -148,3 +148,35 @@ def test_single_formulation_and_stream():
     assert list(out) == [rf.IMPLICIT_STANDARD]
     m, _, _ = check_frame(frame, out[rf.IMPLICIT_STANDARD], cam, 5, rf.IMPLICIT_STANDARD)
     assert m["ok"], m
+
+
+def test_concurrent_callers_on_separate_streams():
+    """Small batches fork the second space's kernel onto a side stream; concurrent callers on
+    their own streams must still get exactly the single-caller results."""
+    import threading
+    cfg = scenes.small_config("C1", 160, 120)
+    cam, maps = _maps(cfg)
+    frames = [scenes.render_frame(cfg, 30 + i).cuda() for i in range(2)]
+    ref = [rf.fit_pixels(f, maps, 5) for f in frames]
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(i):
+        try:
+            st = torch.cuda.Stream()
+            for _ in range(20):
+                with torch.cuda.stream(st):
+                    got = rf.fit_pixels(frames[i], maps, 5, stream=st)
+                st.synchronize()
+                for f in rf.PIXEL_FORMULATIONS:
+                    if not torch.equal(torch.nan_to_num(got[f].normal), torch.nan_to_num(ref[i][f].normal)):
+                        errors.append((i, f))
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:4]
