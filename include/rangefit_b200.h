@@ -91,9 +91,11 @@ typedef struct rf_pixel_out {
 
 /* Replaces compute_tan_maps (camera.py:124-135) + the camera-constant channel
  * stack build_constant_channels (integral.py:193-199), once per camera.
- * delta_x / delta_y (H*W float64 host arrays, CameraIntrinsics.delta_*) must be
- * NULL or all-zero: non-separable distortion lattices return
- * RF_ERR_UNSUPPORTED.  Validation mirrors CameraIntrinsics.__post_init__. */
+ * delta_x / delta_y (H*W float64 host arrays, CameraIntrinsics.delta_*) may be NULL
+ * (zero).  Zero lattices keep the separable tables the tile kernels need; non-zero
+ * lattices are stored whole ((x + delta_x - cx) / fx, ...) and every kernel reads them
+ * per pixel (the per-pixel fits then sum each window directly, slower but exact).
+ * Validation mirrors CameraIntrinsics.__post_init__. */
 rf_status rf_tables_create(const rf_intrinsics* intrinsics, const double* delta_x,
                            const double* delta_y, int device, rf_tables** out);
 rf_status rf_tables_destroy(rf_tables* tables);

@@ -77,6 +77,7 @@ struct KParams {
 }  // namespace
 
 #include "rf_solve.cuh"
+#include "rf_general.cuh"
 
 namespace {
 using namespace rf_dev;
@@ -705,6 +706,114 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   }
 }
 
+// ------------------------------------------------------------------ distortion lattices
+// Cameras with non-zero delta_* lattices (camera.py:35-75): the tan maps are not separable,
+// so the tile kernels' exact-integer geometry does not apply.  One thread per output pixel
+// sums its clipped window directly (fp64 moments relative to the pixel's own tan values,
+// rf_general.cuh) and runs the same solve / canonical output as the tile kernels.
+__device__ __forceinline__ void store_fit(const OutPlanes& o, int64_t p, float nx, float ny, float nz, float off,
+                                          float res, float cur, uint8_t st) {
+  o.normal[3 * p + 0] = nx;
+  o.normal[3 * p + 1] = ny;
+  o.normal[3 * p + 2] = nz;
+  o.offset[p] = off;
+  o.residual[p] = res;
+  o.curvature[p] = cur;
+  o.status[p] = st;
+}
+
+template <int VAR, bool EXP>
+__global__ void __launch_bounds__(128) fit_lattice_kernel(const KParams P, const double* lat_x,
+                                                          const double* lat_y) {
+  const int64_t total = P.batch * P.out_frame;
+  const int r = P.r;
+  const bool std_space = VAR == VAR_STD;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t frame = p / P.out_frame;
+    const int rem = (int)(p - frame * P.out_frame);
+    const int y = rem / P.W, x = rem - y * P.W;
+    auto sample = [&](int yy, int xx, double& z) -> bool {
+      const int64_t off = frame * P.frame_stride + (int64_t)yy * P.row_pitch + xx;
+      bool valid;
+      if (P.dtype == RF_DEPTH_U16_MM) {
+        const unsigned short mm = __ldg(reinterpret_cast<const unsigned short*>(P.depth) + off);
+        valid = mm > 0;
+        z = __ddiv_rn((double)mm, 1000.0);
+      } else if (P.dtype == RF_DEPTH_F64_M) {
+        z = __ldg(reinterpret_cast<const double*>(P.depth) + off);
+        valid = z > 0.0 && z <= 1.7976931348623157e308;
+      } else {
+        const float zf = __ldg(reinterpret_cast<const float*>(P.depth) + off);
+        valid = zf > 0.0f && zf <= 3.402823466e38f;
+        z = (double)zf;
+      }
+      if (P.mask) valid = valid && __ldg(P.mask + frame * P.out_frame + (int64_t)yy * P.W + xx) != 0;
+      return valid;
+    };
+    const float qn = __int_as_float(0x7fc00000);
+    float nx = qn, ny = qn, nz = qn, off = qn, res = qn, cur = qn;
+    float ex = qn, ey = qn, ez = qn, eo = qn, eres = qn, ecur = qn;
+    double zc;
+    const uint8_t valid_bit = sample(y, x, zc) ? RF_PIX_INPUT_VALID : 0;
+    uint8_t st = valid_bit, stx = valid_bit;
+    if (valid_bit) {
+      const double txc = __ldg(lat_x + (int64_t)y * P.W + x), tyc = __ldg(lat_y + (int64_t)y * P.W + x);
+      QMoments m;
+      const int ya = max(y - r, 0), yb = min(y + r, P.H - 1), xa = max(x - r, 0), xb = min(x + r, P.W - 1);
+      for (int yy = ya; yy <= yb; ++yy)
+        for (int xx = xa; xx <= xb; ++xx) {
+          double z;
+          if (!sample(yy, xx, z)) continue;
+          const int64_t li = (int64_t)yy * P.W + xx;
+          q_sample(std_space, z, __ldg(lat_x + li) - txc, __ldg(lat_y + li) - tyc, m);
+        }
+      const int nwin = (int)m.n;
+      if (nwin >= (EXP ? 3 : 4)) {
+        Sym3 C;
+        double mu0, mu1, mu2;
+        q_to_scatter(std_space, m, txc, tyc, C, mu0, mu1, mu2);
+        const double nd = m.n;
+        float kap = 0.0f;
+        if (P.do_imp && nwin >= 4) {
+          WindowFit f;
+          solve_window(C, mu0, mu1, mu2, nd, f);
+          if (std_space) finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
+          else finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
+          res = fsqrt(fmaxf((float)(f.lam / nd), 0.0f));
+          cur = kap = f.kappa;
+          st |= RF_PIX_FIT | (f.degenerate ? RF_PIX_DEGENERATE : 0);
+        }
+        if (EXP && P.do_exp) {
+          if (!(P.do_imp && nwin >= 4)) kap = curvature_only(C);
+          ExplicitFit e;
+          explicit_solve(C, mu0, mu1, mu2, nd, e);
+          if (std_space) finish_plane(e.a, e.b, -1.0, e.c, ex, ey, ez, eo);
+          else finish_plane(e.a, e.b, e.c, -1.0, ex, ey, ez, eo);
+          eres = fsqrt(fmaxf((float)(e.ss / nd), 0.0f));
+          ecur = kap;
+          stx |= RF_PIX_FIT | (e.degenerate ? RF_PIX_DEGENERATE : 0);
+        }
+      }
+    }
+    if (P.do_imp) store_fit(P.imp, p, nx, ny, nz, off, res, cur, st);
+    if (EXP && P.do_exp) store_fit(P.exp, p, ex, ey, ez, eo, eres, ecur, stx);
+  }
+}
+
+template <int VAR>
+cudaError_t launch_lattice(const KParams& P, const double* lat_x, const double* lat_y, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t total = P.batch * P.out_frame;
+  const int64_t want = (total + 127) / 128;
+  const int64_t grid = want < (int64_t)sms * 16 ? want : (int64_t)sms * 16;
+  if (P.do_exp) fit_lattice_kernel<VAR, true><<<(unsigned)grid, 128, 0, s>>>(P, lat_x, lat_y);
+  else fit_lattice_kernel<VAR, false><<<(unsigned)grid, 128, 0, s>>>(P, lat_x, lat_y);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ tables
 __global__ void tan_table_kernel(double* tx, double* ty, int W, int H, double fx, double fy,
                                  double cx, double cy) {
@@ -854,12 +963,9 @@ rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const
   if (!(in->cx >= 0 && in->cx < in->width && in->cy >= 0 && in->cy < in->height))
     return fail(RF_ERR_ARGUMENT, "principal point outside the image%s");
   const int64_t n = (int64_t)in->width * in->height;
-  for (int64_t i = 0; delta_x && i < n; ++i)
-    if (delta_x[i] != 0.0)
-      return fail(RF_ERR_UNSUPPORTED, "non-zero delta_x lattice%s: the sm_100a path needs separable tan maps");
-  for (int64_t i = 0; delta_y && i < n; ++i)
-    if (delta_y[i] != 0.0)
-      return fail(RF_ERR_UNSUPPORTED, "non-zero delta_y lattice%s: the sm_100a path needs separable tan maps");
+  bool separable = true;
+  for (int64_t i = 0; delta_x && i < n && separable; ++i) separable = delta_x[i] == 0.0;
+  for (int64_t i = 0; delta_y && i < n && separable; ++i) separable = delta_y[i] == 0.0;
   int prev = 0;
   cudaGetDevice(&prev);
   cudaError_t e = cudaSetDevice(device);
@@ -867,6 +973,31 @@ rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const
   rf_tables* t = new rf_tables();
   t->intr = *in;
   t->device = device;
+  if (!separable) {
+    // compute_tan_maps (camera.py:131-134): ((x + delta_x) - cx) / fx, evaluated on the host
+    // in the reference's operation order (plain IEEE double), then kept on the device
+    double* hx = new double[n];
+    double* hy = new double[n];
+    for (int y = 0; y < in->height; ++y)
+      for (int x = 0; x < in->width; ++x) {
+        const int64_t i = (int64_t)y * in->width + x;
+        hx[i] = (((double)x + (delta_x ? delta_x[i] : 0.0)) - in->cx) / in->fx;
+        hy[i] = (((double)y + (delta_y ? delta_y[i] : 0.0)) - in->cy) / in->fy;
+      }
+    e = cudaMalloc(&t->lat_x, sizeof(double) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&t->lat_y, sizeof(double) * n);
+    if (e == cudaSuccess) e = cudaMemcpy(t->lat_x, hx, sizeof(double) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(t->lat_y, hy, sizeof(double) * n, cudaMemcpyHostToDevice);
+    delete[] hx;
+    delete[] hy;
+    if (e != cudaSuccess) {
+      cudaFree(t->lat_x);
+      cudaFree(t->lat_y);
+      cudaSetDevice(prev);
+      delete t;
+      return fail(RF_ERR_CUDA, "rf_tables_create: %s", cudaGetErrorString(e));
+    }
+  }
   e = cudaMalloc(&t->tan_x, sizeof(double) * in->width);
   if (e == cudaSuccess) e = cudaMalloc(&t->tan_y, sizeof(double) * in->height);
   if (e == cudaSuccess) {
@@ -880,6 +1011,8 @@ rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const
   if (e != cudaSuccess) {
     cudaFree(t->tan_x);
     cudaFree(t->tan_y);
+    cudaFree(t->lat_x);
+    cudaFree(t->lat_y);
     delete t;
     return fail(RF_ERR_CUDA, "rf_tables_create: %s", cudaGetErrorString(e));
   }
@@ -891,6 +1024,8 @@ rf_status rf_tables_destroy(rf_tables* t) {
   if (!t) return RF_OK;
   cudaFree(t->tan_x);
   cudaFree(t->tan_y);
+  cudaFree(t->lat_x);
+  cudaFree(t->lat_y);
   delete t;
   return RF_OK;
 }
@@ -976,7 +1111,10 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     const size_t sm = smem_bytes(var, r, tma, esz);
     cudaError_t e;
     const cudaStream_t ls = (fork && var == VAR_DF) ? fs->aux : s;
-    if (var == VAR_STD)
+    if (t->lat_x)  // non-separable tan maps
+      e = var == VAR_STD ? launch_lattice<VAR_STD>(P, t->lat_x, t->lat_y, ls)
+                         : launch_lattice<VAR_DF>(P, t->lat_x, t->lat_y, ls);
+    else if (var == VAR_STD)
       e = tma ? launch_radius<VAR_STD>(P, tmap, sm, tiles, ls) : launch_var<VAR_STD, false, 0>(P, tmap, sm, tiles, ls);
     else
       e = tma ? launch_radius<VAR_DF>(P, tmap, sm, tiles, ls) : launch_var<VAR_DF, false, 0>(P, tmap, sm, tiles, ls);

@@ -40,6 +40,8 @@ struct ChanParams {
   const uint8_t* mask;
   const double* tan_x;
   const double* tan_y;
+  const double* lat_x;  // non-separable lattices (distortion offsets) or null
+  const double* lat_y;
   const double* src;  // generic channel (rf_integral) when channel < 0
   int64_t src_pitch;
   int H, W, channel;
@@ -73,7 +75,7 @@ __device__ __forceinline__ double channel_value(const ChanParams& P, int y, int 
     const double v = P.src[(int64_t)y * P.src_pitch + x];
     return (P.mask && P.mask[(int64_t)y * P.W + x] == 0) ? 0.0 : v;
   }
-  const double tx = P.tan_x[x], ty = P.tan_y[y];
+  const double tx = rf_tan(P.tan_x, P.lat_x, P.W, x, y, true), ty = rf_tan(P.tan_y, P.lat_y, P.W, x, y, false);
   switch (P.channel) {  // camera constants: not masked
     case RF_CH_ONES: return 1.0;
     case RF_CH_TX2: return tx * tx;
@@ -477,6 +479,8 @@ rf_status rf_build_channel(const rf_tables* t, const void* depth, int dtype, int
   P.mask = mask;
   P.tan_x = t->tan_x;
   P.tan_y = t->tan_y;
+  P.lat_x = t->lat_x;
+  P.lat_y = t->lat_y;
   P.H = t->intr.height;
   P.W = t->intr.width;
   P.channel = channel;

@@ -6,9 +6,21 @@
 struct rf_tables {
   rf_intrinsics intr;
   int device;
-  double* tan_x;  // [W] device
-  double* tan_y;  // [H] device
+  double* tan_x;  // [W] device: (x - cx) / fx
+  double* tan_y;  // [H] device: (y - cy) / fy
+  // non-zero distortion lattices (CameraIntrinsics.delta_*): the full tan lattices
+  // (x + delta_x - cx) / fx and (y + delta_y - cy) / fy, [H][W] device; null when separable
+  double* lat_x;
+  double* lat_y;
 };
+
+// tan_x / tan_y of pixel (x, y): the lattice when the camera has distortion offsets
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline double rf_tan(const double* table, const double* lattice, int W, int x, int y, bool along_x) {
+  return lattice ? lattice[(long long)y * W + x] : table[along_x ? x : y];
+}
 
 // thread-local error message behind rf_last_error()
 rf_status rf_set_error(rf_status s, const char* msg);

@@ -17,6 +17,7 @@
 #include "../../include/rangefit_b200.h"
 #include "rf_internal.h"
 #include "rf_solve.cuh"
+#include "rf_general.cuh"
 
 namespace {
 using namespace rf_dev;
@@ -28,6 +29,8 @@ struct RectParams {
   const uint8_t* mask;
   const double* tan_x;
   const double* tan_y;
+  const double* lat_x;  // non-separable tan lattices [H][W] (distortion offsets), else null
+  const double* lat_y;
   double ifx, ify;
   int64_t row_pitch, frame_stride, out_frame, batch;
   int H, W, dtype, formulation;
@@ -107,6 +110,23 @@ __global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams 
     }
     if (P.mask) valid = valid && __ldg(P.mask + (int64_t)R.frame * P.out_frame + (int64_t)y * P.W + x) != 0;
     if (!valid) continue;
+    if (P.lat_x) {  // general moments of q about the rect centre's tan values (rf_general.cuh)
+      const int64_t li = (int64_t)y * P.W + x, lc = (int64_t)oy * P.W + ox;
+      const double dtx = P.lat_x[li] - P.lat_x[lc], dty = P.lat_y[li] - P.lat_y[lc];
+      const double q0 = space_std ? z * dtx : dtx, q1 = space_std ? z * dty : dty;
+      const double q2 = space_std ? z : 1.0 / z;
+      s0 += q0;
+      s1 += q1;
+      s2 += q2;
+      s3 = fma(q0, q0, s3);
+      s4 = fma(q0, q1, s4);
+      s5 = fma(q0, q2, s5);
+      s6 = fma(q1, q1, s6);
+      s7 = fma(q1, q2, s7);
+      s8 = fma(q2, q2, s8);
+      n += 1;
+      continue;
+    }
     const int dx = x - ox, dy = y - oy;
     const double fdx = (double)dx, fdy = (double)dy;
     if (!space_std) {
@@ -139,7 +159,7 @@ __global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams 
   s1 = block_sum(s1, redd);
   s2 = block_sum(s2, redd);
   s3 = block_sum(s3, redd);
-  if (space_std) {
+  if (space_std || P.lat_x) {
     s4 = block_sum(s4, redd);
     s5 = block_sum(s5, redd);
     s6 = block_sum(s6, redd);
@@ -147,7 +167,7 @@ __global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams 
     s8 = block_sum(s8, redd);
   }
   n = block_sum_ll(n, redl);
-  if (!space_std) {
+  if (!space_std && !P.lat_x) {
     gx = block_sum_ll(gx, redl);
     gy = block_sum_ll(gy, redl);
     gxx = block_sum_ll(gxx, redl);
@@ -170,7 +190,13 @@ __global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams 
     const double nd = (double)n, invn = 1.0 / nd;
     Sym3 C;
     double mu0, mu1, mu2;
-    if (!space_std) {
+    if (P.lat_x) {
+      QMoments m;
+      m.n = nd;
+      m.s0 = s0; m.s1 = s1; m.s2 = s2; m.s00 = s3; m.s01 = s4; m.s02 = s5; m.s11 = s6; m.s12 = s7; m.s22 = s8;
+      const int64_t lc = (int64_t)oy * P.W + ox;
+      q_to_scatter(space_std, m, P.lat_x[lc], P.lat_y[lc], C, mu0, mu1, mu2);
+    } else if (!space_std) {
       // geometry moments about the rect centre (|gx|, |gy| small relative to gxx, gyy)
       const double fgx = (double)gx, fgy = (double)gy;
       const double cq00 = fma(-fgx, fgx * invn, (double)gxx);
@@ -286,7 +312,7 @@ __global__ void __launch_bounds__(RT_THREADS) max_residual_kernel(const MaxResPa
     }
     if (P.mask) valid = valid && __ldg(P.mask + (int64_t)R.frame * P.out_frame + (int64_t)y * P.W + x) != 0;
     if (!valid) continue;
-    const double tx = P.tan_x[x], ty = P.tan_y[y];
+    const double tx = rf_tan(P.tan_x, P.lat_x, P.W, x, y, true), ty = rf_tan(P.tan_y, P.lat_y, P.W, x, y, false);
     double r;
     switch (P.formulation) {
       case RF_FORM_IMPLICIT_STANDARD:  // c0 z tx + c1 z ty + c2 z + c3
@@ -334,6 +360,8 @@ rf_status rf_max_residuals(const rf_tables* t, const void* depth, int dtype, int
   P.mask = mask;
   P.tan_x = t->tan_x;
   P.tan_y = t->tan_y;
+  P.lat_x = t->lat_x;
+  P.lat_y = t->lat_y;
   P.ifx = 1.0 / t->intr.fx;
   P.ify = 1.0 / t->intr.fy;
   P.row_pitch = row_pitch;
@@ -375,6 +403,8 @@ rf_status rf_fit_rects(const rf_tables* t, const void* depth, int dtype, int64_t
   P.mask = mask;
   P.tan_x = t->tan_x;
   P.tan_y = t->tan_y;
+  P.lat_x = t->lat_x;
+  P.lat_y = t->lat_y;
   P.ifx = 1.0 / t->intr.fx;
   P.ify = 1.0 / t->intr.fy;
   P.row_pitch = row_pitch;

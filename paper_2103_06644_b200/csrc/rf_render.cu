@@ -20,6 +20,8 @@ constexpr int MAX_PLANES = 256;
 struct RenderParams {
   const double* tan_x;
   const double* tan_y;
+  const double* lat_x;  // non-separable lattices (distortion offsets) or null
+  const double* lat_y;
   const double* planes;  // [nplanes][4]
   const int32_t* rects;  // [nplanes][4], already normalised to [0, W] x [0, H]
   int nplanes, H, W;
@@ -35,7 +37,7 @@ __global__ void render_kernel(const RenderParams P) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y;
   if (x >= P.W || y >= P.H) return;
-  const double tx = P.tan_x[x], ty = P.tan_y[y];
+  const double tx = rf_tan(P.tan_x, P.lat_x, P.W, x, y, true), ty = rf_tan(P.tan_y, P.lat_y, P.W, x, y, false);
   double best = INFINITY;
   int label = 0;  // np.argmin of an all-inf column is 0; invalid pixels are relabelled below
   for (int p = 0; p < P.nplanes; ++p) {
@@ -77,7 +79,7 @@ rf_status rf_render_planes(const rf_tables* t, const double* planes, const int32
     return rf_set_error(RF_ERR_ARGUMENT, "rf_render_planes: need 1..256 planes (uint8 labels, 255 = invalid)");
   if (!(dropout >= 0.0 && dropout < 1.0)) return rf_set_error(RF_ERR_ARGUMENT, "dropout must be in [0, 1)");
   if (cudaSetDevice(t->device) != cudaSuccess) return rf_set_error(RF_ERR_CUDA, "cudaSetDevice failed");
-  RenderParams P{t->tan_x, t->tan_y, planes, rects, nplanes, t->intr.height, t->intr.width, eps, uniforms,
+  RenderParams P{t->tan_x, t->tan_y, t->lat_x, t->lat_y, planes, rects, nplanes, t->intr.height, t->intr.width, eps, uniforms,
                  noise_coefficient, dropout, depth, valid, labels};
   const dim3 grid((unsigned)((P.W + 127) / 128), (unsigned)P.H);
   render_kernel<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(P);

@@ -100,18 +100,16 @@ class TanAngleMaps:
 
     @property
     def tan_x(self) -> np.ndarray:
-        """The reference's (H, W) lattice ``(x + delta_x - cx) / fx`` (camera.py:131-134), as a
-        read-only broadcast of the one row the device table holds (delta = 0)."""
+        """The reference's (H, W) lattice ``(x + delta_x - cx) / fx`` (camera.py:131-134), the
+        same values the device tables hold (one row when delta = 0, the lattice otherwise)."""
         i = self.intrinsics
-        row = (np.arange(i.width, dtype=np.float64)[None, :] + 0.0 - i.cx) / i.fx
-        return np.broadcast_to(row, (i.height, i.width))
+        return (np.arange(i.width, dtype=np.float64)[None, :] + i.delta_x - i.cx) / i.fx
 
     @property
     def tan_y(self) -> np.ndarray:
         """The reference's (H, W) lattice ``(y + delta_y - cy) / fy`` (camera.py:131-134)."""
         i = self.intrinsics
-        col = (np.arange(i.height, dtype=np.float64)[:, None] + 0.0 - i.cy) / i.fy
-        return np.broadcast_to(col, (i.height, i.width))
+        return (np.arange(i.height, dtype=np.float64)[:, None] + i.delta_y - i.cy) / i.fy
 
     @property
     def handle(self) -> ctypes.c_void_p:

@@ -73,6 +73,8 @@ def run_case(name, cam, depth_img: "rf.DepthImage", stored, window, dtype):
     r = window // 2
     out = {"depth": stored, "fx": cam.fx, "fy": cam.fy, "cx": cam.cx, "cy": cam.cy,
            "window": window, "dtype": dtype}
+    if np.any(cam.delta_x != 0) or np.any(cam.delta_y != 0):
+        out["delta_x"], out["delta_y"] = cam.delta_x, cam.delta_y
     if depth_img.valid is not None:
         out["valid"] = depth_img.valid.astype(np.uint8)
     for form in FORMS:
@@ -349,6 +351,7 @@ def main():
 
     run_render("render_planes")
 
+
     # integral backend: a holey frame (hole-corrected rgbd stacks) and a hole-free crop
     cam_i = rf.CameraIntrinsics(fx=60.0, fy=60.0, cx=15.5, cy=11.5, width=32, height=24)
     z_i = z32[12:36, 16:48].copy()
@@ -408,6 +411,17 @@ def main():
     d5, _ = rf.render_scene(scene5, maps5, noise=rf.NoiseModel(), seed=12, dropout=0.05)
     z5 = np.where(d5.valid, d5.values, 0.0).astype(np.float32)
     run_case("near_far_w7", cam5, rf.DepthImage(values=z5.astype(np.float64)), z5, 7, "f32")
+
+    # 6. non-separable tan maps: per-pixel distortion offsets (CameraIntrinsics.delta_*)
+    rng_d = np.random.default_rng(41)
+    cam6 = rf.CameraIntrinsics(fx=60.0, fy=58.0, cx=23.5, cy=17.5, width=48, height=36,
+                               delta_x=rng_d.uniform(-0.4, 0.4, (36, 48)),
+                               delta_y=rng_d.uniform(-0.4, 0.4, (36, 48)))
+    maps6 = rf.compute_tan_maps(cam6)
+    scene6 = rf.SyntheticScene((random_plane(rng_d, 1.0, 3.0), random_plane(rng_d, 1.0, 3.0)))
+    d6, _ = rf.render_scene(scene6, maps6, noise=rf.NoiseModel(), seed=13, dropout=0.05)
+    z6 = np.where(d6.valid, d6.values, 0.0).astype(np.float32)
+    run_case("distorted_f32_w5", cam6, rf.DepthImage(values=z6.astype(np.float64)), z6, 5, "f32")
 
 
 if __name__ == "__main__":

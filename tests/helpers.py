@@ -23,7 +23,8 @@ def oracle_frame(depth: torch.Tensor, cam, window: int, formulation: str, pixels
     if mask is not None:
         m = mask.cpu().numpy() if isinstance(mask, torch.Tensor) else np.asarray(mask)
         valid = valid & m.astype(bool)
-    tx, ty = O.tan_maps(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height)
+    tx, ty = O.tan_maps(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height,
+                        getattr(cam, "delta_x", None), getattr(cam, "delta_y", None))
     return O.fit_pixels(values, valid, tx, ty, window, FORM_CODE[formulation], backend=backend,
                         pixels=pixels)
 
@@ -51,12 +52,19 @@ def check_frame(depth_gpu, fits, cam, window, formulation, frame=0, pixels=None,
 # ------------------------------------------------------------ golden fixtures
 GOLDEN_DIR = __import__("pathlib").Path(__file__).resolve().parent / "golden"
 GOLDEN_CASES = ("planes_f32_w3", "planes_f32_w5", "planes_f32_mask_w5", "planes_u16_w5",
-                "frontal_z3_w5", "half_invalid_w3", "near_far_w7")
+                "frontal_z3_w5", "half_invalid_w3", "near_far_w7", "distorted_f32_w5")
 
 
 class Cam:
-    def __init__(self, fx, fy, cx, cy, width, height):
+    def __init__(self, fx, fy, cx, cy, width, height, delta_x=None, delta_y=None):
         self.fx, self.fy, self.cx, self.cy, self.width, self.height = fx, fy, cx, cy, width, height
+        self.delta_x, self.delta_y = delta_x, delta_y
+
+    def intrinsics(self):
+        """The package's CameraIntrinsics (distortion lattices included)."""
+        import paper_2103_06644_b200 as rf
+        return rf.CameraIntrinsics(self.fx, self.fy, self.cx, self.cy, self.width, self.height,
+                                   self.delta_x, self.delta_y)
 
 
 def load_golden(name: str) -> dict:
@@ -64,7 +72,8 @@ def load_golden(name: str) -> dict:
     z = np.load(GOLDEN_DIR / f"{name}.npz")
     depth = z["depth"]
     H, W = depth.shape
-    cam = Cam(float(z["fx"]), float(z["fy"]), float(z["cx"]), float(z["cy"]), W, H)
+    cam = Cam(float(z["fx"]), float(z["fy"]), float(z["cx"]), float(z["cy"]), W, H,
+              z["delta_x"] if "delta_x" in z.files else None, z["delta_y"] if "delta_y" in z.files else None)
     g = {"depth": depth, "cam": cam, "window": int(z["window"]), "dtype": str(z["dtype"]),
          "valid": z["valid"].astype(bool) if "valid" in z.files else None}
     for key, form in (("rgbd", "implicit-rgbd"), ("std", "implicit-standard"),

@@ -60,18 +60,6 @@ def test_tables_create_validation(fx, fy, cx, cy, w, h, msg):
     assert not out
 
 
-def test_tables_create_rejects_nonseparable_distortion():
-    lib = N.load()
-    intr = N.RfIntrinsics(10.0, 10.0, 1.5, 1.5, 4, 4)
-    dx = np.zeros(16)
-    dx[5] = 0.25
-    out = ctypes.c_void_p()
-    st = lib.rf_tables_create(ctypes.byref(intr), dx.ctypes.data, None, 0, ctypes.byref(out))
-    assert st == N.RF_ERR_UNSUPPORTED
-    with pytest.raises(NotImplementedError):
-        N.check(st, "compute_tan_maps")
-
-
 def test_fit_pixels_null_arguments():
     lib = N.load()
     st = lib.rf_fit_pixels(None, None, 0, 1, 4, 4, 4, None, 5, 3, None, None)

@@ -22,7 +22,8 @@ def test_oracle_matches_reference_golden(case, form):
     ref = g[form]
     mask = golden_mask(g)
     got = O.fit_pixels(*(_vals(g, mask)), *O.tan_maps(g["cam"].fx, g["cam"].fy, g["cam"].cx, g["cam"].cy,
-                                                      g["cam"].width, g["cam"].height),
+                                                      g["cam"].width, g["cam"].height,
+                                                      g["cam"].delta_x, g["cam"].delta_y),
                        g["window"], form, want_coef=True)
     # status: bit-exact (including the degenerate bit: same algorithm)
     np.testing.assert_array_equal(got["status"], ref["status"])
@@ -175,3 +176,13 @@ def test_oracle_rects_match_reference(form):
     assert np.abs(got["coef"][ok] - ref["coef"][ok]).max() <= 1e-6
     np.testing.assert_allclose(got["rms"][ok], ref["rms"][ok], rtol=1e-5,
                                atol=float(np.sqrt(1e-10 * np.nanmax(ref["scale"]))))
+
+
+def test_tan_maps_known_answers():
+    """The reference's camera known-answer tests (tests/test_camera.py:27-40)."""
+    tx, _ = O.tan_maps(500.0, 500.0, 320.0, 240.0, 1024, 480)
+    assert tx[0, 820] == 1.0  # one focal length right of cx
+    dx = np.full((480, 640), 0.25)
+    tx, ty = O.tan_maps(525.0, 525.0, 319.5, 239.5, 640, 480, dx)
+    assert tx[7, 100] == pytest.approx(-0.4176190476190476, rel=1e-15)
+    assert ty[240, 3] == pytest.approx((240 - 239.5) / 525.0, rel=1e-15)
