@@ -25,6 +25,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <stdarg.h>
 
 #include <mutex>
 
@@ -825,9 +826,11 @@ __global__ void tan_table_kernel(double* tx, double* ty, int W, int H, double fx
 
 thread_local char g_err[512] = "";
 
-rf_status fail(rf_status s, const char* fmt, const char* a = "", long long b = 0,
-               long long c = 0) {
-  snprintf(g_err, sizeof(g_err), fmt, a, b, c);
+__attribute__((format(printf, 2, 3))) rf_status fail(rf_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
   return s;
 }
 
@@ -954,14 +957,14 @@ int32_t rf_launches_per_call(int32_t formulation_mask) {
 
 rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const double* delta_y,
                            int device, rf_tables** out) {
-  if (!in || !out) return fail(RF_ERR_ARGUMENT, "rf_tables_create: null argument%s");
+  if (!in || !out) return fail(RF_ERR_ARGUMENT, "rf_tables_create: null argument");
   *out = nullptr;
   // CameraIntrinsics.__post_init__ (camera.py:54-63)
   if (!(in->fx > 0) || !(in->fy > 0))
-    return fail(RF_ERR_ARGUMENT, "focal lengths must be positive%s");
-  if (in->width <= 0 || in->height <= 0) return fail(RF_ERR_ARGUMENT, "image size must be positive%s");
+    return fail(RF_ERR_ARGUMENT, "focal lengths must be positive");
+  if (in->width <= 0 || in->height <= 0) return fail(RF_ERR_ARGUMENT, "image size must be positive");
   if (!(in->cx >= 0 && in->cx < in->width && in->cy >= 0 && in->cy < in->height))
-    return fail(RF_ERR_ARGUMENT, "principal point outside the image%s");
+    return fail(RF_ERR_ARGUMENT, "principal point outside the image");
   const int64_t n = (int64_t)in->width * in->height;
   bool separable = true;
   for (int64_t i = 0; delta_x && i < n && separable; ++i) separable = delta_x[i] == 0.0;
@@ -1033,26 +1036,25 @@ rf_status rf_tables_destroy(rf_tables* t) {
 rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_t batch,
                         int32_t H, int32_t W, int64_t row_pitch, const uint8_t* mask,
                         int32_t window, int32_t fmask, const rf_pixel_out* outs, void* stream) {
-  if (!t) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null tables%s");
-  if (!depth && batch != 0) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null depth%s");
+  if (!t) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null tables");
+  if (!depth && batch != 0) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null depth");
   if (dtype != RF_DEPTH_F32_M && dtype != RF_DEPTH_U16_MM && dtype != RF_DEPTH_F64_M)
-    return fail(RF_ERR_SHAPE, "unknown depth dtype%s %lld", "", dtype);
+    return fail(RF_ERR_SHAPE, "unknown depth dtype %d", dtype);
   if (H != t->intr.height || W != t->intr.width)
-    return fail(RF_ERR_SHAPE, "depth %s%lldx%lld does not match the camera tables", "", W, H);
-  if (batch < 0) return fail(RF_ERR_ARGUMENT, "batch%s %lld is negative", "", batch);
-  if (row_pitch < W) return fail(RF_ERR_ARGUMENT, "row_pitch%s %lld < width", "", row_pitch);
+    return fail(RF_ERR_SHAPE, "depth %dx%d does not match the camera tables", W, H);
+  if (batch < 0) return fail(RF_ERR_ARGUMENT, "batch %lld is negative", (long long)batch);
+  if (row_pitch < W) return fail(RF_ERR_ARGUMENT, "row_pitch %lld < width", (long long)row_pitch);
   if (window < 1 || (window & 1) == 0 || window / 2 > MAX_RADIUS)
-    return fail(RF_ERR_ARGUMENT, "window%s must be odd and in [1, %lld], got %lld", "",
-                2 * MAX_RADIUS + 1, window);
+    return fail(RF_ERR_ARGUMENT, "window must be odd and in [1, %d], got %d", 2 * MAX_RADIUS + 1, window);
   if ((fmask & ~RF_ALL_FORMULATIONS) != 0 || fmask == 0)
-    return fail(RF_ERR_ARGUMENT, "formulation_mask%s %lld invalid", "", fmask);
+    return fail(RF_ERR_ARGUMENT, "formulation_mask %d invalid", fmask);
   if (batch == 0) return RF_OK;
-  if (!outs) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null output array%s");
+  if (!outs) return fail(RF_ERR_ARGUMENT, "rf_fit_pixels: null output array");
   for (int f = 0; f < RF_NUM_FORMULATIONS; ++f) {
     if (!(fmask & (1 << f))) continue;
     const rf_pixel_out& o = outs[f];
     if (!o.normal || !o.offset || !o.residual || !o.curvature || !o.status)
-      return fail(RF_ERR_ARGUMENT, "formulation %s%lld requested without output buffers", "", f);
+      return fail(RF_ERR_ARGUMENT, "formulation %d requested without output buffers", f);
   }
   const int r = window / 2;
   const int64_t tiles = (int64_t)((W + TW - 1) / TW) * ((H + TH - 1) / TH) * batch;
@@ -1079,7 +1081,7 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   const bool fork = both && tiles <= (int64_t)8 * nsm && getenv("RF_NO_FORK") == nullptr;
   if (fork) {
     fork_lock.lock();
-    if (!fork_stream(dev, fs)) return fail(RF_ERR_CUDA, "side stream creation failed%s");
+    if (!fork_stream(dev, fs)) return fail(RF_ERR_CUDA, "side stream creation failed");
     cudaEventRecord(fs->fork, s);
     cudaStreamWaitEvent(fs->aux, fs->fork, 0);
   }
