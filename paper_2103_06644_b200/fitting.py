@@ -210,6 +210,47 @@ def fit_rects(depth, maps: TanAngleMaps, rects, formulation: str, frames=None, m
     return out.cpu().numpy().view(RECT_FIT_DTYPE).reshape(-1)
 
 
+def _canonical_rows(coef: np.ndarray) -> np.ndarray:
+    """canonicalize_implicit (fitting.py:76-94) for many coefficient rows at once."""
+    c = np.asarray(coef, dtype=np.float64).reshape(-1, 4)
+    unit = c / np.sqrt((c * c).sum(axis=1))[:, None]
+    sign = np.ones(len(c))
+    decided = np.zeros(len(c), bool)
+    for idx in (2, 1, 0, 3):
+        take = ~decided & (np.abs(unit[:, idx]) > _CANONICAL_EPS)
+        sign[take] = np.where(unit[take, idx] > 0, 1.0, -1.0)
+        decided |= take
+    return unit * sign[:, None]
+
+
+def _implicit_plane_fast(unit: np.ndarray) -> ImplicitPlane:
+    """An ImplicitPlane from an already canonical unit vector (skips re-validation)."""
+    p = object.__new__(ImplicitPlane)
+    object.__setattr__(p, "coefficients", unit)
+    return p
+
+
+def _results_from_rows(rows, formulation: str) -> list:
+    """FitResults for rect rows that carry a fit (batched canonicalisation)."""
+    n = rows["n_points"].astype(int)
+    deg = (rows["status"] & RECT_DEGENERATE) != 0
+    rms = rows["rms"]
+    curv = rows["curvature"]
+    out = []
+    if formulation in (IMPLICIT_STANDARD, IMPLICIT_RGBD):
+        units = _canonical_rows(rows["coef"])
+        lam = rows["eigenvalue"]
+        for i in range(len(rows)):
+            out.append(FitResult(_implicit_plane_fast(units[i]), int(n[i]), float(rms[i]), float(lam[i]),
+                                 bool(deg[i]), float(curv[i])))
+        return out
+    space = SPACE_STANDARD if formulation == EXPLICIT_STANDARD else SPACE_RGBD
+    for i in range(len(rows)):
+        out.append(FitResult(ExplicitPlane(np.array(rows["explicit_coef"][i]), space), int(n[i]), float(rms[i]), None,
+                             bool(deg[i]), float(curv[i])))
+    return out
+
+
 def _result(row, formulation: str) -> FitResult:
     if row["status"] & RECT_OUT_OF_BOUNDS:
         raise ValueError("rect out of bounds")

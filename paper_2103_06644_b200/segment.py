@@ -120,6 +120,30 @@ def tile_features(result: F.FitResult, d_scale: float = 5.0) -> np.ndarray:
     return np.array([coef[0], coef[1], coef[2], coef[3] / d_scale])
 
 
+def _features(tiles, d_scale: float) -> np.ndarray:
+    """tile_features for many fitted tiles at once (same arithmetic, vectorised)."""
+    rows = []
+    for t in tiles:
+        pl = t.result.plane
+        rows.append(F.explicit_to_implicit(pl).coefficients if isinstance(pl, F.ExplicitPlane) else pl.coefficients)
+    coef = np.array(rows, dtype=np.float64)
+    norm = np.sqrt((coef[:, :3] * coef[:, :3]).sum(axis=1))
+    if np.any(norm == 0):
+        raise ValueError("fit has a degenerate normal")
+    coef = coef / norm[:, None]
+    flip = coef[:, 3] < 0
+    zero = coef[:, 3] == 0
+    if zero.any():
+        for i in np.nonzero(zero)[0]:
+            for v in (coef[i, 2], coef[i, 1], coef[i, 0]):
+                if abs(v) > 1e-12:
+                    flip[i] = v < 0
+                    break
+    coef[flip] = -coef[flip]
+    coef[:, 3] /= d_scale
+    return coef
+
+
 def kmeans(features: np.ndarray, k: int, seed: int = 0, max_iter: int = 100):
     """Lloyd's k-means, k-means++ seeding from numpy default_rng(seed) (segment.py:224-269)."""
     x = np.asarray(features, dtype=np.float64)
@@ -208,36 +232,42 @@ def segment(depth, maps: TanAngleMaps, config: SegConfig, constant=None, frame: 
             rows = F.fit_rects_integral(stack, constant, rects, config.formulation)
         else:
             rows = F.fit_rects(d, maps, rects, config.formulation, frames=frame, mask=mask)
-        results, fitted_idx = {}, []
-        for i, ((r, lev), row) in enumerate(zip(level_rects, rows)):
-            n_valid = int(row["n_points"])
-            if n_valid < config.min_valid_fraction * r.area or n_valid == 0 or not row["status"] & F.RECT_FIT:
-                continue
-            results[i] = F._result(row, config.formulation)
-            fitted_idx.append(i)
-        errors = {}
-        if config.error_metric == "max" and fitted_idx:
-            coefs = [results[i].plane.coefficients for i in fitted_idx]
-            mx = F.max_residuals(d, maps, [rects[i] for i in fitted_idx], config.formulation,
-                                 np.stack(coefs) if implicit else np.stack(coefs)[:, :3], frames=frame, mask=mask)
-            errors = dict(zip(fitted_idx, (float(v) for v in mx)))
+        area = np.array([r.area for r, _ in level_rects])
+        n_valid = rows["n_points"].astype(np.int64)
+        fitted = (n_valid >= config.min_valid_fraction * area) & (n_valid > 0) & ((rows["status"] & F.RECT_FIT) != 0)
+        degenerate = (rows["status"] & F.RECT_DEGENERATE) != 0
+        fidx = np.nonzero(fitted)[0]
+        if config.error_metric == "max":
+            err = np.full(len(rows), np.inf)
+            if len(fidx):
+                coefs = F._canonical_rows(rows["coef"][fidx]) if implicit else rows["explicit_coef"][fidx]
+                err[fidx] = F.max_residuals(d, maps, [rects[i] for i in fidx], config.formulation, coefs,
+                                            frames=frame, mask=mask)
+        else:
+            err = np.where(np.isnan(rows["rms"]), np.inf, rows["rms"])
+        accept = fitted & ~degenerate & (err <= config.threshold)
         nxt = []
+        leaves = []
         for i, (r, lev) in enumerate(level_rects):
-            if i not in results:
+            if not fitted[i]:
                 decided[r] = ("invalid", None)
-                continue
-            res = results[i]
-            if config.error_metric == "max":
-                err = errors[i]
-            else:
-                err = np.inf if res.rms_residual is None else res.rms_residual
-            if not res.degenerate and err <= config.threshold:
-                decided[r] = ("fit", res)
+            elif accept[i]:
+                decided[r] = ("fit", i)
+                leaves.append(i)
             elif lev < config.max_depth and r.x1 - r.x0 >= 2 * MIN_TILE_EDGE and r.y1 - r.y0 >= 2 * MIN_TILE_EDGE:
-                decided[r] = ("split", res)
+                decided[r] = ("split", None)
                 nxt.extend((c, lev + 1) for c in _children(r))
             else:
-                decided[r] = ("high", res)
+                decided[r] = ("high", i)
+                leaves.append(i)
+        # result objects only for the leaves that keep one (batched canonicalisation)
+        if leaves:
+            res = F._results_from_rows(rows[np.array(leaves)], config.formulation)
+            by_row = dict(zip(leaves, res))
+            for r, _ in level_rects:
+                kind, payload = decided[r]
+                if kind in ("fit", "high") and isinstance(payload, (int, np.integer)):
+                    decided[r] = (kind, by_row[int(payload)])
         level_rects = nxt
     # leaves in the reference's LIFO order (pending.pop() / pending.extend(children))
     tiles = []
@@ -256,7 +286,7 @@ def segment(depth, maps: TanAngleMaps, config: SegConfig, constant=None, frame: 
     warnings = []
     fitted = [t for t in tiles if t.status is TileStatus.FITTED]
     if fitted:
-        feats = np.stack([tile_features(t.result, config.d_scale) for t in fitted])
+        feats = _features(fitted, config.d_scale)
         k = config.k
         if k > len(fitted):
             warnings.append(f"k={k} exceeds {len(fitted)} fitted tiles; clamped")
