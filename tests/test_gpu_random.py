@@ -93,3 +93,44 @@ def test_random_rects(case):
         ok = ((ref["status"] & 2) != 0) & ((ref["status"] & 4) == 0) & ((got["status"] & 4) == 0)
         if ok.any():
             assert normal_angles(got["coef"][ok, :3], ref["coef"][ok, :3]).max() <= 1e-4, (case, form)
+
+
+def _adversarial(kind, W=96, H=48):
+    """Hand-made hard windows: stripes of validity (collinear samples), checkerboards, depth
+    steps through window centres, noiseless oblique planes (lambda ~ 0), near-grazing planes."""
+    fx = 80.0
+    cx, cy = (W - 1) / 2.0, (H - 1) / 2.0
+    tx = (np.arange(W) - cx) / fx
+    ty = (np.arange(H) - cy) / fx
+    TX, TY = np.meshgrid(tx, ty)
+    if kind == "stripes":
+        z = 2.0 + 0.3 * TX - 0.2 * TY
+        z[np.arange(H) % 3 != 0, :] = 0.0           # only every third row valid
+    elif kind == "checker":
+        z = 1.5 - 0.4 * TY + 1e-3 * np.sin(7 * TX)
+        z[(np.arange(H)[:, None] + np.arange(W)[None, :]) % 2 == 1] = 0.0
+    elif kind == "steps":
+        z = np.where(TX < 0, 1.0, 3.0) + np.where(TY < 0, 0.0, 0.5)
+    elif kind == "oblique":
+        n = np.array([0.6, -0.3, -0.74])            # noiseless plane n.X + 2 = 0
+        z = -2.0 / (n[0] * TX + n[1] * TY + n[2])
+    else:  # grazing: plane nearly parallel to the viewing rays
+        n = np.array([0.995, 0.0, -0.0999])
+        z = -0.2 / (n[0] * TX + n[1] * TY + n[2])
+        z = np.where((z > 0) & (z < 50), z, 0.0)
+    return z.astype(np.float32), Cam(fx, fx, cx, cy, W, H)
+
+
+@pytest.mark.parametrize("kind", ["stripes", "checker", "steps", "oblique", "grazing"])
+@pytest.mark.parametrize("window", [3, 5, 9])
+def test_adversarial_windows(kind, window):
+    z, cam = _adversarial(kind)
+    H, W = z.shape
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H))
+    out = rf.fit_pixels(torch.from_numpy(z).cuda(), maps, window, rf.FORMULATIONS)
+    torch.cuda.synchronize()
+    for form in rf.FORMULATIONS:
+        ref = oracle_frame(torch.from_numpy(z), cam, window, form)
+        m = compare(gpu_flat(out[form]), ref, explicit_fit=form.startswith("explicit"))
+        assert m["ok"], (kind, window, form, {k: m[k] for k in ("status_mismatch", "max_normal_rad",
+                                                                 "max_residual_rel", "max_curvature_rel")})
