@@ -9,7 +9,10 @@ oracle (restated reference), with the tolerances of BASELINE.json's north_star:
   where a relative error is ill-posed (noiseless windows, where lambda is
   rounding noise of size ~eps*||S||_F): residual allowance
   sqrt(1e-11 * ||S||_F / n) (the rms of a rounding-level eigenvalue),
-  curvature allowance 1e-8.
+  curvature allowance 1e-8 plus 1e-15 * curv_cond, where curv_cond (from the oracle) is the
+  uncentred monomial diagonal over the centred trace -- the factor by which centring the
+  window sums amplifies rounding in lambda_min / trace (e.g. millimetre depths among metres
+  in the disparity form put 1/Z^2 ~ 1e6 next to tan-angle spreads ~ 1e-3).
 """
 
 from __future__ import annotations
@@ -19,6 +22,7 @@ import numpy as np
 NORMAL_TOL_RAD = 1e-4
 REL_TOL = 1e-4
 CURV_FLOOR = 1e-8
+CURV_COND_REL = 1e-15
 LAM_FLOOR_REL = 1e-11
 
 
@@ -53,7 +57,11 @@ def compare(gpu: dict, ref: dict, explicit_fit: bool = False) -> dict:
     res_err = np.abs(gres - rres) / (REL_TOL * np.abs(rres) + res_floor) * REL_TOL
     gc = np.asarray(gpu["curvature"], np.float64).ravel()[sel]
     rc = np.asarray(ref["curvature"], np.float64).ravel()[sel]
-    cur_err = np.abs(gc - rc) / (REL_TOL * np.abs(rc) + CURV_FLOOR) * REL_TOL
+    cur_floor = CURV_FLOOR
+    if "curv_cond" in ref:
+        cond = np.asarray(ref["curv_cond"], np.float64).ravel()[sel]
+        cur_floor = CURV_FLOOR + CURV_COND_REL * np.where(np.isfinite(cond), cond, 0.0)
+    cur_err = np.abs(gc - rc) / (REL_TOL * np.abs(rc) + cur_floor) * REL_TOL
     # offsets: same sign convention, relative to max(|offset|, 1e-6)
     go = np.asarray(gpu["offset"], np.float64).ravel()[sel]
     ro = np.asarray(ref["offset"], np.float64).ravel()[sel]

@@ -59,7 +59,7 @@ def lib() -> ctypes.CDLL:
         i64p = ctypes.POINTER(ctypes.c_int64)
         L.rfo_fit_pixels.argtypes = [
             dp, u8p, dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-            i64p, ctypes.c_int64, fp, fp, fp, fp, u8p, dp, dp, dp, ctypes.c_int,
+            i64p, ctypes.c_int64, fp, fp, fp, fp, u8p, dp, dp, dp, dp, ctypes.c_int,
         ]
         L.rfo_fit_pixels.restype = ctypes.c_int
         L.rfo_fit_scatter.argtypes = [
@@ -118,7 +118,8 @@ def fit_pixels(values, valid, tan_x, tan_y, window, formulation, backend=NAIVE, 
 
     Returns a dict with ``normal`` (P,3) f32, ``offset``/``residual``/``curvature`` (P,) f32
     and ``status`` (P,) u8, where P = H*W (or len(pixels)), ``scale`` = ||S||_F / n (P,)
-    f64 (the rounding floor of lambda); optionally the canonical
+    f64 (the rounding floor of lambda), ``curv_cond`` = sum of the uncentred monomial
+    diagonal / trace of the centred scatter (the rounding amplification of the curvature); optionally the canonical
     fp64 coefficient vector ``coef`` (P,4) and smallest eigenvalue ``lam`` (for the explicit
     formulations ``coef`` is explicit_to_implicit of the fit and ``lam`` the residual sum
     of squares sum(b^2) - alpha.rhs).
@@ -146,6 +147,7 @@ def fit_pixels(values, valid, tan_x, tan_y, window, formulation, backend=NAIVE, 
     coef = np.empty((P, 4), np.float64) if want_coef else None
     lam = np.empty(P, np.float64) if want_coef else None
     scale = np.empty(P, np.float64)
+    curv_cond = np.empty(P, np.float64)
     rc = lib().rfo_fit_pixels(
         _ptr(values, ctypes.c_double), _ptr(valid, ctypes.c_uint8), _ptr(tan_x, ctypes.c_double),
         _ptr(tan_y, ctypes.c_double), H, W, int(window), int(formulation), int(backend),
@@ -155,11 +157,12 @@ def fit_pixels(values, valid, tan_x, tan_y, window, formulation, backend=NAIVE, 
         _ptr(out["status"], ctypes.c_uint8),
         None if coef is None else _ptr(coef, ctypes.c_double),
         None if lam is None else _ptr(lam, ctypes.c_double), _ptr(scale, ctypes.c_double),
-        int(nthreads),
+        _ptr(curv_cond, ctypes.c_double), int(nthreads),
     )
     if rc != 0:
         raise ValueError(f"oracle rfo_fit_pixels failed with code {rc}")
     out["scale"] = scale
+    out["curv_cond"] = curv_cond
     if want_coef:
         out["coef"] = coef
         out["lam"] = lam

@@ -147,9 +147,12 @@ typedef struct {
   double rms;
   double curvature;
   double scale;     /* ||S||_F / n, sets the rounding floor of lambda */
+  double curv_cond; /* sum of the uncentred diagonal / trace(C3): rounding amplification of kappa */
   int degenerate;
   int failed;
 } fit_out;
+
+static double curvature_of(const double* S, int space, double* cond);
 
 /* _fit_implicit fitting.py:546-559 plus the A17 curvature extension */
 static void fit_scatter(const double* S, int n, int formulation, fit_out* o) {
@@ -170,25 +173,12 @@ static void fit_scatter(const double* S, int n, int formulation, fit_out* o) {
   o->lam = lam;
   o->rms = sqrt((lam > 0.0 ? lam : 0.0) / (double)n);
   /* curvature: centred 3x3 block of the non-constant monomials */
-  int I[3], k;
-  if (formulation == RFO_STANDARD) { I[0] = 0; I[1] = 1; I[2] = 2; k = 3; }
-  else { I[0] = 0; I[1] = 1; I[2] = 3; k = 2; }
-  double nn = S[k * 4 + k];
-  double C3[9];
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j)
-      C3[i * 3 + j] = S[I[i] * 4 + I[j]] - S[I[i] * 4 + k] * S[I[j] * 4 + k] / nn;
-  double cv[3], cvec[9];
-  jacobi_eigh(3, C3, cv, cvec);
-  double mn = cv[0];
-  if (cv[1] < mn) mn = cv[1];
-  if (cv[2] < mn) mn = cv[2];
-  double tr = C3[0] + C3[4] + C3[8];
-  o->curvature = tr > 0.0 ? mn / tr : 0.0;
+  o->curvature = curvature_of(S, formulation, &o->curv_cond);
 }
 
-/* curvature (A17) from an implicit 4x4 scatter of the formulation's space */
-static double curvature_of(const double* S, int space) {
+/* curvature (A17) from an implicit 4x4 scatter of the formulation's space; *cond receives
+ * the rounding amplification sum_i S[I_i][I_i] / trace(C3) of the centring (test metric) */
+static double curvature_of(const double* S, int space, double* cond) {
   int I[3], k;
   if (space == RFO_STANDARD) { I[0] = 0; I[1] = 1; I[2] = 2; k = 3; }
   else { I[0] = 0; I[1] = 1; I[2] = 3; k = 2; }
@@ -203,6 +193,7 @@ static double curvature_of(const double* S, int space) {
   if (cv[1] < mn) mn = cv[1];
   if (cv[2] < mn) mn = cv[2];
   double tr = C3[0] + C3[4] + C3[8];
+  if (cond) *cond = tr > 0.0 ? (S[I[0] * 4 + I[0]] + S[I[1] * 4 + I[1]] + S[I[2] * 4 + I[2]]) / tr : INFINITY;
   return tr > 0.0 ? mn / tr : 0.0;
 }
 
@@ -274,7 +265,7 @@ static void fit_explicit(const double* S, int n, int space, fit_out* o) {
   double fro2 = 0.0;
   for (int i = 0; i < 16; ++i) fro2 += S[i] * S[i];
   o->scale = sqrt(fro2) / (double)n;
-  o->curvature = curvature_of(S, space);
+  o->curvature = curvature_of(S, space, &o->curv_cond);
 }
 
 /* ---- naive scatter: gather_window_samples + accumulate_scatter_naive ---- */
@@ -447,7 +438,7 @@ typedef struct {
   int64_t npix;
   float *normal, *offset, *residual, *curvature;
   uint8_t* status;
-  double *coef, *lam, *scale;
+  double *coef, *lam, *scale, *curv_cond;
   atomic_llong next;
 } job_t;
 
@@ -487,6 +478,7 @@ static void fit_one(job_t* J, int64_t k) {
       if (J->coef) memcpy(J->coef + 4 * k, o.coef, sizeof(o.coef));
       if (J->lam) J->lam[k] = o.lam;
       if (J->scale) J->scale[k] = o.scale;
+      if (J->curv_cond) J->curv_cond[k] = o.curv_cond;
     }
   }
   if (!(s & 2)) {
@@ -495,6 +487,7 @@ static void fit_one(job_t* J, int64_t k) {
     if (J->coef) J->coef[4 * k] = J->coef[4 * k + 1] = J->coef[4 * k + 2] = J->coef[4 * k + 3] = NAN;
     if (J->lam) J->lam[k] = NAN;
     if (J->scale) J->scale[k] = NAN;
+    if (J->curv_cond) J->curv_cond[k] = NAN;
   }
   J->status[k] = s;
 }
@@ -520,7 +513,7 @@ int rfo_fit_pixels(const double* depth, const uint8_t* valid, const double* tan_
                    const double* tan_y, int H, int W, int window, int formulation, int backend,
                    const int64_t* pix, int64_t npix, float* normal, float* offset, float* residual,
                    float* curvature, uint8_t* status, double* coef, double* lam, double* scale,
-                   int nthreads) {
+                   double* curv_cond, int nthreads) {
   if (window < 1 || (window & 1) == 0 || H <= 0 || W <= 0) return -1;
   if (formulation < RFO_STANDARD || formulation > RFO_EXPLICIT_RGBD) return -1;
   sat_stack st;
@@ -529,7 +522,7 @@ int rfo_fit_pixels(const double* depth, const uint8_t* valid, const double* tan_
     if (build_stack(depth, valid, tan_x, tan_y, H, W, RFO_SPACE(formulation), &st) != 0) return -1;
   }
   job_t J = {depth, tan_x, tan_y, valid, H, W, window / 2, formulation, backend, &st, pix, npix,
-             normal, offset, residual, curvature, status, coef, lam, scale, 0};
+             normal, offset, residual, curvature, status, coef, lam, scale, curv_cond, 0};
   atomic_init(&J.next, 0);
   if (nthreads <= 0) nthreads = rfo_max_threads();
   if (nthreads > 256) nthreads = 256;

@@ -134,3 +134,28 @@ def test_adversarial_windows(kind, window):
         m = compare(gpu_flat(out[form]), ref, explicit_fit=form.startswith("explicit"))
         assert m["ok"], (kind, window, form, {k: m[k] for k in ("status_mismatch", "max_normal_rad",
                                                                  "max_residual_rel", "max_curvature_rel")})
+
+
+@pytest.mark.parametrize("window,dtype,use_mask,direct", [(3, "f32", False, False), (5, "u16", True, False),
+                                                           (9, "f64", False, False), (15, "f32", True, False),
+                                                           (31, "f32", False, False), (5, "f32", True, True),
+                                                           (11, "u16", False, True)])
+def test_distortion_lattices(window, dtype, use_mask, direct, monkeypatch):
+    """Cameras with per-pixel distortion offsets: the tiled lattice kernel (and the direct
+    per-pixel fallback) against the oracle with the same lattices."""
+    if direct:
+        monkeypatch.setenv("RF_LATTICE_DIRECT", "1")
+    rng = np.random.default_rng(window * 7 + len(dtype))
+    W, H = 100, 70
+    z, cam = _frame(rng, W, H, dtype)
+    dx, dy = rng.uniform(-0.45, 0.45, (H, W)), rng.uniform(-0.45, 0.45, (H, W))
+    cam = Cam(cam.fx, cam.fy, cam.cx, cam.cy, W, H, dx, dy)
+    maps = rf.compute_tan_maps(cam.intrinsics())
+    mask = torch.from_numpy(rng.random((H, W)) > 0.1).cuda() if use_mask else None
+    out = rf.fit_pixels(torch.from_numpy(z).cuda(), maps, window, rf.FORMULATIONS, mask=mask)
+    torch.cuda.synchronize()
+    for form in rf.FORMULATIONS:
+        ref = oracle_frame(torch.from_numpy(z), cam, window, form, mask=None if mask is None else mask.cpu())
+        m = compare(gpu_flat(out[form]), ref, explicit_fit=form.startswith("explicit"))
+        assert m["ok"], (window, dtype, form, {k: m[k] for k in ("status_mismatch", "max_normal_rad",
+                                                                  "max_residual_rel", "max_curvature_rel")})
