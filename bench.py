@@ -349,7 +349,9 @@ def run_ours(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         frames_host = depth[:4].cpu()
         r, cores, el, sample = cpu_reference_rate(frames_host, cfg, args.cpu_seconds)
-        cpu_baseline = {"value": r / 1e6, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        r1, _, _, sample1 = cpu_reference_rate(frames_host, cfg, 0.5, threads=1)
+        cpu_baseline = {"value": r / 1e6, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                        "value_1core": r1 / 1e6, "sample_1core": sample1}
 
     if rank == 0:
         line = {
