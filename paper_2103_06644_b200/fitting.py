@@ -580,6 +580,102 @@ def max_residuals(depth, maps: TanAngleMaps, rects, formulation: str, coefs, fra
     return out.cpu().numpy()
 
 
+def gather_window_samples(depth, maps: TanAngleMaps, rect, formulation: str) -> np.ndarray:
+    """Valid samples of a window for the naive path (fitting.py:384-402): (X, Y, Z) rows for
+    the standard formulations, (tan_x, tan_y, Z) for rgbd.  Host helper on a DepthImage."""
+    from . import integral as I
+
+    _check_formulation(formulation)
+    rect = Rect(*rect)
+    I._check_rect(rect, depth.width, depth.height)
+    sl = (slice(rect.y0, rect.y1), slice(rect.x0, rect.x1))
+    valid = depth.valid[sl]
+    z = depth.values[sl][valid]
+    tx, ty = maps.tan_x[sl][valid], maps.tan_y[sl][valid]
+    if formulation in (IMPLICIT_STANDARD, EXPLICIT_STANDARD):
+        return np.column_stack((z * tx, z * ty, z))
+    return np.column_stack((tx, ty, z))
+
+
+def accumulate_scatter_naive(samples, formulation: str):
+    """Scatter system straight from per-sample monomials (fitting.py:339-381): the Gram
+    matrix of [u, v, z, 1] (standard) / [tx, ty, 1, 1/Z] (rgbd), symmetrised; explicit forms
+    get the 3x3 normal equations, right-hand side and sum of squared targets."""
+    _check_formulation(formulation)
+    smp = np.asarray(samples, dtype=np.float64)
+    if smp.ndim != 2 or smp.shape[1] != 3:
+        raise ValueError(f"samples must be (N, 3), got shape {smp.shape}")
+    n = smp.shape[0]
+    if n < MIN_SAMPLES[formulation]:
+        raise InsufficientSamplesError(f"{formulation} needs at least {MIN_SAMPLES[formulation]} samples, got {n}")
+    u, v, z = smp[:, 0], smp[:, 1], smp[:, 2]
+    rgbd = formulation in (IMPLICIT_RGBD, EXPLICIT_RGBD)
+    if rgbd and np.any(z <= 0):
+        raise ValueError("rgbd formulations require strictly positive depths")
+    one = np.ones(n)
+
+    def gram(m):
+        g = m.T @ m
+        return (g + g.T) * 0.5
+
+    if formulation == IMPLICIT_STANDARD:
+        return Scatter4(matrix=gram(np.column_stack((u, v, z, one))), n=n)
+    if formulation == IMPLICIT_RGBD:
+        return Scatter4(matrix=gram(np.column_stack((u, v, one, 1.0 / z))), n=n)
+    m = np.column_stack((u, v, one))
+    target = 1.0 / z if rgbd else z
+    return Scatter3(matrix=gram(m), rhs=m.T @ target, n=n, target_sq=float(target @ target))
+
+
+def smallest_eigenvector(matrix):
+    """Unit eigenvector of the smallest eigenvalue of a symmetric matrix, and that eigenvalue
+    (fitting.py:256-261).  The sign of the vector is arbitrary, as in the reference."""
+    a = np.asarray(matrix, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError(f"expected a square matrix, got shape {a.shape}")
+    if not np.all(np.isfinite(a)):
+        raise ValueError("matrix holds non-finite entries")
+    if float(np.abs(a - a.T).max()) > 1e-12 * max(float(np.linalg.norm(a)), 1.0):
+        raise ValueError("matrix is not symmetric")
+    vals, vecs = np.linalg.eigh(a)
+    v = vecs[:, 0]
+    return v / float(np.linalg.norm(v)), float(vals[0])
+
+
+def solve_spd3(matrix, rhs) -> np.ndarray:
+    """Solve a 3x3 symmetric positive-definite system by Cholesky (fitting.py:264-310); a pivot
+    below 1e-12 of the trace raises DegenerateFitError, as in the reference."""
+    s = np.asarray(matrix, dtype=np.float64)
+    if s.shape != (3, 3):
+        raise ValueError(f"expected a 3x3 matrix, got shape {s.shape}")
+    trace = float(s[0, 0] + s[1, 1] + s[2, 2])
+    floor = _PIVOT_REL * trace
+    if not np.isfinite(trace) or trace <= 0.0:
+        raise DegenerateFitError("scatter matrix has non-positive trace")
+    p0 = float(s[0, 0])
+    if p0 <= floor:
+        raise DegenerateFitError("rank-deficient scatter matrix (pivot 1)")
+    l00 = math.sqrt(p0)
+    l10, l20 = float(s[1, 0]) / l00, float(s[2, 0]) / l00
+    p1 = float(s[1, 1]) - l10 * l10
+    if p1 <= floor:
+        raise DegenerateFitError("rank-deficient scatter matrix (pivot 2)")
+    l11 = math.sqrt(p1)
+    l21 = (float(s[2, 1]) - l20 * l10) / l11
+    p2 = float(s[2, 2]) - l20 * l20 - l21 * l21
+    if p2 <= floor:
+        raise DegenerateFitError("rank-deficient scatter matrix (pivot 3)")
+    l22 = math.sqrt(p2)
+    b0, b1, b2 = (float(v) for v in np.asarray(rhs, dtype=np.float64))
+    y0 = b0 / l00
+    y1 = (b1 - l10 * y0) / l11
+    y2 = (b2 - l20 * y0 - l21 * y1) / l22
+    x2 = y2 / l22
+    x1 = (y1 - l21 * x2) / l11
+    x0 = (y0 - l10 * x1 - l20 * x2) / l00
+    return np.array([x0, x1, x2])
+
+
 class ExplicitRgbdFitter:
     """Explicit inverse-depth fits over a camera-constant stack (fitting.py:632-726).
 

@@ -83,6 +83,26 @@ class SyntheticScene:
         object.__setattr__(self, "planes", tuple(self.planes))
 
 
+def ray_for_pixel(maps: TanAngleMaps, pixel) -> np.ndarray:
+    """Unnormalised viewing ray (tan_x, tan_y, 1) of one pixel (synth.py:117-122)."""
+    x, y = pixel
+    if not (0 <= x < maps.width and 0 <= y < maps.height):
+        raise ValueError(f"pixel ({x}, {y}) outside {maps.width}x{maps.height} image")
+    return np.array([maps.tan_x[y, x], maps.tan_y[y, x], 1.0])
+
+
+def intersect_plane(ray: np.ndarray, plane: GroundTruthPlane):
+    """Depth of a ray-plane intersection, None if behind or parallel (synth.py:125-134)."""
+    a, b, c, d = plane.coefficients
+    denom = a * ray[0] + b * ray[1] + c * ray[2]
+    if denom == 0.0:
+        return None
+    z = -d / denom
+    if z <= 0 or not np.isfinite(z):
+        return None
+    return float(z)
+
+
 def _plane_rects(scene: SyntheticScene, width: int, height: int) -> np.ndarray:
     """Mask rects as the reference's numpy slices select them (masked[y0:y1, x0:x1])."""
     out = np.empty((len(scene.planes), 4), np.int32)

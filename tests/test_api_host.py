@@ -135,3 +135,56 @@ def test_scene_parsing_and_mask_rect_slices():
         synth.GroundTruthPlane(np.array([0, 0, 1.0, -1]), mask_rect=(5, -3, 99, 20)))), 40, 30)
     # numpy slice semantics of masked[y0:y1, x0:x1] (synth.py:145-148)
     assert rects.tolist() == [[0, 0, 40, 30], [30, 22, 30, 30], [5, 27, 40, 27]]
+
+
+def _host_maps(intr):
+    """TanAngleMaps without device tables (its lattices are computed on the host)."""
+    import ctypes
+    from paper_2103_06644_b200.pixels import TanAngleMaps
+    return TanAngleMaps(intrinsics=intr, device=0, _handle=ctypes.c_void_p())
+
+
+def test_camera_helpers(tmp_path):
+    intr = rf.CameraIntrinsics(fx=500.0, fy=520.0, cx=319.5, cy=239.5, width=640, height=480)
+    maps = _host_maps(intr)
+    p = rf.back_project((100, 200), 2.0, maps)
+    assert p == rf.Point3(2.0 * (100 - 319.5) / 500.0, 2.0 * (200 - 239.5) / 520.0, 2.0)
+    x, y = rf.project_point(p, intr)
+    assert abs(x - 100) < 1e-9 and abs(y - 200) < 1e-9
+    img = rf.back_project_image(np.full((480, 640), 3.0), maps)
+    assert img.shape == (480, 640, 3) and img[200, 100, 2] == 3.0
+    sx, sy, sz = rf.noise_sigma(2.0, (100, 200), maps, rf.NoiseModel())
+    assert sz == pytest.approx(1.425e-3 * 4.0) and sx == pytest.approx(sz * (100 - 319.5) / 500.0)
+    (tmp_path / "cam.txt").write_text("# test camera\nfx=500\nfy=520\ncx=1.5\ncy=1.0\nwidth=4\nheight=3\n"
+                                      "distortion=d.raw\n")
+    np.concatenate([np.full(12, 0.25), np.full(12, -0.5)]).astype("<f8").tofile(tmp_path / "d.raw")
+    c = rf.load_intrinsics(tmp_path / "cam.txt")
+    assert c.width == 4 and c.delta_x[2, 3] == 0.25 and c.delta_y[0, 0] == -0.5
+    with pytest.raises(ValueError, match="distortion_pixel"):
+        rf.project_point(rf.Point3(0.1, 0.1, 1.0), c)
+    ray = rf.ray_for_pixel(maps, (319, 239))
+    assert rf.intersect_plane(ray, rf.GroundTruthPlane(np.array([0.0, 0.0, 1.0, -2.0]))) == pytest.approx(2.0)
+    assert rf.intersect_plane(ray, rf.GroundTruthPlane(np.array([0.0, 0.0, 1.0, 2.0]))) is None
+
+
+def test_naive_helpers_and_small_solvers():
+    # the reference's known answers: diag(4,3,2,1) -> e4 with lambda 1 (tests/test_fitting_kernels.py:24-27)
+    v, lam = rf.smallest_eigenvector(np.diag([4.0, 3.0, 2.0, 1.0]))
+    assert lam == pytest.approx(1.0) and abs(abs(v[3]) - 1.0) < 1e-12
+    a = np.array([[4.0, 1.0, 0.5], [1.0, 3.0, 0.2], [0.5, 0.2, 2.0]])
+    b = np.array([1.0, -2.0, 0.5])
+    np.testing.assert_allclose(rf.solve_spd3(a, b), np.linalg.solve(a, b), rtol=1e-12)
+    with pytest.raises(rf.DegenerateFitError):
+        rf.solve_spd3(np.ones((3, 3)), b)
+    intr = rf.CameraIntrinsics(fx=20.0, fy=20.0, cx=3.5, cy=2.5, width=8, height=6)
+    maps = _host_maps(intr)
+    d = rf.DepthImage(values=np.full((6, 8), 2.0))
+    smp = rf.gather_window_samples(d, maps, rf.Rect(1, 1, 5, 4), "implicit-standard")
+    assert smp.shape == (12, 3) and np.all(smp[:, 2] == 2.0)
+    sc = rf.accumulate_scatter_naive(smp, "implicit-standard")
+    assert sc.n == 12 and sc.matrix[3, 3] == 12.0 and sc.matrix[2, 2] == 48.0
+    sx = rf.accumulate_scatter_naive(rf.gather_window_samples(d, maps, rf.Rect(1, 1, 5, 4), "explicit-rgbd"),
+                                     "explicit-rgbd")
+    assert sx.target_sq == pytest.approx(12 * 0.25) and sx.rhs[2] == pytest.approx(6.0)
+    with pytest.raises(rf.InsufficientSamplesError):
+        rf.accumulate_scatter_naive(smp[:3], "implicit-rgbd")
