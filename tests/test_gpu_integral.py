@@ -170,3 +170,21 @@ def test_tan_lattices_match_the_reference_formula():
     # is the running sum of row 0 of the lattice
     const = rf.build_constant_channels(maps)
     np.testing.assert_array_equal(const.channels["tx"].table.cpu().numpy()[1, 1:], np.cumsum(tx[0]))
+
+
+def test_reference_timing_harness():
+    """run_bench's rows, CSV schema and ratios (bench.py:86-341) on the device paths."""
+    cfg = rf.BenchConfig(width=96, height=64, tile=20, plane_counts=(0, 1, 7), repetitions=3, warmup=1)
+    rep = rf.run_bench(cfg)
+    csv = rep.to_csv().splitlines()
+    assert csv[0] == "method,backend,phase,plane_count,rep,seconds"
+    # per rep x formulation x backend: build + total(0) + (fit + total) per non-zero count
+    assert len(csv) - 1 == 3 * 4 * 2 * (2 + 2 * 2)
+    assert rep.median_seconds("implicit-rgbd", "integral", "fit", 7) > 0
+    assert rep.build_ratio("implicit") > 0 and rep.per_fit_ratio("explicit") > 0
+    assert len(rep.workload_digest) == 64 and "build ratio" in rep.summary()
+    for f in rf.FORMULATIONS:
+        assert rf.op_count_audit(f).per_frame_channels == {"implicit-standard": 9, "implicit-rgbd": 4,
+                                                           "explicit-standard": 8, "explicit-rgbd": 3}[f]
+    with pytest.raises(ValueError):
+        rf.BenchConfig(repetitions=2)
