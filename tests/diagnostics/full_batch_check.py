@@ -4,7 +4,7 @@ the two implicit formulations): the batched outputs of a few frames (first, midd
 must equal a separate single-frame call bit for bit, and sampled pixels of the last frame
 must match the oracle.  Prints one JSON line.
 
-usage: python tools/full_batch_check.py [C4|C3|C5] [frames]
+usage: python tests/diagnostics/full_batch_check.py [C4|C3|C5] [frames]
 """
 import json
 import sys
@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import paper_2103_06644_b200 as rf  # noqa: E402
 from paper_2103_06644_b200 import scenes  # noqa: E402
 from oracle.compare import compare  # noqa: E402

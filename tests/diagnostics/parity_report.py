@@ -1,7 +1,7 @@
 """Diagnostic: print parity metrics (and worst pixels) for small BASELINE-shaped scenes."""
 import json, sys
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import numpy as np, torch
 import paper_2103_06644_b200 as rf
 from paper_2103_06644_b200 import scenes

@@ -1,7 +1,7 @@
 """Diagnostic: a 3-frame batch through the TMA-fed kernels, parity per frame against the oracle."""
 import sys
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import torch, paper_2103_06644_b200 as rf
 from paper_2103_06644_b200 import scenes
 from tests.helpers import check_frame

@@ -1,6 +1,6 @@
 #!/bin/bash
 # quick GPU check: parity report + bench summary line
-python tools/parity_report.py C4 C5 C2 C1 2>&1 | grep case | python -c "
+python tests/diagnostics/parity_report.py C4 C5 C2 C1 2>&1 | grep case | python -c "
 import json,sys
 bad=0; n=0
 for l in sys.stdin:
