@@ -1242,6 +1242,7 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     if (!o.normal || !o.offset || !o.residual || !o.curvature || !o.status)
       return fail(RF_ERR_ARGUMENT, "formulation %d requested without output buffers", f);
   }
+  const rf_device_guard guard(t->device);
   const int r = window / 2;
   const int64_t tiles = (int64_t)((W + TW - 1) / TW) * ((H + TH - 1) / TH) * batch;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -471,7 +471,7 @@ rf_status rf_build_channel(const rf_tables* t, const void* depth, int dtype, int
       return rf_set_error(RF_ERR_SHAPE, "rf_build_channel: unknown depth dtype");
     if (row_pitch < t->intr.width) return rf_set_error(RF_ERR_SHAPE, "rf_build_channel: row_pitch < width");
   }
-  if (cudaSetDevice(t->device) != cudaSuccess) return rf_set_error(RF_ERR_CUDA, "cudaSetDevice failed");
+  const rf_device_guard guard(t->device);
   ChanParams P{};
   P.depth = depth;
   P.dtype = dtype;

@@ -22,5 +22,22 @@ inline double rf_tan(const double* table, const double* lattice, int W, int x, i
   return lattice ? lattice[(long long)y * W + x] : table[along_x ? x : y];
 }
 
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+// makes the tables' device current for one entry point (restored on exit), so that a
+// caller whose current device differs still launches where the tables and buffers live
+struct rf_device_guard {
+  int prev = -1;
+  explicit rf_device_guard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != device) cudaSetDevice(device);
+    else prev = -1;
+  }
+  ~rf_device_guard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+#endif
+
 // thread-local error message behind rf_last_error()
 rf_status rf_set_error(rf_status s, const char* msg);

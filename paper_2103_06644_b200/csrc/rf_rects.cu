@@ -354,6 +354,7 @@ rf_status rf_max_residuals(const rf_tables* t, const void* depth, int dtype, int
   if (nrects == 0) return RF_OK;
   if (!depth || !rects || !coefs || !out || nrects > 0x7fffffff)
     return rf_set_error(RF_ERR_ARGUMENT, "rf_max_residuals: null pointer");
+  const rf_device_guard guard(t->device);
   MaxResParams M;
   RectParams& P = M.base;
   P.depth = depth;
@@ -398,6 +399,7 @@ rf_status rf_fit_rects(const rf_tables* t, const void* depth, int dtype, int64_t
   if (nrects == 0) return RF_OK;
   if (!depth || !rects || !out || nrects > 0x7fffffff)
     return rf_set_error(RF_ERR_ARGUMENT, "rf_fit_rects: null depth / rects / out");
+  const rf_device_guard guard(t->device);
   RectParams P;
   P.depth = depth;
   P.mask = mask;

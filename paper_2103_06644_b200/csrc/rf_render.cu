@@ -78,7 +78,7 @@ rf_status rf_render_planes(const rf_tables* t, const double* planes, const int32
   if (nplanes < 1 || nplanes > MAX_PLANES)
     return rf_set_error(RF_ERR_ARGUMENT, "rf_render_planes: need 1..256 planes (uint8 labels, 255 = invalid)");
   if (!(dropout >= 0.0 && dropout < 1.0)) return rf_set_error(RF_ERR_ARGUMENT, "dropout must be in [0, 1)");
-  if (cudaSetDevice(t->device) != cudaSuccess) return rf_set_error(RF_ERR_CUDA, "cudaSetDevice failed");
+  const rf_device_guard guard(t->device);
   RenderParams P{t->tan_x, t->tan_y, t->lat_x, t->lat_y, planes, rects, nplanes, t->intr.height, t->intr.width, eps, uniforms,
                  noise_coefficient, dropout, depth, valid, labels};
   const dim3 grid((unsigned)((P.W + 127) / 128), (unsigned)P.H);

@@ -336,10 +336,11 @@ def fit_scatters(matrices, counts, formulation: str, rhs=None, target_sq=None, d
             dtype=np.float64)
         d_tq = torch.from_numpy(tq.reshape(n)).to(dev)
     out = torch.empty((n, RECT_FIT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
-    st = N.load().rf_fit_scatters(d_m.data_ptr(), d_rhs.data_ptr() if d_rhs is not None else None,
-                                  d_tq.data_ptr() if d_tq is not None else None, d_c.data_ptr(), n,
-                                  _FORM_ID[formulation], out.data_ptr(),
-                                  ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+    with torch.cuda.device(dev):
+        st = N.load().rf_fit_scatters(d_m.data_ptr(), d_rhs.data_ptr() if d_rhs is not None else None,
+                                      d_tq.data_ptr() if d_tq is not None else None, d_c.data_ptr(), n,
+                                      _FORM_ID[formulation], out.data_ptr(),
+                                      ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
     N.check(st, "fit_scatters")
     return out.cpu().numpy().view(RECT_FIT_DTYPE).reshape(-1)
 

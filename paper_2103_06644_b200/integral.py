@@ -109,7 +109,8 @@ def build_integral(channel, mask=None, name: str = "", device=None) -> IntegralI
         mptr = m.data_ptr()
     H, W = c.shape
     table = torch.empty((H + 1, W + 1), dtype=torch.float64, device=dev)
-    N.check(N.load().rf_integral(c.data_ptr(), W, mptr, H, W, table.data_ptr(), _stream(dev)), "build_integral")
+    with torch.cuda.device(dev):
+        N.check(N.load().rf_integral(c.data_ptr(), W, mptr, H, W, table.data_ptr(), _stream(dev)), "build_integral")
     return IntegralImage(name=name, table=table)
 
 
@@ -128,8 +129,9 @@ def box_sums(tables, rects) -> np.ndarray:
     d_rects = torch.from_numpy(rr).to(dev)
     out = torch.empty((len(rr), len(tables)), dtype=torch.float64, device=dev)
     ptrs = (ctypes.c_void_p * len(tables))(*[t.data_ptr() for t in tables])
-    N.check(N.load().rf_box_sums(ptrs, len(tables), H, W, d_rects.data_ptr(), len(rr), out.data_ptr(),
-                                 _stream(dev)), "box_sums")
+    with torch.cuda.device(dev):
+        N.check(N.load().rf_box_sums(ptrs, len(tables), H, W, d_rects.data_ptr(), len(rr), out.data_ptr(),
+                                     _stream(dev)), "box_sums")
     return out.cpu().numpy()
 
 
