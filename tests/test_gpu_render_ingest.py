@@ -90,10 +90,13 @@ def test_batched_ingest(tmp_path):
         torch.testing.assert_close(a[f].status, b[f].status, rtol=0, atol=0)
 
 
-def test_host_pipeline_equals_device_call():
+@pytest.mark.parametrize("dtype", ["f32", "u16", "f64"])
+def test_host_pipeline_equals_device_call(dtype):
     from paper_2103_06644_b200 import scenes
-    cfg = scenes.small_config("C2", 160, 120)
+    cfg = scenes.small_config("C4" if dtype == "u16" else "C2", 160, 120)
     depth = scenes.render_batch(cfg, frames=11, device="cuda")
+    if dtype == "f64":
+        depth = depth.double()
     maps = rf.compute_tan_maps(rf.CameraIntrinsics(cfg.f, cfg.f, cfg.cx, cfg.cy, cfg.width, cfg.height))
     ref = rf.fit_pixels(depth, maps, 5)
     pipe = rf.HostPipeline(maps, 5, chunk_frames=4, slots=2)   # 3 chunks, the last one short
