@@ -3,9 +3,11 @@
 Mirrors the reference's fitting vocabulary (``rangefit``):
 
 * :class:`CameraIntrinsics` -- reference ``camera.py:35-75`` (same fields and
-  validation; ``delta_x``/``delta_y`` lattices must be zero, see below).
+  validation; non-zero ``delta_x``/``delta_y`` lattices take the tiled lattice kernel).
 * :func:`compute_tan_maps` -- reference ``camera.py:124-135``; here it builds
   the per-camera device tables (``rf_tables_create``) once.
+* :class:`HostPipeline` -- host frames in, host outputs out, copies overlapped with the
+  kernels (the reference-facing call with host buffers).
 * :func:`fit_pixels` -- the batched per-pixel entry the reference lacks (all four
   reference formulations, ``FORMULATIONS``, ``fitting.py:45-49``): for
   every pixel it is ``fit_rect(depth, maps, Rect(max(x-r,0), max(y-r,0),
