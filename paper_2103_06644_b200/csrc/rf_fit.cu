@@ -244,6 +244,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   double* vd = prim + (NOPRIM ? 0 : HH_ * HW_);                          // [NVD][TH][VRS]
   int* vi = reinterpret_cast<int*>(vd + NVD * TH * VRS);                 // [NVI][TH][VRS]
   uint64_t* bars = reinterpret_cast<uint64_t*>(vi + NVI * TH * VRS + ((NVI * TH * VRS) & 1));
+  // explicit fits stage their 4 pixels' outputs in shared memory (7 float4 per thread: the
+  // implicit outputs already hold the register budget) and store them as vectors
+  float* xstage = reinterpret_cast<float*>(bars + 2 + ((smem_u32(bars + 2) & 15u) ? 1 : 0));
 
   const int tid = threadIdx.x;
   const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;
@@ -628,26 +631,27 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
             if (VAR == VAR_DF) finish_plane(e.a, e.b, e.c, -1.0, ex, ey, ez, eo);
             else finish_plane(e.a, e.b, -1.0, e.c, ex, ey, ez, eo);
             stx |= RF_PIX_FIT | (e.degenerate ? RF_PIX_DEGENERATE : 0);
-            const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
-            P.exp.normal[3 * p + 0] = ex;
-            P.exp.normal[3 * p + 1] = ey;
-            P.exp.normal[3 * p + 2] = ez;
-            P.exp.offset[p] = eo;
-            P.exp.residual[p] = fsqrt(fmaxf((float)(e.ss * invn), 0.0f));
-            P.exp.curvature[p] = kap;
-            P.exp.status[p] = stx;
+            float* xs_ = xstage + 28 * tid;
+            xs_[3 * j + 0] = ex;
+            xs_[3 * j + 1] = ey;
+            xs_[3 * j + 2] = ez;
+            xs_[12 + j] = eo;
+            xs_[16 + j] = fsqrt(fmaxf((float)(e.ss * invn), 0.0f));
+            xs_[20 + j] = kap;
           }
         }
-        if (EXP && P.do_exp && !(stx & RF_PIX_FIT) && gx < P.W) {
-          const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
-          const float qn = __int_as_float(0x7fc00000);
-          P.exp.normal[3 * p + 0] = qn;
-          P.exp.normal[3 * p + 1] = qn;
-          P.exp.normal[3 * p + 2] = qn;
-          P.exp.offset[p] = qn;
-          P.exp.residual[p] = qn;
-          P.exp.curvature[p] = qn;
-          P.exp.status[p] = stx;
+        if (EXP && P.do_exp) {
+          float* xs_ = xstage + 28 * tid;
+          if (!(stx & RF_PIX_FIT)) {
+            const float qn = __int_as_float(0x7fc00000);
+            xs_[3 * j + 0] = qn;
+            xs_[3 * j + 1] = qn;
+            xs_[3 * j + 2] = qn;
+            xs_[12 + j] = qn;
+            xs_[16 + j] = qn;
+            xs_[20 + j] = qn;
+          }
+          reinterpret_cast<uint8_t*>(xs_ + 24)[j] = stx;
         }
     #if RF_STAGE_OUTPUTS
         o_n[j][0] = nx;
@@ -671,6 +675,33 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     #endif
       }
 
+      if (EXP && P.do_exp) {  // staged explicit outputs -> global, as vectors when aligned
+        const float* xs_ = xstage + 28 * tid;
+        const int64_t pix0 = frame * P.out_frame + (int64_t)gy * P.W + gxs;
+        if (((P.W & (KSEG - 1)) == 0) && (gxs + KSEG <= P.W)) {
+          const float4* sv = reinterpret_cast<const float4*>(xs_);
+          float4* pn = reinterpret_cast<float4*>(P.exp.normal + 3 * pix0);
+          pn[0] = sv[0];
+          pn[1] = sv[1];
+          pn[2] = sv[2];
+          *reinterpret_cast<float4*>(P.exp.offset + pix0) = sv[3];
+          *reinterpret_cast<float4*>(P.exp.residual + pix0) = sv[4];
+          *reinterpret_cast<float4*>(P.exp.curvature + pix0) = sv[5];
+          *reinterpret_cast<uchar4*>(P.exp.status + pix0) = *reinterpret_cast<const uchar4*>(xs_ + 24);
+        } else {
+          for (int j = 0; j < KSEG; ++j) {
+            if (gxs + j >= P.W) break;
+            const int64_t p = pix0 + j;
+            P.exp.normal[3 * p + 0] = xs_[3 * j + 0];
+            P.exp.normal[3 * p + 1] = xs_[3 * j + 1];
+            P.exp.normal[3 * p + 2] = xs_[3 * j + 2];
+            P.exp.offset[p] = xs_[12 + j];
+            P.exp.residual[p] = xs_[16 + j];
+            P.exp.curvature[p] = xs_[20 + j];
+            P.exp.status[p] = reinterpret_cast<const uint8_t*>(xs_ + 24)[j];
+          }
+        }
+      }
     #if RF_STAGE_OUTPUTS
       // ---- stores
       if (P.do_imp) {
@@ -1020,14 +1051,15 @@ __attribute__((format(printf, 2, 3))) rf_status fail(rf_status s, const char* fm
   return s;
 }
 
-size_t smem_bytes(int var, int r, bool tma, int esz) {
+size_t smem_bytes(int var, int r, bool tma, int esz, bool exp = false) {
   const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
   const int nvd = var == VAR_DF ? 3 : 5, nvi = var == VAR_DF ? 3 : 1;
   const bool noprim = tma && noprim_radius(r);  // matches the kernel's NOPRIM (RT == r)
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
   const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
   return 2 * raw + sizeof(double) * ((noprim ? 0 : (size_t)hh * hw) + (size_t)nvd * TH * vrs) +
-         sizeof(int) * (size_t)nvi * TH * vrs + 8 /* align */ + 2 * sizeof(uint64_t) + 128 /* base align */;
+         sizeof(int) * (size_t)nvi * TH * vrs + 8 /* align */ + 2 * sizeof(uint64_t) + 128 /* base align */ +
+         (exp ? (size_t)28 * sizeof(float) * NTHREADS + 16 : 0);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
@@ -1254,8 +1286,9 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   int dev = 0, smem_optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const bool tma_fits = smem_bytes(VAR_STD, r, true, esz) <= (size_t)smem_optin &&
-                        smem_bytes(VAR_DF, r, true, esz) <= (size_t)smem_optin;
+  const bool want_exp = (fmask & (RF_EXPLICIT_STANDARD | RF_EXPLICIT_RGBD)) != 0;
+  const bool tma_fits = smem_bytes(VAR_STD, r, true, esz, want_exp) <= (size_t)smem_optin &&
+                        smem_bytes(VAR_DF, r, true, esz, want_exp) <= (size_t)smem_optin;
   const bool tma = getenv("RF_DISABLE_TMA") == nullptr && tma_fits &&
                    make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
   // one launch per space: standard (implicit/explicit-standard), rgbd (implicit/explicit-rgbd)
@@ -1297,7 +1330,7 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     if (di) P.imp = OutPlanes{outs[fi].normal, outs[fi].offset, outs[fi].residual, outs[fi].curvature, outs[fi].status};
     if (de) P.exp = OutPlanes{outs[fe].normal, outs[fe].offset, outs[fe].residual, outs[fe].curvature, outs[fe].status};
     P.batch = batch;
-    const size_t sm = smem_bytes(var, r, tma, esz);
+    const size_t sm = smem_bytes(var, r, tma, esz, de);
     cudaError_t e;
     const cudaStream_t ls = (fork && var == VAR_DF) ? fs->aux : s;
     if (t->lat_x)  // non-separable tan maps
