@@ -14,8 +14,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 SOURCES = [PKG / "csrc" / "rf_fit.cu", PKG / "csrc" / "rf_rects.cu", PKG / "csrc" / "rf_integral.cu",
-           PKG / "csrc" / "rf_render.cu"]
-HEADERS = [ROOT / "include" / "rangefit_b200.h", PKG / "csrc" / "rf_solve.cuh", PKG / "csrc" / "rf_internal.h"]
+           PKG / "csrc" / "rf_render.cu", PKG / "csrc" / "rf_lattice.cu"]
+HEADERS = [ROOT / "include" / "rangefit_b200.h", PKG / "csrc" / "rf_solve.cuh", PKG / "csrc" / "rf_internal.h",
+           PKG / "csrc" / "rf_tile.cuh", PKG / "csrc" / "rf_general.cuh"]
 OUT = PKG / "librangefit_b200.so"
 
 NVCC_FLAGS = [

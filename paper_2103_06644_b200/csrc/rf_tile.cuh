@@ -1,0 +1,83 @@
+// rf_tile.cuh -- definitions shared by the per-pixel fit kernels (rf_fit.cu: separable tan
+// maps; rf_lattice.cu: distortion lattices): tile geometry, kernel parameters, output planes.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rangefit_b200.h"
+
+namespace rf_tile {
+
+constexpr int TW = 64;       // output tile width  (pixels)
+constexpr int TH = 16;       // output tile height (pixels)
+constexpr int KSEG = 4;      // consecutive output pixels per thread
+constexpr int NTHREADS = (TW / KSEG) * TH;  // 256
+constexpr int MAX_RADIUS = 32;
+#ifndef RF_ABLATE
+#define RF_ABLATE 0
+#endif
+#ifndef RF_STAGE_OUTPUTS
+#define RF_STAGE_OUTPUTS 1
+#endif
+#ifndef RF_MIN_BLOCKS
+#define RF_MIN_BLOCKS 2
+#endif
+
+constexpr int VAR_STD = 0;   // implicit-standard
+constexpr int VAR_DF = 1;    // implicit-rgbd (disparity form)
+
+struct OutPlanes {
+  float* normal;
+  float* offset;
+  float* residual;
+  float* curvature;
+  uint8_t* status;
+};
+
+struct KParams {
+  const void* depth;
+  const uint8_t* mask;
+  const double* tan_x;  // [W]
+  const double* tan_y;  // [H]
+  double ifx, ify;
+  int64_t row_pitch;
+  int64_t frame_stride;
+  int64_t out_frame;    // H*W
+  int64_t batch;
+  int H, W, r, dtype;
+  int do_imp, do_exp;  // implicit / explicit fit of this kernel's space requested
+  OutPlanes imp, exp;  // implicit-* / explicit-* output planes of the space
+};
+
+// bytes per depth element
+__host__ __device__ __forceinline__ int elem_size(int dtype) {
+  return dtype == RF_DEPTH_U16_MM ? 2 : dtype == RF_DEPTH_F64_M ? 8 : 4;
+}
+
+// residue-major column stride of the column-sum buffers (VQ = 4 mod 8 spreads the banks)
+__host__ __device__ __forceinline__ int vq_of(int hw) {
+  int q = (hw + 3) / 4;
+  return q + ((4 - q % 8) + 8) % 8;
+}
+
+struct TileGeom {
+  int64_t frame;
+  int x0, y0;
+};
+
+__device__ __forceinline__ TileGeom tile_of(int64_t t, int ntx, int nty) {
+  TileGeom g;
+  const int64_t per_frame = (int64_t)ntx * nty;
+  g.frame = t / per_frame;
+  const int rem = (int)(t - g.frame * per_frame);
+  const int ty = rem / ntx;
+  g.y0 = ty * TH;
+  g.x0 = (rem - ty * ntx) * TW;
+  return g;
+}
+
+// launch the per-pixel fits of one space on cameras with distortion lattices (rf_lattice.cu)
+cudaError_t launch_lattice(int var, const KParams& P, const double* lat_x, const double* lat_y,
+                           cudaStream_t s);
+
+}  // namespace rf_tile

@@ -34,7 +34,7 @@ def line_of(marker):
     return 10 ** 9
 
 
-marks = sorted([(line_of("// residue-major column stride"), "tma_helpers"),
+marks = sorted([(line_of("__device__ __forceinline__ uint32_t smem_u32"), "tma_helpers"),
                 (line_of("double primary_from_f32"), "primary"),
                 (line_of("template <int VAR, bool USE_TMA, int RT, bool EXP>"), "kernel-setup"),
                 (line_of("// ---- 1. halo tile -> primary"), "convert"),
