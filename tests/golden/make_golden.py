@@ -423,6 +423,24 @@ def main():
     z6 = np.where(d6.valid, d6.values, 0.0).astype(np.float32)
     run_case("distorted_f32_w5", cam6, rf.DepthImage(values=z6.astype(np.float64)), z6, 5, "f32")
 
+    # 7. larger windows: uint16 with an explicit mask at 9x9, and a 15x15 near/far crop
+    rng_w = np.random.default_rng(57)
+    cam7 = rf.CameraIntrinsics(fx=45.0, fy=45.0, cx=19.5, cy=15.5, width=40, height=32)
+    maps7 = rf.compute_tan_maps(cam7)
+    d7, _ = rf.render_scene(rf.SyntheticScene((random_plane(rng_w, 0.8, 3.0), random_plane(rng_w, 0.8, 3.0))),
+                            maps7, noise=rf.NoiseModel(), seed=21, dropout=0.08)
+    mm7 = d7.to_millimeters()
+    mask7 = rng_w.random(mm7.shape) > 0.1
+    dm7 = rf.DepthImage.from_millimeters(mm7)
+    run_case("planes_u16_mask_w9", cam7, rf.DepthImage(values=dm7.values, valid=dm7.valid & mask7), mm7, 9, "u16")
+    cam8 = rf.CameraIntrinsics(fx=1400.0, fy=1400.0, cx=23.5, cy=17.5, width=48, height=36)
+    maps8 = rf.compute_tan_maps(cam8)
+    scene8 = rf.SyntheticScene((rf.GroundTruthPlane(np.array([0.1, -0.05, -1.0, 0.45]), mask_rect=(0, 0, 30, 36)),
+                                rf.GroundTruthPlane(np.array([-0.2, 0.1, -1.0, 7.5]), mask_rect=(30, 0, 48, 36))))
+    d8, _ = rf.render_scene(scene8, maps8, noise=rf.NoiseModel(), seed=22, dropout=0.05)
+    z8 = np.where(d8.valid, d8.values, 0.0).astype(np.float32)
+    run_case("near_far_w15", cam8, rf.DepthImage(values=z8.astype(np.float64)), z8, 15, "f32")
+
 
 if __name__ == "__main__":
     main()

@@ -47,6 +47,8 @@ def test_oracle_matches_reference_golden(case, form):
 def _vals(g, mask):
     if g["dtype"] == "u16":
         v, valid = O.depth_from_millimeters(g["depth"])
+        if mask is not None:
+            valid = valid & mask.astype(bool)
     else:
         v, valid = O.depth_from_meters(g["depth"], mask)
     return v, valid
