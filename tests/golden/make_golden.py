@@ -440,6 +440,14 @@ def main():
     d8, _ = rf.render_scene(scene8, maps8, noise=rf.NoiseModel(), seed=22, dropout=0.05)
     z8 = np.where(d8.valid, d8.values, 0.0).astype(np.float32)
     run_case("near_far_w15", cam8, rf.DepthImage(values=z8.astype(np.float64)), z8, 15, "f32")
+    # C5's 31x31 windows on a 64x48 crop of an f=2900 camera, near and far planes
+    cam9 = rf.CameraIntrinsics(fx=2900.0, fy=2900.0, cx=31.5, cy=23.5, width=64, height=48)
+    maps9 = rf.compute_tan_maps(cam9)
+    scene9 = rf.SyntheticScene((rf.GroundTruthPlane(np.array([0.03, 0.01, -1.0, 0.35]), mask_rect=(0, 0, 40, 48)),
+                                rf.GroundTruthPlane(np.array([0.1, -0.2, -1.0, 16.0]), mask_rect=(40, 0, 64, 48))))
+    d9, _ = rf.render_scene(scene9, maps9, noise=rf.NoiseModel(), seed=23, dropout=0.05)
+    z9 = np.where(d9.valid, d9.values, 0.0).astype(np.float32)
+    run_case("near_far_w31", cam9, rf.DepthImage(values=z9.astype(np.float64)), z9, 31, "f32")
 
 
 if __name__ == "__main__":
