@@ -87,6 +87,19 @@ def profiled_pipes(kernel: str):
             "source": "profiles/ncu_summary.json (ncu --set full)"}
 
 
+def host_cpu() -> dict:
+    """CPU model and the cores this process may run on."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "affinity_cores": len(os.sched_getaffinity(0))}
+
+
 def link_bandwidth(host_out, out, forms, stream) -> float:
     """Device->host bandwidth of one plain pinned copy of a whole step's outputs (GB/s): the
     ceiling the end-to-end pipeline is held to."""
@@ -351,7 +364,7 @@ def run_ours(args, world, rank, local):
         r, cores, el, sample = cpu_reference_rate(frames_host, cfg, args.cpu_seconds)
         r1, _, _, sample1 = cpu_reference_rate(frames_host, cfg, 0.5, threads=1)
         cpu_baseline = {"value": r / 1e6, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
-                        "value_1core": r1 / 1e6, "sample_1core": sample1}
+                        "value_1core": r1 / 1e6, "sample_1core": sample1, "host": host_cpu()}
 
     if rank == 0:
         line = {
