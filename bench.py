@@ -253,7 +253,8 @@ def run_reference(args, world, rank):
         "config": {"workload": "C2: 64x640x480 f32 depth, window 5, implicit-rgbd + implicit-standard",
                    "note": "each step fits a bounded sample (whole frames for ~2 s); value extrapolates "
                            "pixel-fits/s to the 64-frame step"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "host": host_cpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
