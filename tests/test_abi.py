@@ -74,3 +74,33 @@ def test_check_maps_status_to_exceptions():
         N.check(N.RF_ERR_SHAPE, "x")
     with pytest.raises(RuntimeError):
         N.check(N.RF_ERR_CUDA, "x")
+
+
+def test_new_entry_points_validate_before_the_device():
+    """The integral / scatter / rect / render entry points reject bad arguments without any
+    CUDA call (so these run on a CPU-only host)."""
+    lib = N.load()
+    vp = ctypes.c_void_p
+    # rf_box_sums: counts and pointers
+    assert lib.rf_box_sums(None, 0, 4, 4, None, 0, None, None) == N.RF_OK  # nothing to do
+    assert lib.rf_box_sums(None, -1, 4, 4, None, 1, None, None) == N.RF_ERR_ARGUMENT
+    ptrs = (vp * 40)()
+    assert lib.rf_box_sums(ptrs, 40, 4, 4, vp(1), 1, vp(1), None) == N.RF_ERR_ARGUMENT  # > 32 tables
+    assert lib.rf_box_sums(ptrs, 1, 0, 4, vp(1), 1, vp(1), None) == N.RF_ERR_SHAPE
+    # rf_fit_scatters: count, formulation, explicit systems need a right-hand side
+    assert lib.rf_fit_scatters(None, None, None, None, -1, 0, None, None) == N.RF_ERR_ARGUMENT
+    assert lib.rf_fit_scatters(None, None, None, None, 1, 7, None, None) == N.RF_ERR_ARGUMENT
+    assert lib.rf_fit_scatters(vp(1), None, None, vp(1), 1, N.RF_FORM_EXPLICIT_RGBD, vp(1), None) \
+        == N.RF_ERR_ARGUMENT
+    assert lib.rf_fit_scatters(None, None, None, None, 0, 0, None, None) == N.RF_OK
+    # rf_integral: shape and pointers
+    assert lib.rf_integral(None, 4, None, 4, 4, None, None) == N.RF_ERR_ARGUMENT
+    assert lib.rf_integral(vp(1), 2, None, 4, 4, vp(1), None) == N.RF_ERR_SHAPE  # pitch < width
+    # entry points that need camera tables reject a null handle
+    assert lib.rf_build_channel(None, None, 0, 4, None, 0, vp(1), None) == N.RF_ERR_ARGUMENT
+    assert lib.rf_fit_rects(None, None, 0, 1, 4, 4, 4, None, None, 1, 0, None, None) == N.RF_ERR_ARGUMENT
+    assert lib.rf_max_residuals(None, None, 0, 1, 4, 4, 4, None, None, 1, 0, None, None, None) \
+        == N.RF_ERR_ARGUMENT
+    assert lib.rf_render_planes(None, None, None, 1, None, None, 0.0, 0.0, None, None, None, None) \
+        == N.RF_ERR_ARGUMENT
+    assert "rf_render_planes" in N.last_error()
