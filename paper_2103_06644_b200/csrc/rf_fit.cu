@@ -934,12 +934,16 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   ForkStream* fs = nullptr;
   std::unique_lock<std::mutex> fork_lock(g_fork_mu, std::defer_lock);
-  const bool fork = both && tiles <= (int64_t)8 * nsm && getenv("RF_NO_FORK") == nullptr;
+  bool fork = both && tiles <= (int64_t)8 * nsm && getenv("RF_NO_FORK") == nullptr;
   if (fork) {
     fork_lock.lock();
-    if (!fork_stream(dev, fs)) return fail(RF_ERR_CUDA, "side stream creation failed");
-    cudaEventRecord(fs->fork, s);
-    cudaStreamWaitEvent(fs->aux, fs->fork, 0);
+    fork = fork_stream(dev, fs);  // no side stream (e.g. device index >= 64): launch in order
+    if (fork) {
+      cudaEventRecord(fs->fork, s);
+      cudaStreamWaitEvent(fs->aux, fs->fork, 0);
+    } else {
+      fork_lock.unlock();
+    }
   }
   for (int var = 0; var < 2; ++var) {
     const int fi = var == VAR_STD ? RF_FORM_IMPLICIT_STANDARD : RF_FORM_IMPLICIT_RGBD;
