@@ -42,3 +42,25 @@ def test_segment_matches_reference(form, case, backend):
     assert [t.status.value for t in seg.tiles] == list(z[f"{key}_status"])
     np.testing.assert_array_equal(np.array([t.cluster for t in seg.tiles]), z[f"{key}_cluster"])
     np.testing.assert_array_equal(seg.labels.cpu().numpy(), z[f"{key}_labels"])
+
+
+def test_segment_frame_of_a_batch_and_mask():
+    """segment() on frame k of a [B,H,W] batch equals segment() of that frame alone; a mask
+    equals zeroing the masked depth."""
+    z = np.load(GOLDEN_DIR / "segment_planes.npz")
+    d = torch.from_numpy(z["depth"]).cuda()
+    H, W = d.shape
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(float(z["fx"]), float(z["fy"]), float(z["cx"]),
+                                                   float(z["cy"]), W, H))
+    cfg = S.SegConfig(formulation="implicit-rgbd", initial_tile=32, max_depth=3, k=6, seed=3)
+    batch = torch.stack([torch.flip(d, dims=[1]), d])
+    a = S.segment(batch, maps, cfg, frame=1)
+    b = S.segment(d, maps, cfg)
+    assert [tuple(t.rect) for t in a.tiles] == [tuple(t.rect) for t in b.tiles]
+    assert torch.equal(a.labels, b.labels)
+    mask = torch.ones_like(d, dtype=torch.bool)
+    mask[10:40, 20:70] = False
+    c = S.segment(d, maps, cfg, mask=mask)
+    e = S.segment(torch.where(mask, d, torch.zeros_like(d)), maps, cfg)
+    assert [t.status for t in c.tiles] == [t.status for t in e.tiles]
+    assert torch.equal(c.labels, e.labels)
