@@ -448,6 +448,14 @@ def main():
     d9, _ = rf.render_scene(scene9, maps9, noise=rf.NoiseModel(), seed=23, dropout=0.05)
     z9 = np.where(d9.valid, d9.values, 0.0).astype(np.float32)
     run_case("near_far_w31", cam9, rf.DepthImage(values=z9.astype(np.float64)), z9, 31, "f32")
+    # C2's 11x11 window on a 5-plane frame with holes
+    rng_11 = np.random.default_rng(61)
+    cam10 = rf.CameraIntrinsics(fx=70.0, fy=70.0, cx=27.5, cy=19.5, width=56, height=40)
+    maps10 = rf.compute_tan_maps(cam10)
+    d10, _ = rf.render_scene(rf.SyntheticScene(tuple(random_plane(rng_11, 0.7, 3.5) for _ in range(5))), maps10,
+                             noise=rf.NoiseModel(), seed=24, dropout=0.12)
+    z10 = np.where(d10.valid, d10.values, 0.0).astype(np.float32)
+    run_case("planes_f32_w11", cam10, rf.DepthImage(values=z10.astype(np.float64)), z10, 11, "f32")
 
 
 if __name__ == "__main__":

@@ -53,7 +53,7 @@ def check_frame(depth_gpu, fits, cam, window, formulation, frame=0, pixels=None,
 GOLDEN_DIR = __import__("pathlib").Path(__file__).resolve().parent / "golden"
 GOLDEN_CASES = ("planes_f32_w3", "planes_f32_w5", "planes_f32_mask_w5", "planes_u16_w5",
                 "frontal_z3_w5", "half_invalid_w3", "near_far_w7", "distorted_f32_w5", "planes_u16_mask_w9",
-                "near_far_w15", "near_far_w31")
+                "near_far_w15", "near_far_w31", "planes_f32_w11")
 
 
 class Cam:

@@ -67,3 +67,31 @@ def test_rects_out_of_bounds_and_frames():
     out = rf.fit_rects(batch, maps, [(0, 0, 8, 8), (0, 0, 8, 8), (-1, 0, 4, 4)], rf.IMPLICIT_RGBD, frames=[0, 1, 0])
     assert out["status"][2] & rf.fitting.RECT_OUT_OF_BOUNDS
     np.testing.assert_array_equal(out["coef"][0], out["coef"][1])
+
+
+@pytest.mark.parametrize("window", [3, 7, 15])
+def test_pixel_and_rect_kernels_agree(window):
+    """Two independent device paths, one semantics: the per-pixel tile kernel at pixel (x, y)
+    and the rect kernel on that pixel's clipped window (A9) give the same fit."""
+    from paper_2103_06644_b200 import scenes
+    cfg = scenes.small_config("C2", 128, 80)
+    depth = scenes.render_frame(cfg, 9).cuda()
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(cfg.f, cfg.f, cfg.cx, cfg.cy, cfg.width, cfg.height))
+    out = rf.fit_pixels(depth, maps, window, rf.FORMULATIONS)
+    rng = np.random.default_rng(window)
+    H, W = depth.shape
+    r = window // 2
+    pix = rng.choice(H * W, 300, replace=False)
+    rects = [(max(p % W - r, 0), max(p // W - r, 0), min(p % W + r + 1, W), min(p // W + r + 1, H)) for p in pix]
+    for form in rf.FORMULATIONS:
+        rows = rf.fit_rects(depth, maps, rects, form)
+        st = out[form].status.reshape(-1)[torch.from_numpy(pix).cuda()].cpu().numpy()
+        center_valid = (st & 1) != 0
+        # the rect fit ignores the centre pixel's own validity (a rect has no centre rule)
+        np.testing.assert_array_equal((st & 2) != 0, center_valid & ((rows["status"] & 2) != 0))
+        ok = ((st & 6) == 2) & ((rows["status"] & 4) == 0)
+        gn = out[form].normal.reshape(-1, 3)[torch.from_numpy(pix).cuda()].cpu().numpy()[ok]
+        rn = rows["coef"][ok, :3] / np.linalg.norm(rows["coef"][ok, :3], axis=1, keepdims=True)
+        assert normal_angles(gn, rn).max() <= 1e-5, form
+        gr = out[form].residual.reshape(-1)[torch.from_numpy(pix).cuda()].cpu().numpy()[ok]
+        np.testing.assert_allclose(gr, rows["rms"][ok], rtol=1e-4, atol=1e-9)
