@@ -30,6 +30,9 @@ def test_gpu_matches_reference_golden(case):
         m = compare(gpu_flat(out[form], 0) if out[form].normal.dim() == 4 else gpu_flat_2d(out[form]), g[form],
                     explicit_fit=form.startswith("explicit"))
         assert m["ok"], (case, form, m)
+        # against the reference's own outputs the degenerate bit matches too (it is a float
+        # threshold, so the general parity contract only reports it)
+        assert m["degenerate_mismatch"] == 0, (case, form, m["degenerate_mismatch"])
 
 
 def gpu_flat_2d(fits):
