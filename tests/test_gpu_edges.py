@@ -180,3 +180,29 @@ def test_concurrent_callers_on_separate_streams():
     for t in ts:
         t.join()
     assert not errors, errors[:4]
+
+
+def test_fit_pixels_is_cuda_graph_capturable():
+    """A streaming loop can capture fit_pixels once in a CUDA graph and replay it (the fork
+    onto the side stream and the join are captured too)."""
+    cfg = scenes.small_config("C1", 160, 120)
+    _, maps = _maps(cfg)
+    static_in = scenes.render_frame(cfg, 40).cuda()
+    out = {f: rf.PixelFits.empty(1, cfg.height, cfg.width, "cuda") for f in rf.PIXEL_FORMULATIONS}
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        rf.fit_pixels(static_in, maps, 5, out=out, stream=s)  # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        rf.fit_pixels(static_in, maps, 5, out=out, stream=torch.cuda.current_stream())
+    for seed in (41, 42):
+        frame = scenes.render_frame(cfg, seed).cuda()
+        static_in.copy_(frame)
+        g.replay()
+        torch.cuda.synchronize()
+        ref = rf.fit_pixels(frame, maps, 5)
+        for f in rf.PIXEL_FORMULATIONS:
+            assert torch.equal(out[f].status[0], ref[f].status)
+            assert torch.equal(torch.nan_to_num(out[f].normal[0]), torch.nan_to_num(ref[f].normal))
