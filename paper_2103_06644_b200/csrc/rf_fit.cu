@@ -35,6 +35,7 @@
 #include "rf_tile.cuh"
 #include "rf_solve.cuh"
 #include "rf_general.cuh"
+#include "rf_direct.cuh"
 
 namespace {
 using namespace rf_dev;
@@ -182,6 +183,11 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;
   const int64_t total = (int64_t)ntx * nty * P.batch;
   const uint32_t box_bytes = (uint32_t)(HH_ * HWP * esz);
+  // sliding-sum guard: high word of the tile's largest primary (p >= 0, so the word orders
+  // like the value), double-buffered by tile parity; see the row pass
+  __shared__ unsigned int s_pmax[2];
+  if (tid == 0) s_pmax[0] = s_pmax[1] = 0u;
+  __syncthreads();
 
   if (USE_TMA) {
     if (tid == 0) {
@@ -274,6 +280,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       __syncthreads();
     }
 
+    // running column sums: high word of this thread's largest primary entering the sums
+    // (the tile max feeds the sliding-sum guard at the end of the row pass)
+    unsigned int pm = 0u;
 #if RF_ABLATE >= 4
     if (false)
 #endif
@@ -362,6 +371,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         auto add = [&](int ii, double fdy, int dy, double sg) {
           const double p = NOPRIM ? raw_primary(ii, col) : prim[ii * HW_ + col];
           const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
+          if (sg > 0.0) pm = max(pm, (unsigned)__double2hiint(p));
           if (VAR == VAR_DF) {
             a[0] = fma(sg, p, a[0]);
             a[1] = fma(sg * p, p, a[1]);
@@ -395,6 +405,10 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         }
       }
     }
+    if constexpr (!CENTRED) {
+      const unsigned int b = __reduce_max_sync(0xffffffffu, pm);
+      if ((tid & 31) == 0 && b) atomicMax(&s_pmax[it & 1], b);
+    }
     __syncthreads();
 
     // ---- 3/4. horizontal running sums + per-window solve
@@ -410,7 +424,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       const double* vrow = vd + orow * VRS;
       const int* irow = vi + orow * VRS;
       const int vstride = TH * VRS;
-
+      if (!CENTRED && tid == 0) s_pmax[(it + 1) & 1] = 0u;  // read by the previous tile, written by the next
       // running horizontal sums (origin: segment start xs, tile row y0)
       double h[VAR == VAR_DF ? 4 : 9];
       int hi[VAR == VAR_DF ? 6 : 1];
@@ -662,6 +676,48 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       }
       }
     #endif
+      {
+        // Sliding-sum guard.  A running sum keeps the rounding residue (~eps x value) of
+        // every sample that has left it, so a window far smaller than the samples that slid
+        // through its sums (a few millimetre depths in a column that just held metres) would
+        // inherit an error the reference's direct sums do not have.  Mass that passed through
+        // one of this segment's window sums outside the window: the row pass's 3 leading
+        // columns (their vertical sums of p^2, read back), and with running column sums also
+        // the (o - o0) leading rows of the column segment over 2r + 4 columns, each sample
+        // <= the tile's largest p^2.  When that bound exceeds 1024x a lower bound of a fitted
+        // window's own sum of p^2 -- its centre column's vertical sum, which holds the centre
+        // sample itself (empty columns belong to unfitted pixels and are skipped) -- the
+        // residue could exceed what the parity allowances absorb for every conditioning, and
+        // the segment is queued for a direct refit after this kernel (queue_refit /
+        // refit_kernel, rf_direct.cuh / rf_lattice.cu); only depth ratios of ~10x or more
+        // inside one tile's footprint can trigger it.  All of it runs after the unrolled loop
+        // (no register held through the solve), in whole exponent steps on the high words of
+        // the non-negative doubles (they order like the values; the guard needs orders of
+        // magnitude only).
+        const int* vhi = reinterpret_cast<const int*>(vd + (TH + orow) * VRS);  // channel 1, row orow
+        auto col_hi = [&](int c) { return vhi[2 * ((c & 3) * VQ + (c >> 2)) + 1]; };
+        // log2 of the departed mass, rounded up: 3 x the largest departed column sum ...
+        int te = (max(col_hi(xs), max(col_hi(xs + 1), col_hi(xs + 2))) >> 20) - 1023 + 2;
+        if (!CENTRED) {  // ... and (o - o0) x (2r + 4) departed samples of the column segment
+          int o0r = 0;
+          const int parts = max(1, min(NTHREADS / HW_, TH));
+#pragma unroll 1
+          for (int q = 1; q < parts; ++q)
+            if ((q * TH) / parts <= orow) o0r = (q * TH) / parts;
+          const int rows = (orow - o0r) * (2 * r + KSEG);
+          if (rows > 0) te = max(te, 2 * ((int)(s_pmax[it & 1] >> 20) - 1023) + 32 - __clz(rows)) + 1;
+        }
+        te -= 10;  // / 1024
+        const int thr = te < -1022 ? 0 : te > 1023 ? 0x7ff00000 : (te + 1023) << 20;
+        int h1min = 0x7fffffff;
+#pragma unroll
+        for (int j = 0; j < KSEG; ++j) {
+          const int w = col_hi(xs + j + r);
+          h1min = min(h1min, w > 0 ? w : 0x7fffffff);
+        }
+        if (h1min < thr)
+          queue_refit(P, frame, gy, gxs, (1u << min(KSEG, P.W - gxs)) - 1u);
+      }
       }
     }
     __syncthreads();  // prim / vd are rewritten by the next tile
@@ -805,8 +861,9 @@ int32_t rf_abi_version(void) { return RF_ABI_VERSION; }
 const char* rf_last_error(void) { return g_err; }
 
 int32_t rf_launches_per_call(int32_t formulation_mask) {
+  // one tile kernel per space + one sliding-sum guard refit launch
   return ((formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) ? 1 : 0) +
-         ((formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) ? 1 : 0);
+         ((formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) ? 1 : 0) + (formulation_mask ? 1 : 0);
 }
 
 rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const double* delta_y,
@@ -857,6 +914,9 @@ rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const
   }
   e = cudaMalloc(&t->tan_x, sizeof(double) * in->width);
   if (e == cudaSuccess) e = cudaMalloc(&t->tan_y, sizeof(double) * in->height);
+  if (e == cudaSuccess) e = cudaMalloc(&t->fix_ctr, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMemset(t->fix_ctr, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&t->fix_list, sizeof(unsigned long long) * 2 * RF_FIX_CAP);
   if (e == cudaSuccess) {
     const int m = in->width > in->height ? in->width : in->height;
     tan_table_kernel<<<(m + 255) / 256, 256>>>(t->tan_x, t->tan_y, in->width, in->height, in->fx,
@@ -870,6 +930,8 @@ rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const
     cudaFree(t->tan_y);
     cudaFree(t->lat_x);
     cudaFree(t->lat_y);
+    cudaFree(t->fix_ctr);
+    cudaFree(t->fix_list);
     delete t;
     return fail(RF_ERR_CUDA, "rf_tables_create: %s", cudaGetErrorString(e));
   }
@@ -883,6 +945,8 @@ rf_status rf_tables_destroy(rf_tables* t) {
   cudaFree(t->tan_y);
   cudaFree(t->lat_x);
   cudaFree(t->lat_y);
+  cudaFree(t->fix_ctr);
+  cudaFree(t->fix_list);
   delete t;
   return RF_OK;
 }
@@ -945,6 +1009,8 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
       fork_lock.unlock();
     }
   }
+  KParams PP[2];
+  memset(PP, 0, sizeof(PP));
   for (int var = 0; var < 2; ++var) {
     const int fi = var == VAR_STD ? RF_FORM_IMPLICIT_STANDARD : RF_FORM_IMPLICIT_RGBD;
     const int fe = var == VAR_STD ? RF_FORM_EXPLICIT_STANDARD : RF_FORM_EXPLICIT_RGBD;
@@ -970,6 +1036,9 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     if (di) P.imp = OutPlanes{outs[fi].normal, outs[fi].offset, outs[fi].residual, outs[fi].curvature, outs[fi].status};
     if (de) P.exp = OutPlanes{outs[fe].normal, outs[fe].offset, outs[fe].residual, outs[fe].curvature, outs[fe].status};
     P.batch = batch;
+    P.fix_ctr = t->fix_ctr + (var == VAR_STD ? 0 : 2);
+    P.fix_list = t->fix_list + (size_t)var * RF_FIX_CAP;
+    P.fix_cap = RF_FIX_CAP;
     const size_t sm = smem_bytes(var, r, tma, esz, de);
     cudaError_t e;
     const cudaStream_t ls = (fork && var == VAR_DF) ? fs->aux : s;
@@ -979,6 +1048,7 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
       e = tma ? launch_radius<VAR_STD>(P, tmap, sm, tiles, ls) : launch_var<VAR_STD, false, 0>(P, tmap, sm, tiles, ls);
     else
       e = tma ? launch_radius<VAR_DF>(P, tmap, sm, tiles, ls) : launch_var<VAR_DF, false, 0>(P, tmap, sm, tiles, ls);
+    PP[var] = P;
     if (e != cudaSuccess) {
       if (fork) {  // keep the caller's stream joined even on failure
         cudaEventRecord(fs->join, fs->aux);
@@ -991,6 +1061,8 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     cudaEventRecord(fs->join, fs->aux);
     cudaStreamWaitEvent(s, fs->join, 0);
   }
+  const cudaError_t e = launch_refit(PP[VAR_STD], PP[VAR_DF], t->lat_x, t->lat_y, t->fix_ctr, s);
+  if (e != cudaSuccess) return fail(RF_ERR_CUDA, "refit launch: %s", cudaGetErrorString(e));
   return RF_OK;
 }
 

@@ -11,6 +11,7 @@
 #include "rf_tile.cuh"
 #include "rf_solve.cuh"
 #include "rf_general.cuh"
+#include "rf_direct.cuh"
 
 namespace {
 using namespace rf_dev;
@@ -18,96 +19,18 @@ using namespace rf_tile;
 
 // ------------------------------------------------------------------ distortion lattices
 // Cameras with non-zero delta_* lattices (camera.py:35-75): the tan maps are not separable,
-// so the tile kernels' exact-integer geometry does not apply.  One thread per output pixel
-// sums its clipped window directly (fp64 moments relative to the pixel's own tan values,
-// rf_general.cuh) and runs the same solve / canonical output as the tile kernels.
-__device__ __forceinline__ void store_fit(const OutPlanes& o, int64_t p, float nx, float ny, float nz, float off,
-                                          float res, float cur, uint8_t st) {
-  o.normal[3 * p + 0] = nx;
-  o.normal[3 * p + 1] = ny;
-  o.normal[3 * p + 2] = nz;
-  o.offset[p] = off;
-  o.residual[p] = res;
-  o.curvature[p] = cur;
-  o.status[p] = st;
-}
-
+// so the tile kernels' exact-integer geometry does not apply.  Direct fallback: one thread
+// per output pixel sums its clipped window directly (rf_direct.cuh).
 template <int VAR, bool EXP>
 __global__ void __launch_bounds__(128) fit_lattice_kernel(const KParams P, const double* lat_x,
                                                           const double* lat_y) {
   const int64_t total = P.batch * P.out_frame;
-  const int r = P.r;
-  const bool std_space = VAR == VAR_STD;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t frame = p / P.out_frame;
     const int rem = (int)(p - frame * P.out_frame);
-    const int y = rem / P.W, x = rem - y * P.W;
-    auto sample = [&](int yy, int xx, double& z) -> bool {
-      const int64_t off = frame * P.frame_stride + (int64_t)yy * P.row_pitch + xx;
-      bool valid;
-      if (P.dtype == RF_DEPTH_U16_MM) {
-        const unsigned short mm = __ldg(reinterpret_cast<const unsigned short*>(P.depth) + off);
-        valid = mm > 0;
-        z = __ddiv_rn((double)mm, 1000.0);
-      } else if (P.dtype == RF_DEPTH_F64_M) {
-        z = __ldg(reinterpret_cast<const double*>(P.depth) + off);
-        valid = z > 0.0 && z <= 1.7976931348623157e308;
-      } else {
-        const float zf = __ldg(reinterpret_cast<const float*>(P.depth) + off);
-        valid = zf > 0.0f && zf <= 3.402823466e38f;
-        z = (double)zf;
-      }
-      if (P.mask) valid = valid && __ldg(P.mask + frame * P.out_frame + (int64_t)yy * P.W + xx) != 0;
-      return valid;
-    };
-    const float qn = __int_as_float(0x7fc00000);
-    float nx = qn, ny = qn, nz = qn, off = qn, res = qn, cur = qn;
-    float ex = qn, ey = qn, ez = qn, eo = qn, eres = qn, ecur = qn;
-    double zc;
-    const uint8_t valid_bit = sample(y, x, zc) ? RF_PIX_INPUT_VALID : 0;
-    uint8_t st = valid_bit, stx = valid_bit;
-    if (valid_bit) {
-      const double txc = __ldg(lat_x + (int64_t)y * P.W + x), tyc = __ldg(lat_y + (int64_t)y * P.W + x);
-      QMoments m;
-      const int ya = max(y - r, 0), yb = min(y + r, P.H - 1), xa = max(x - r, 0), xb = min(x + r, P.W - 1);
-      for (int yy = ya; yy <= yb; ++yy)
-        for (int xx = xa; xx <= xb; ++xx) {
-          double z;
-          if (!sample(yy, xx, z)) continue;
-          const int64_t li = (int64_t)yy * P.W + xx;
-          q_sample(std_space, z, __ldg(lat_x + li) - txc, __ldg(lat_y + li) - tyc, m);
-        }
-      const int nwin = (int)m.n;
-      if (nwin >= (EXP ? 3 : 4)) {
-        Sym3 C;
-        double mu0, mu1, mu2;
-        q_to_scatter(std_space, m, txc, tyc, C, mu0, mu1, mu2);
-        const double nd = m.n;
-        float kap = 0.0f;
-        if (P.do_imp && nwin >= 4) {
-          WindowFit f;
-          solve_window(C, mu0, mu1, mu2, nd, f);
-          if (std_space) finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
-          else finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
-          res = fsqrt(fmaxf((float)(f.lam / nd), 0.0f));
-          cur = kap = f.kappa;
-          st |= RF_PIX_FIT | (f.degenerate ? RF_PIX_DEGENERATE : 0);
-        }
-        if (EXP && P.do_exp) {
-          if (!(P.do_imp && nwin >= 4)) kap = curvature_only(C);
-          ExplicitFit e;
-          explicit_solve(C, mu0, mu1, mu2, nd, e);
-          if (std_space) finish_plane(e.a, e.b, -1.0, e.c, ex, ey, ez, eo);
-          else finish_plane(e.a, e.b, e.c, -1.0, ex, ey, ez, eo);
-          eres = fsqrt(fmaxf((float)(e.ss / nd), 0.0f));
-          ecur = kap;
-          stx |= RF_PIX_FIT | (e.degenerate ? RF_PIX_DEGENERATE : 0);
-        }
-      }
-    }
-    if (P.do_imp) store_fit(P.imp, p, nx, ny, nz, off, res, cur, st);
-    if (EXP && P.do_exp) store_fit(P.exp, p, ex, ey, ez, eo, eres, ecur, stx);
+    const int y = rem / P.W;
+    fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, y, rem - y * P.W);
   }
 }
 
@@ -137,7 +60,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
   const int tid = threadIdx.x;
   const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;
   const int64_t total = (int64_t)ntx * nty * P.batch;
-  for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+  __shared__ unsigned int s_qmax[2];  // sliding-sum guard (fit_tile_kernel): high word of max |q_i|
+  if (tid == 0) s_qmax[0] = s_qmax[1] = 0u;
+  __syncthreads();
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
     const TileGeom g = tile_of(t, ntx, nty);
     const int64_t frame = g.frame;
     const int x0 = g.x0, y0 = g.y0;
@@ -171,8 +98,9 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
     };
 
     // ---- column sums (running, over row segments; all threads busy)
+    const int parts = max(1, min(NTHREADS / HW_, TH));
+    unsigned int qm = 0u;
     {
-      const int parts = max(1, min(NTHREADS / HW_, TH));
       const int col = tid % HW_, part = tid / HW_;
       if (part < parts) {
         const int o0 = (part * TH) / parts, o1 = ((part + 1) * TH) / parts;
@@ -185,6 +113,9 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
           double q0, q1, q2;
           if (!qof(y0 - r + ii, x, q0, q1, q2)) return;
           const double s0 = sg * q0, s1 = sg * q1, s2 = sg * q2;
+          if (sg > 0.0)
+            qm = max(qm, max((unsigned)__double2hiint(q0) & 0x7fffffffu,
+                             max((unsigned)__double2hiint(q1) & 0x7fffffffu, (unsigned)__double2hiint(q2) & 0x7fffffffu)));
           a[0] += s0;
           a[1] += s1;
           a[2] += s2;
@@ -206,6 +137,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
           add(o, -1.0);
         }
       }
+    }
+    {
+      const unsigned int b = __reduce_max_sync(0xffffffffu, qm);
+      if ((tid & 31) == 0 && b) atomicMax(&s_qmax[it & 1], b);
     }
     __syncthreads();
 
@@ -231,6 +166,13 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
         };
         for (int k = 0; k <= 2 * r; ++k) accum(k, 1.0);
         const float qn = __int_as_float(0x7fc00000);
+        if (tid == 0) s_qmax[(it + 1) & 1] = 0u;
+        const float qmax = (float)__hiloint2double((int)s_qmax[it & 1], -1);
+        int o0r = 0;
+#pragma unroll 1
+        for (int q = 1; q < parts; ++q)
+          if ((q * TH) / parts <= orow) o0r = (q * TH) / parts;
+        unsigned bad = 0u;  // pixels the sliding-sum guard sends to the direct refit
         for (int j = 0; j < KSEG; ++j) {
           if (j > 0) {
             accum(j + 2 * r, 1.0);
@@ -244,6 +186,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
           float nx = qn, ny = qn, nz = qn, off = qn, res = qn, cur = qn;
           float ex = qn, ey = qn, ez = qn, eo = qn, eres = qn, ecur = qn;
           if (vbit && hc >= (EXP ? 3 : 4)) {
+            const int dep = (orow - o0r) * (2 * r + 1 + j) + j * (2 * r + 1);
+            if (dep && max(__double2hiint(h[3]), max(__double2hiint(h[6]), __double2hiint(h[8]))) <
+                           __double2hiint((double)(qmax * qmax * (float)dep * 0.0009765625f)))
+              bad |= 1u << j;
             QMoments m;
             m.n = (double)hc;
             m.s0 = h[0]; m.s1 = h[1]; m.s2 = h[2];
@@ -277,9 +223,56 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
           if (P.do_imp) store_fit(P.imp, p, nx, ny, nz, off, res, cur, st);
           if (EXP && P.do_exp) store_fit(P.exp, p, ex, ey, ez, eo, eres, ecur, stx);
         }
+        if (bad) queue_refit(P, frame, gy, gxs, bad);
       }
     }
     __syncthreads();  // vd / vc are rewritten by the next tile
+  }
+}
+
+// Sliding-sum guard refit (rf_direct.cuh), both spaces of one rf_fit_pixels call in one
+// launch: one thread per queued (entry, pixel bit); on worklist overflow every pixel of the
+// space.  The last block to finish resets both spaces' counters, so the next call on the
+// stream starts from empty lists.
+template <int VAR, bool EXP>
+__device__ __forceinline__ void refit_space(const KParams& P, const double* lat_x, const double* lat_y) {
+  const unsigned n = P.fix_ctr[0];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n > P.fix_cap) {
+    for (int64_t p = i0; p < P.batch * P.out_frame; p += stride) {
+      const int64_t frame = p / P.out_frame;
+      const int rem = (int)(p - frame * P.out_frame);
+      const int y = rem / P.W;
+      fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, y, rem - y * P.W);
+    }
+    return;
+  }
+  for (int64_t i = i0; i < 4 * (int64_t)n; i += stride) {
+    const unsigned long long e = P.fix_list[i >> 2];
+    const int bit = (int)(i & 3);
+    if (!((e >> bit) & 1ull)) continue;
+    const int64_t p = (int64_t)(e >> 4);
+    const int64_t frame = p / P.out_frame;
+    const int rem = (int)(p - frame * P.out_frame);
+    const int y = rem / P.W;
+    fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, y, rem - y * P.W + bit);
+  }
+}
+
+template <bool EXP_STD, bool EXP_DF>
+__global__ void __launch_bounds__(128) refit_kernel(const KParams Ps, const KParams Pd, const double* lat_x,
+                                                    const double* lat_y, unsigned* ctr) {
+  if (Ps.fix_ctr) refit_space<VAR_STD, EXP_STD>(Ps, lat_x, lat_y);
+  if (Pd.fix_ctr) refit_space<VAR_DF, EXP_DF>(Pd, lat_x, lat_y);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // ctr: [std entries, blocks done, df entries, unused]
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+      ctr[2] = 0u;
+    }
   }
 }
 
@@ -313,6 +306,20 @@ cudaError_t launch_lattice_var(const KParams& P, const double* lat_x, const doub
 }  // namespace
 
 namespace rf_tile {
+cudaError_t launch_refit(const KParams& Ps, const KParams& Pd, const double* lat_x, const double* lat_y,
+                         unsigned* ctr, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool es = Ps.do_exp, ed = Pd.do_exp;
+  sms = sms < 32 ? sms : 32;  // usually an empty list: keep the launch small
+  if (es && ed) refit_kernel<true, true><<<sms, 128, 0, s>>>(Ps, Pd, lat_x, lat_y, ctr);
+  else if (es) refit_kernel<true, false><<<sms, 128, 0, s>>>(Ps, Pd, lat_x, lat_y, ctr);
+  else if (ed) refit_kernel<false, true><<<sms, 128, 0, s>>>(Ps, Pd, lat_x, lat_y, ctr);
+  else refit_kernel<false, false><<<sms, 128, 0, s>>>(Ps, Pd, lat_x, lat_y, ctr);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_lattice(int var, const KParams& P, const double* lat_x, const double* lat_y,
                            cudaStream_t s) {
   return var == VAR_STD ? launch_lattice_var<VAR_STD>(P, lat_x, lat_y, s)

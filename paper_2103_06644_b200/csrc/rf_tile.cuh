@@ -47,6 +47,11 @@ struct KParams {
   int H, W, r, dtype;
   int do_imp, do_exp;  // implicit / explicit fit of this kernel's space requested
   OutPlanes imp, exp;  // implicit-* / explicit-* output planes of the space
+  // sliding-sum guard worklist of this space (rf_tables, rf_direct.cuh): fix_ctr[0] = entries
+  // appended, fix_ctr[1] = refit blocks done; entry = (first pixel index << 4) | pixel bits
+  unsigned* fix_ctr;
+  unsigned long long* fix_list;
+  unsigned fix_cap;
 };
 
 // bytes per depth element
@@ -77,6 +82,11 @@ __device__ __forceinline__ TileGeom tile_of(int64_t t, int ntx, int nty) {
 }
 
 // launch the per-pixel fits of one space on cameras with distortion lattices (rf_lattice.cu)
+// direct refit of the pixels the tile kernels' sliding-sum guard appended to the spaces'
+// worklists (one small launch after both tile kernels of a call; resets the worklists).
+// A space not computed by the call has a zeroed KParams (null fix_ctr).
+cudaError_t launch_refit(const KParams& Ps, const KParams& Pd, const double* lat_x, const double* lat_y,
+                         unsigned* ctr, cudaStream_t s);
 cudaError_t launch_lattice(int var, const KParams& P, const double* lat_x, const double* lat_y,
                            cudaStream_t s);
 
