@@ -109,7 +109,11 @@ rf_status rf_tables_destroy(rf_tables* tables);
  * (DepthImage(values, valid=mask), synth.py:88-94) or NULL.  outs: array of
  * RF_NUM_FORMULATIONS output sets indexed by RF_FORM_*; only the requested entries
  * are read.  The implicit and explicit fits of one space share one kernel launch
- * (one pass over the window moments).  stream: a cudaStream_t (NULL = legacy default). */
+ * (one pass over the window moments); one more small launch per call refits, from direct
+ * window sums, the rare windows whose running sums carried residue from far larger
+ * departed samples.  That worklist lives in the tables handle: calls sharing one handle
+ * must be ordered on one stream (use one handle per concurrent stream).
+ * stream: a cudaStream_t (NULL = legacy default). */
 rf_status rf_fit_pixels(const rf_tables* tables, const void* depth, int dtype, int64_t batch,
                         int32_t height, int32_t width, int64_t row_pitch, const uint8_t* mask,
                         int32_t window, int32_t formulation_mask, const rf_pixel_out* outs,
@@ -154,7 +158,8 @@ rf_status rf_max_residuals(const rf_tables* tables, const void* depth, int dtype
                            const rf_rect* rects, int64_t nrects, int32_t formulation, const double* coefs,
                            double* out, void* stream);
 
-/* Number of kernel launches rf_fit_pixels issues for a given formulation mask. */
+/* Number of kernel launches rf_fit_pixels issues for a given formulation mask (one tile
+ * kernel per space plus the refit launch). */
 int32_t rf_launches_per_call(int32_t formulation_mask);
 
 /* Thread-local message describing the last non-RF_OK status. */
