@@ -162,6 +162,11 @@ rf_status rf_max_residuals(const rf_tables* tables, const void* depth, int dtype
  * kernel per space plus the refit launch). */
 int32_t rf_launches_per_call(int32_t formulation_mask);
 
+/* Diagnostics: 4-pixel segments the last completed rf_fit_pixels call on these tables
+ * refit from direct window sums (the sliding-sum guard); synchronises
+ * the device.  -1 on error. */
+int64_t rf_last_refit_segments(const rf_tables* tables);
+
 /* Thread-local message describing the last non-RF_OK status. */
 const char* rf_last_error(void);
 

@@ -183,11 +183,14 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;
   const int64_t total = (int64_t)ntx * nty * P.batch;
   const uint32_t box_bytes = (uint32_t)(HH_ * HWP * esz);
-  // sliding-sum guard: high word of the tile's largest primary (p >= 0, so the word orders
-  // like the value), double-buffered by tile parity; see the row pass
-  __shared__ unsigned int s_pmax[2];
-  if (tid == 0) s_pmax[0] = s_pmax[1] = 0u;
-  __syncthreads();
+  // running column sums: high word of the largest primary that has left the tile's column
+  // sums (p >= 0, so high words order like the values), double-buffered by tile parity; the
+  // sliding-sum guard's departed-mass bound at the end of the row pass
+  __shared__ unsigned s_dmax[2];
+  if (!CENTRED) {
+    if (tid == 0) s_dmax[0] = s_dmax[1] = 0u;
+    __syncthreads();
+  }
 
   if (USE_TMA) {
     if (tid == 0) {
@@ -280,9 +283,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       __syncthreads();
     }
 
-    // running column sums: high word of this thread's largest primary entering the sums
-    // (the tile max feeds the sliding-sum guard at the end of the row pass)
-    unsigned int pm = 0u;
+    int dm = 0;  // running column sums: high word of the largest primary that left this thread's sums
 #if RF_ABLATE >= 4
     if (false)
 #endif
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         auto add = [&](int ii, double fdy, int dy, double sg) {
           const double p = NOPRIM ? raw_primary(ii, col) : prim[ii * HW_ + col];
           const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
-          if (sg > 0.0) pm = max(pm, (unsigned)__double2hiint(p));
+          if (sg < 0.0) dm = max(dm, __double2hiint(p));  // p >= 0: high words order like values
           if (VAR == VAR_DF) {
             a[0] = fma(sg, p, a[0]);
             a[1] = fma(sg * p, p, a[1]);
@@ -406,8 +407,8 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       }
     }
     if constexpr (!CENTRED) {
-      const unsigned int b = __reduce_max_sync(0xffffffffu, pm);
-      if ((tid & 31) == 0 && b) atomicMax(&s_pmax[it & 1], b);
+      const unsigned b = __reduce_max_sync(0xffffffffu, (unsigned)dm);  // dm >= 0
+      if ((tid & 31) == 0) atomicMax(&s_dmax[it & 1], b);
     }
     __syncthreads();
 
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       const double* vrow = vd + orow * VRS;
       const int* irow = vi + orow * VRS;
       const int vstride = TH * VRS;
-      if (!CENTRED && tid == 0) s_pmax[(it + 1) & 1] = 0u;  // read by the previous tile, written by the next
+      if (!CENTRED && tid == 0) s_dmax[(it + 1) & 1] = 0u;  // read by the previous tile, written by the next
       // running horizontal sums (origin: segment start xs, tile row y0)
       double h[VAR == VAR_DF ? 4 : 9];
       int hi[VAR == VAR_DF ? 6 : 1];
@@ -684,36 +685,38 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         // one of this segment's window sums outside the window: the row pass's 3 leading
         // columns (their vertical sums of p^2, read back), and with running column sums also
         // the (o - o0) leading rows of the column segment over 2r + 4 columns, each sample
-        // <= the tile's largest p^2.  When that bound exceeds 1024x a lower bound of a fitted
-        // window's own sum of p^2 -- its centre column's vertical sum, which holds the centre
-        // sample itself (empty columns belong to unfitted pixels and are skipped) -- the
-        // residue could exceed what the parity allowances absorb for every conditioning, and
-        // the segment is queued for a direct refit after this kernel (queue_refit /
-        // refit_kernel, rf_direct.cuh / rf_lattice.cu); only depth ratios of ~10x or more
-        // inside one tile's footprint can trigger it.  All of it runs after the unrolled loop
-        // (no register held through the solve), in whole exponent steps on the high words of
-        // the non-negative doubles (they order like the values; the guard needs orders of
-        // magnitude only).
-        const int* vhi = reinterpret_cast<const int*>(vd + (TH + orow) * VRS);  // channel 1, row orow
-        auto col_hi = [&](int c) { return vhi[2 * ((c & 3) * VQ + (c >> 2)) + 1]; };
+        // <= the largest p^2 that has left the tile's column sums (s_dmax).  A lower bound of
+        // a fitted window's own sum of p^2 is its centre column's vertical sum, which holds
+        // the centre sample (columns whose exact valid count is 0 belong to unfitted pixels
+        // and are skipped: their running sums hold nothing but residue).  When the departed
+        // mass exceeds 2^20 x that bound (millimetre depths next to metres; realistic scenes
+        // stay orders of magnitude below: bench.py's configs queue nothing), the segment is
+        // queued for a direct refit after this kernel (queue_refit / refit_kernel,
+        // rf_direct.cuh / rf_lattice.cu).  All of it runs after the unrolled loop (no register
+        // held through the solve), in whole exponent steps on the high words of the
+        // non-negative doubles (they order like the values; orders of magnitude suffice).
+        // column xs + k of this row sits at vbase + (k & 3) VQ + (k >> 2): compile-time offsets
+        // from one base (xs is a multiple of 4)
+        const int* vhi = reinterpret_cast<const int*>(vd + (TH + orow) * VRS + vbase) + 1;  // channel 1
+        const int* cnt = irow + vbase;
+        auto col_hi = [&](int k) { return vhi[2 * ((k & 3) * VQ + (k >> 2))]; };
+        auto col_n = [&](int k) { return cnt[(k & 3) * VQ + (k >> 2)]; };
         // log2 of the departed mass, rounded up: 3 x the largest departed column sum ...
-        int te = (max(col_hi(xs), max(col_hi(xs + 1), col_hi(xs + 2))) >> 20) - 1023 + 2;
-        if (!CENTRED) {  // ... and (o - o0) x (2r + 4) departed samples of the column segment
-          int o0r = 0;
+        int te = (max(col_hi(0), max(col_hi(1), col_hi(2))) >> 20) - 1023 + 2;
+        if (!CENTRED) {  // ... and the (o - o0) x (2r + 4) samples that left the column sums
+          // this row's column segment starts at o0 = floor(p TH / parts), p = its segment
           const int parts = max(1, min(NTHREADS / HW_, TH));
-#pragma unroll 1
-          for (int q = 1; q < parts; ++q)
-            if ((q * TH) / parts <= orow) o0r = (q * TH) / parts;
-          const int rows = (orow - o0r) * (2 * r + KSEG);
-          if (rows > 0) te = max(te, 2 * ((int)(s_pmax[it & 1] >> 20) - 1023) + 32 - __clz(rows)) + 1;
+          const int seg = ((orow + 1) * parts + TH - 1) / TH - 1;
+          const int rows = (orow - (seg * TH) / parts) * (2 * r + KSEG);
+          if (rows > 0) te = max(te, 2 * ((int)(s_dmax[it & 1] >> 20) - 1023) + 32 - __clz(rows)) + 1;
         }
-        te -= 10;  // / 1024
+        te -= 20;  // / 2^20
         const int thr = te < -1022 ? 0 : te > 1023 ? 0x7ff00000 : (te + 1023) << 20;
         int h1min = 0x7fffffff;
 #pragma unroll
         for (int j = 0; j < KSEG; ++j) {
-          const int w = col_hi(xs + j + r);
-          h1min = min(h1min, w > 0 ? w : 0x7fffffff);
+          const int w = col_hi(j + r);
+          h1min = min(h1min, col_n(j + r) > 0 ? w : 0x7fffffff);  // exact valid count
         }
         if (h1min < thr)
           queue_refit(P, frame, gy, gxs, (1u << min(KSEG, P.W - gxs)) - 1u);
@@ -860,10 +863,18 @@ int32_t rf_abi_version(void) { return RF_ABI_VERSION; }
 
 const char* rf_last_error(void) { return g_err; }
 
+int64_t rf_last_refit_segments(const rf_tables* t) {
+  if (!t) return -1;
+  const rf_device_guard guard(t->device);
+  unsigned c[8];
+  if (cudaMemcpy(c, t->fix_ctr, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return (int64_t)c[2] + (int64_t)c[6];  // entries of each space's last refit
+}
+
 int32_t rf_launches_per_call(int32_t formulation_mask) {
-  // one tile kernel per space + one sliding-sum guard refit launch
-  return ((formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) ? 1 : 0) +
-         ((formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) ? 1 : 0) + (formulation_mask ? 1 : 0);
+  // per space: the tile kernel + the sliding-sum guard's refit (programmatic dependent launch)
+  return 2 * (((formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) ? 1 : 0) +
+              ((formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) ? 1 : 0));
 }
 
 rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const double* delta_y,
@@ -914,8 +925,8 @@ rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const
   }
   e = cudaMalloc(&t->tan_x, sizeof(double) * in->width);
   if (e == cudaSuccess) e = cudaMalloc(&t->tan_y, sizeof(double) * in->height);
-  if (e == cudaSuccess) e = cudaMalloc(&t->fix_ctr, sizeof(unsigned) * 4);
-  if (e == cudaSuccess) e = cudaMemset(t->fix_ctr, 0, sizeof(unsigned) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&t->fix_ctr, sizeof(unsigned) * 8);
+  if (e == cudaSuccess) e = cudaMemset(t->fix_ctr, 0, sizeof(unsigned) * 8);
   if (e == cudaSuccess) e = cudaMalloc(&t->fix_list, sizeof(unsigned long long) * 2 * RF_FIX_CAP);
   if (e == cudaSuccess) {
     const int m = in->width > in->height ? in->width : in->height;
@@ -1009,8 +1020,6 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
       fork_lock.unlock();
     }
   }
-  KParams PP[2];
-  memset(PP, 0, sizeof(PP));
   for (int var = 0; var < 2; ++var) {
     const int fi = var == VAR_STD ? RF_FORM_IMPLICIT_STANDARD : RF_FORM_IMPLICIT_RGBD;
     const int fe = var == VAR_STD ? RF_FORM_EXPLICIT_STANDARD : RF_FORM_EXPLICIT_RGBD;
@@ -1036,7 +1045,7 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     if (di) P.imp = OutPlanes{outs[fi].normal, outs[fi].offset, outs[fi].residual, outs[fi].curvature, outs[fi].status};
     if (de) P.exp = OutPlanes{outs[fe].normal, outs[fe].offset, outs[fe].residual, outs[fe].curvature, outs[fe].status};
     P.batch = batch;
-    P.fix_ctr = t->fix_ctr + (var == VAR_STD ? 0 : 2);
+    P.fix_ctr = t->fix_ctr + (var == VAR_STD ? 0 : 4);
     P.fix_list = t->fix_list + (size_t)var * RF_FIX_CAP;
     P.fix_cap = RF_FIX_CAP;
     const size_t sm = smem_bytes(var, r, tma, esz, de);
@@ -1048,7 +1057,7 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
       e = tma ? launch_radius<VAR_STD>(P, tmap, sm, tiles, ls) : launch_var<VAR_STD, false, 0>(P, tmap, sm, tiles, ls);
     else
       e = tma ? launch_radius<VAR_DF>(P, tmap, sm, tiles, ls) : launch_var<VAR_DF, false, 0>(P, tmap, sm, tiles, ls);
-    PP[var] = P;
+    if (e == cudaSuccess) e = launch_refit(var, P, t->lat_x, t->lat_y, ls);
     if (e != cudaSuccess) {
       if (fork) {  // keep the caller's stream joined even on failure
         cudaEventRecord(fs->join, fs->aux);
@@ -1061,8 +1070,6 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     cudaEventRecord(fs->join, fs->aux);
     cudaStreamWaitEvent(s, fs->join, 0);
   }
-  const cudaError_t e = launch_refit(PP[VAR_STD], PP[VAR_DF], t->lat_x, t->lat_y, t->fix_ctr, s);
-  if (e != cudaSuccess) return fail(RF_ERR_CUDA, "refit launch: %s", cudaGetErrorString(e));
   return RF_OK;
 }
 

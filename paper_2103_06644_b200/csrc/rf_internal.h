@@ -12,9 +12,9 @@ struct rf_tables {
   // (x + delta_x - cx) / fx and (y + delta_y - cy) / fy, [H][W] device; null when separable
   double* lat_x;
   double* lat_y;
-  // sliding-sum guard worklists (rf_fit.cu row pass), one per space: counters [4] = (standard
-  // entries, refit blocks done, rgbd entries, unused) and RF_FIX_CAP entries per space; reset
-  // by the refit kernel, so fits sharing one tables handle must be ordered on one stream
+  // sliding-sum guard worklists (rf_fit.cu row pass), one per space: counters [2][4] =
+  // (entries, refit blocks done, entries of the last call, unused) and RF_FIX_CAP entries per
+  // space; reset by the refit kernel, so fits sharing one handle must be ordered on one stream
   unsigned* fix_ctr;
   unsigned long long* fix_list;
 };

@@ -60,8 +60,10 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
   const int tid = threadIdx.x;
   const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;
   const int64_t total = (int64_t)ntx * nty * P.batch;
-  __shared__ unsigned int s_qmax[2];  // sliding-sum guard (fit_tile_kernel): high word of max |q_i|
-  if (tid == 0) s_qmax[0] = s_qmax[1] = 0u;
+  // high word of the largest |q_i| that has left the tile's column sums, double-buffered by
+  // tile parity (the sliding-sum guard, fit_tile_kernel)
+  __shared__ unsigned s_dmax[2];
+  if (tid == 0) s_dmax[0] = s_dmax[1] = 0u;
   __syncthreads();
   int it = 0;
   for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
 
     // ---- column sums (running, over row segments; all threads busy)
     const int parts = max(1, min(NTHREADS / HW_, TH));
-    unsigned int qm = 0u;
+    int dm = 0;
     {
       const int col = tid % HW_, part = tid / HW_;
       if (part < parts) {
@@ -113,9 +115,9 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
           double q0, q1, q2;
           if (!qof(y0 - r + ii, x, q0, q1, q2)) return;
           const double s0 = sg * q0, s1 = sg * q1, s2 = sg * q2;
-          if (sg > 0.0)
-            qm = max(qm, max((unsigned)__double2hiint(q0) & 0x7fffffffu,
-                             max((unsigned)__double2hiint(q1) & 0x7fffffffu, (unsigned)__double2hiint(q2) & 0x7fffffffu)));
+          if (sg < 0.0)
+            dm = max(dm, max(__double2hiint(q0) & 0x7fffffff,
+                             max(__double2hiint(q1) & 0x7fffffff, __double2hiint(q2) & 0x7fffffff)));
           a[0] += s0;
           a[1] += s1;
           a[2] += s2;
@@ -139,8 +141,8 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
       }
     }
     {
-      const unsigned int b = __reduce_max_sync(0xffffffffu, qm);
-      if ((tid & 31) == 0 && b) atomicMax(&s_qmax[it & 1], b);
+      const unsigned b = __reduce_max_sync(0xffffffffu, (unsigned)dm);  // dm >= 0
+      if ((tid & 31) == 0) atomicMax(&s_dmax[it & 1], b);
     }
     __syncthreads();
 
@@ -166,13 +168,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
         };
         for (int k = 0; k <= 2 * r; ++k) accum(k, 1.0);
         const float qn = __int_as_float(0x7fc00000);
-        if (tid == 0) s_qmax[(it + 1) & 1] = 0u;
-        const float qmax = (float)__hiloint2double((int)s_qmax[it & 1], -1);
-        int o0r = 0;
-#pragma unroll 1
-        for (int q = 1; q < parts; ++q)
-          if ((q * TH) / parts <= orow) o0r = (q * TH) / parts;
-        unsigned bad = 0u;  // pixels the sliding-sum guard sends to the direct refit
+        if (tid == 0) s_dmax[(it + 1) & 1] = 0u;  // read by the previous tile, written by the next
         for (int j = 0; j < KSEG; ++j) {
           if (j > 0) {
             accum(j + 2 * r, 1.0);
@@ -186,10 +182,6 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
           float nx = qn, ny = qn, nz = qn, off = qn, res = qn, cur = qn;
           float ex = qn, ey = qn, ez = qn, eo = qn, eres = qn, ecur = qn;
           if (vbit && hc >= (EXP ? 3 : 4)) {
-            const int dep = (orow - o0r) * (2 * r + 1 + j) + j * (2 * r + 1);
-            if (dep && max(__double2hiint(h[3]), max(__double2hiint(h[6]), __double2hiint(h[8]))) <
-                           __double2hiint((double)(qmax * qmax * (float)dep * 0.0009765625f)))
-              bad |= 1u << j;
             QMoments m;
             m.n = (double)hc;
             m.s0 = h[0]; m.s1 = h[1]; m.s2 = h[2];
@@ -223,19 +215,44 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
           if (P.do_imp) store_fit(P.imp, p, nx, ny, nz, off, res, cur, st);
           if (EXP && P.do_exp) store_fit(P.exp, p, ex, ey, ez, eo, eres, ecur, stx);
         }
-        if (bad) queue_refit(P, frame, gy, gxs, bad);
+        {
+          // sliding-sum guard (fit_tile_kernel, rf_fit.cu): departed mass of the segment's
+          // window sums -- 3 leading columns' sums of q_i^2 and the (o - o0) x (2r + 4)
+          // samples that left the column sums (each <= 3 x the tile's largest departed |q_i|^2) --
+          // against each window's centre-column sums, in exponent steps on high words
+          auto colq = [&](int c) {  // largest high word of the column's sums of q0^2, q1^2, q2^2
+            const int cp = (c & 3) * VQ + (c >> 2);
+            const int* w = reinterpret_cast<const int*>(vrow + cp);
+            return max(w[2 * 3 * vstride + 1], max(w[2 * 6 * vstride + 1], w[2 * 8 * vstride + 1]));
+          };
+          int te = (max(colq(xs), max(colq(xs + 1), colq(xs + 2))) >> 20) - 1023 + 4;  // x 9
+          const int seg = ((orow + 1) * parts + TH - 1) / TH - 1;
+          const int rows = (orow - (seg * TH) / parts) * (2 * r + KSEG);
+          if (rows > 0) te = max(te, 2 * ((int)(s_dmax[it & 1] >> 20) - 1023) + 2 + 32 - __clz(rows)) + 1;
+          te -= 20;  // / 2^20
+          const int thr = te < -1022 ? 0 : te > 1023 ? 0x7ff00000 : (te + 1023) << 20;
+          int wmin = 0x7fffffff;
+          for (int j = 0; j < KSEG; ++j) {
+            const int c = xs + j + r;
+            wmin = min(wmin, crow[(c & 3) * VQ + (c >> 2)] > 0 ? colq(c) : 0x7fffffff);  // exact count
+          }
+          if (wmin < thr) queue_refit(P, frame, gy, gxs, (1u << min(KSEG, P.W - gxs)) - 1u);
+        }
       }
     }
     __syncthreads();  // vd / vc are rewritten by the next tile
   }
 }
 
-// Sliding-sum guard refit (rf_direct.cuh), both spaces of one rf_fit_pixels call in one
-// launch: one thread per queued (entry, pixel bit); on worklist overflow every pixel of the
-// space.  The last block to finish resets both spaces' counters, so the next call on the
-// stream starts from empty lists.
+// Sliding-sum guard refit (rf_direct.cuh) of one space: one thread per queued (entry, pixel
+// bit); on worklist overflow every pixel of the launch.  Launched right behind the space's
+// tile kernel on the same stream as a programmatic dependent launch: its blocks are resident
+// while the tile kernel drains and wait (griddepcontrol.wait) for its completion, so an empty
+// list costs about a kernel's exit, not a launch.  The last block to finish resets the
+// counters (P.fix_ctr: entries, blocks done, entries of the last call).
 template <int VAR, bool EXP>
-__device__ __forceinline__ void refit_space(const KParams& P, const double* lat_x, const double* lat_y) {
+__global__ void __launch_bounds__(128) refit_kernel(const KParams P, const double* lat_x, const double* lat_y) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const unsigned n = P.fix_ctr[0];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -246,34 +263,41 @@ __device__ __forceinline__ void refit_space(const KParams& P, const double* lat_
       const int y = rem / P.W;
       fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, y, rem - y * P.W);
     }
-    return;
+  } else {
+    for (int64_t i = i0; i < 4 * (int64_t)n; i += stride) {
+      const unsigned long long e = P.fix_list[i >> 2];
+      const int bit = (int)(i & 3);
+      if (!((e >> bit) & 1ull)) continue;
+      const int64_t p = (int64_t)(e >> 4);
+      const int64_t frame = p / P.out_frame;
+      const int rem = (int)(p - frame * P.out_frame);
+      const int y = rem / P.W;
+      fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, y, rem - y * P.W + bit);
+    }
   }
-  for (int64_t i = i0; i < 4 * (int64_t)n; i += stride) {
-    const unsigned long long e = P.fix_list[i >> 2];
-    const int bit = (int)(i & 3);
-    if (!((e >> bit) & 1ull)) continue;
-    const int64_t p = (int64_t)(e >> 4);
-    const int64_t frame = p / P.out_frame;
-    const int rem = (int)(p - frame * P.out_frame);
-    const int y = rem / P.W;
-    fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, y, rem - y * P.W + bit);
-  }
-}
-
-template <bool EXP_STD, bool EXP_DF>
-__global__ void __launch_bounds__(128) refit_kernel(const KParams Ps, const KParams Pd, const double* lat_x,
-                                                    const double* lat_y, unsigned* ctr) {
-  if (Ps.fix_ctr) refit_space<VAR_STD, EXP_STD>(Ps, lat_x, lat_y);
-  if (Pd.fix_ctr) refit_space<VAR_DF, EXP_DF>(Pd, lat_x, lat_y);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {  // ctr: [std entries, blocks done, df entries, unused]
-      ctr[0] = 0u;
-      ctr[1] = 0u;
-      ctr[2] = 0u;
+    if (atomicAdd(P.fix_ctr + 1, 1u) == gridDim.x - 1) {
+      P.fix_ctr[2] = n;
+      P.fix_ctr[0] = 0u;
+      P.fix_ctr[1] = 0u;
     }
   }
+}
+
+template <int VAR, bool EXP>
+cudaError_t launch_refit_pdl(const KParams& P, const double* lat_x, const double* lat_y, int blocks, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, refit_kernel<VAR, EXP>, P, lat_x, lat_y);
 }
 
 template <int VAR>
@@ -306,18 +330,13 @@ cudaError_t launch_lattice_var(const KParams& P, const double* lat_x, const doub
 }  // namespace
 
 namespace rf_tile {
-cudaError_t launch_refit(const KParams& Ps, const KParams& Pd, const double* lat_x, const double* lat_y,
-                         unsigned* ctr, cudaStream_t s) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool es = Ps.do_exp, ed = Pd.do_exp;
-  sms = sms < 32 ? sms : 32;  // usually an empty list: keep the launch small
-  if (es && ed) refit_kernel<true, true><<<sms, 128, 0, s>>>(Ps, Pd, lat_x, lat_y, ctr);
-  else if (es) refit_kernel<true, false><<<sms, 128, 0, s>>>(Ps, Pd, lat_x, lat_y, ctr);
-  else if (ed) refit_kernel<false, true><<<sms, 128, 0, s>>>(Ps, Pd, lat_x, lat_y, ctr);
-  else refit_kernel<false, false><<<sms, 128, 0, s>>>(Ps, Pd, lat_x, lat_y, ctr);
-  return cudaGetLastError();
+cudaError_t launch_refit(int var, const KParams& P, const double* lat_x, const double* lat_y, cudaStream_t s) {
+  const int blocks = 16;  // usually an empty list: a small launch
+  if (var == VAR_STD)
+    return P.do_exp ? launch_refit_pdl<VAR_STD, true>(P, lat_x, lat_y, blocks, s)
+                    : launch_refit_pdl<VAR_STD, false>(P, lat_x, lat_y, blocks, s);
+  return P.do_exp ? launch_refit_pdl<VAR_DF, true>(P, lat_x, lat_y, blocks, s)
+                  : launch_refit_pdl<VAR_DF, false>(P, lat_x, lat_y, blocks, s);
 }
 
 cudaError_t launch_lattice(int var, const KParams& P, const double* lat_x, const double* lat_y,

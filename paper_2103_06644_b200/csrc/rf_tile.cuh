@@ -82,11 +82,10 @@ __device__ __forceinline__ TileGeom tile_of(int64_t t, int ntx, int nty) {
 }
 
 // launch the per-pixel fits of one space on cameras with distortion lattices (rf_lattice.cu)
-// direct refit of the pixels the tile kernels' sliding-sum guard appended to the spaces'
-// worklists (one small launch after both tile kernels of a call; resets the worklists).
-// A space not computed by the call has a zeroed KParams (null fix_ctr).
-cudaError_t launch_refit(const KParams& Ps, const KParams& Pd, const double* lat_x, const double* lat_y,
-                         unsigned* ctr, cudaStream_t s);
+// direct refit of the pixels the tile kernel's sliding-sum guard appended to P.fix_list: a
+// small programmatic dependent launch right behind the tile kernel, same stream; resets the
+// worklist
+cudaError_t launch_refit(int var, const KParams& P, const double* lat_x, const double* lat_y, cudaStream_t s);
 cudaError_t launch_lattice(int var, const KParams& P, const double* lat_x, const double* lat_y,
                            cudaStream_t s);
 

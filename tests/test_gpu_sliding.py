@@ -28,13 +28,18 @@ W, H = 64, 48
 
 
 def _scene(far: float, near: float) -> np.ndarray:
-    """Rows 0..15 and a block at `far`; isolated `near` samples and a small `near` patch below."""
+    """Rows 0..15 and blocks at `far`; isolated `near` samples, a small `near` patch, and a
+    far-to-near step inside one row segment."""
     z = np.zeros((H, W))
     z[:16, :] = far
     z[25:40, 44:50] = far
     for (y, x) in [(31, 30), (35, 25), (44, 40), (27, 36), (20, 20), (30, 3), (31, 6), (33, 60)]:
         z[y, x] = near
     z[31:34, 52:58] = near
+    # a step inside one 4-pixel row segment (segments start at multiples of 4): far columns
+    # that the row pass slides past, then near pixels whose windows hold only near samples
+    z[40:47, 13:16] = far
+    z[40:47, 16:21] = near
     return z
 
 
@@ -72,9 +77,22 @@ def test_sliding_residue(distort, window, dtype, far, near):
     sel = _single_class(z, window, far)
     assert sel.sum() > 100
     out = rf.fit_pixels(torch.from_numpy(z).cuda(), maps, window, rf.FORMULATIONS)
-    torch.cuda.synchronize()
+    assert rf.last_refit_segments(maps) > 0  # the guard found the millimetre windows
     for form in rf.FORMULATIONS:
         ref = oracle_frame(torch.from_numpy(z), cam, window, form)
         m = compare(_subset(gpu_flat(out[form]), sel), _subset(ref, sel), explicit_fit=form.startswith("explicit"))
         assert m["ok"], f"{form} " + " ".join(f"{k}={m[k]:.3g}" for k in (
             "compared", "status_mismatch", "max_normal_rad", "max_residual_rel", "max_curvature_rel"))
+
+
+@pytest.mark.parametrize("config,window", [("C1", 5), ("C2", 11), ("C3", 9), ("C4", 15), ("C5", 31)])
+def test_guard_quiet_on_scenes(config, window):
+    """The BASELINE scene generator (planes over 0.3-20 m, noise, holes) queues (almost) no
+    refits: the guard's 2^20 margin sits far above realistic depth ratios."""
+    from paper_2103_06644_b200 import scenes
+    cfg = scenes.CONFIGS[config]
+    depth = scenes.render_batch(cfg, frames=1, device="cuda")
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(cfg.f, cfg.f, cfg.cx, cfg.cy, cfg.width, cfg.height))
+    rf.fit_pixels(depth, maps, window, rf.PIXEL_FORMULATIONS)
+    segments = cfg.width * cfg.height // 4
+    assert rf.last_refit_segments(maps) <= segments // 100000 + 4
