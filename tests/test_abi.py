@@ -19,7 +19,7 @@ HEADER = ROOT / "include" / "rangefit_b200.h"
 
 def header_functions():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:rf_status|int32_t|const char\*)\s+(rf_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:rf_status|int32_t|int64_t|const char\*)\s+(rf_\w+)\(", text, re.M)))
 
 
 def test_header_and_binding_agree():
