@@ -9,7 +9,10 @@
 namespace rf_tile {
 
 constexpr int TW = 64;       // output tile width  (pixels)
-constexpr int TH = 16;       // output tile height (pixels)
+#ifndef RF_TH
+#define RF_TH 16
+#endif
+constexpr int TH = RF_TH;    // output tile height (pixels)
 constexpr int KSEG = 4;      // consecutive output pixels per thread
 constexpr int NTHREADS = (TW / KSEG) * TH;  // 256
 constexpr int MAX_RADIUS = 32;
@@ -73,9 +76,19 @@ struct TileGeom {
 __device__ __forceinline__ TileGeom tile_of(int64_t t, int ntx, int nty) {
   TileGeom g;
   const int64_t per_frame = (int64_t)ntx * nty;
-  g.frame = t / per_frame;
-  const int rem = (int)(t - g.frame * per_frame);
-  const int ty = rem / ntx;
+  int rem;
+  if ((uint64_t)t <= 0xffffffffull && per_frame <= 0xffffffffll) {
+    // every BASELINE batch (C4: 2.1 M tiles): 32-bit division, not the 64-bit routine that
+    // all threads would otherwise run once per tile
+    const unsigned tt = (unsigned)t, pf = (unsigned)per_frame;
+    const unsigned f = tt / pf;
+    g.frame = f;
+    rem = (int)(tt - f * pf);
+  } else {
+    g.frame = t / per_frame;
+    rem = (int)(t - g.frame * per_frame);
+  }
+  const int ty = (int)((unsigned)rem / (unsigned)ntx);
   g.y0 = ty * TH;
   g.x0 = (rem - ty * ntx) * TW;
   return g;
