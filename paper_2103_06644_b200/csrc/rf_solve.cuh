@@ -357,7 +357,10 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
 #pragma unroll
   for (int it = 0; it < 2; ++it) {
     l -= newton(l);
-    cs.x = curv_newton(t, c1, det, cs.x);
+    // one step suffices for the curvature: outside the close (< 5% gap) cases, which
+    // take curvature_slow, the fp32 seed is within ~1e-4 and one quadratic step leaves
+    // < 1e-6 relative
+    if (it == 0) cs.x = curv_newton(t, c1, det, cs.x);
   }
   if (!tie) {
     if (grel > 1e-4f) l -= newton(l);
@@ -438,11 +441,12 @@ __device__ __forceinline__ void finish_plane(double a, double b, double c, doubl
   const double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023 - e)
   const float fa = (float)(a * sc), fb = (float)(b * sc), fc = (float)(c * sc),
               fd = (float)(d * sc);
-  const float n4 = frsqrt(fa * fa + fb * fb + fc * fc + fd * fd);
+  // |u_k| / |u| > 1e-9 on the unit 4-vector, squared (no reciprocal square root)
+  const float e4 = 1e-18f * (fa * fa + fb * fb + fc * fc + fd * fd);
   float sign = 1.0f;
-  if (fabsf(fc * n4) > 1e-9f) sign = fc > 0.0f ? 1.0f : -1.0f;
-  else if (fabsf(fb * n4) > 1e-9f) sign = fb > 0.0f ? 1.0f : -1.0f;
-  else if (fabsf(fa * n4) > 1e-9f) sign = fa > 0.0f ? 1.0f : -1.0f;
+  if (fc * fc > e4) sign = fc > 0.0f ? 1.0f : -1.0f;
+  else if (fb * fb > e4) sign = fb > 0.0f ? 1.0f : -1.0f;
+  else if (fa * fa > e4) sign = fa > 0.0f ? 1.0f : -1.0f;
   else if (fd < 0.0f) sign = -1.0f;
   const float in3 = sign * frsqrt(fa * fa + fb * fb + fc * fc);
   nx = fa * in3;
