@@ -373,7 +373,15 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
   }
 
   // eigenvector: dominant column of adj(C - lam B), B = I + beta mu mu^T
-  const double beta = n * rcp_fast(n - lam);
+  // beta = n / (n - lam) = 1 + lam / (n - lam): one Newton step on the reciprocal
+  // (~1e-12 relative) is far below what the lam * beta terms need
+  double beta;
+  {
+    const double dn = n - lam;
+    double r = rcp_approx(dn);
+    r = fma(r, fma(-dn, r, 1.0), r);
+    beta = fma(lam, r, 1.0);
+  }
   const double gam = lam * beta;
   const double E00 = c00 - lam - gam * m0 * m0;
   const double E11 = c11 - lam - gam * m1 * m1;
@@ -381,25 +389,22 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
   const double E01 = c01 - gam * m0 * m1;
   const double E02 = c02 - gam * m0 * m2;
   const double E12 = c12 - gam * m1 * m2;
+  // the six cofactors of the symmetric E; the column with the largest diagonal is taken
+  // by selects (no branches)
   const double B00 = E11 * E22 - E12 * E12;
   const double B11 = E00 * E22 - E02 * E02;
   const double B22 = E00 * E11 - E01 * E01;
+  const double B01 = E02 * E12 - E01 * E22;
+  const double B02 = E01 * E12 - E02 * E11;
+  const double B12 = E01 * E02 - E00 * E12;
   double u0, u1, u2;
   {
     const double a0 = fabs(B00), a1 = fabs(B11), a2 = fabs(B22);
-    if (a0 >= a1 && a0 >= a2) {
-      u0 = B00;
-      u1 = E02 * E12 - E01 * E22;
-      u2 = E01 * E12 - E02 * E11;
-    } else if (a1 >= a2) {
-      u0 = E02 * E12 - E01 * E22;
-      u1 = B11;
-      u2 = E01 * E02 - E00 * E12;
-    } else {
-      u0 = E01 * E12 - E02 * E11;
-      u1 = E01 * E02 - E00 * E12;
-      u2 = B22;
-    }
+    const bool s0 = a0 >= a1 && a0 >= a2;
+    const bool s1 = !s0 && a1 >= a2;
+    u0 = s0 ? B00 : s1 ? B01 : B02;
+    u1 = s0 ? B01 : s1 ? B11 : B12;
+    u2 = s0 ? B02 : s1 ? B12 : B22;
     if (a0 == 0.0 && a1 == 0.0 && a2 == 0.0) {  // rank <= 1: any null vector
       u0 = 0.0;
       u1 = 0.0;
