@@ -155,7 +155,7 @@ __device__ __forceinline__ CurvSeed curv_seed(float k1, float k2, float k3) {
   c.top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
   c.fast = !c.top && (k2 - k1) >= 0.2f * k2;
   c.close = c.top ? (k3 - k2) < 0.05f * k3 : (k2 - k1) < 0.05f * k2;
-  c.x = c.top ? (double)k3 : (double)k1 * (1.0 - 1e-5);
+  c.x = (double)(c.top ? k3 : k1 * (1.0f - 1e-5f));  // one conversion
   return c;
 }
 __device__ __forceinline__ double curv_newton(double t, double c1, double det, double x) {
@@ -405,7 +405,8 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     u0 = s0 ? B00 : s1 ? B01 : B02;
     u1 = s0 ? B01 : s1 ? B11 : B12;
     u2 = s0 ? B02 : s1 ? B12 : B22;
-    if (a0 == 0.0 && a1 == 0.0 && a2 == 0.0) {  // rank <= 1: any null vector
+    const double amax = s0 ? a0 : s1 ? a1 : a2;
+    if (amax == 0.0) {  // all diagonal cofactors 0, rank <= 1: any null vector
       u0 = 0.0;
       u1 = 0.0;
       u2 = 1.0;
