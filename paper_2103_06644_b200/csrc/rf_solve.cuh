@@ -139,22 +139,26 @@ static __device__ __noinline__ float curvature_slow(double t, double c1, double 
 }
 
 // Curvature in three pieces so that solve_window can interleave the curvature Newton
-// steps with its own (independent chains, half the latency):
-//  * curv_seed: fast exit (well separated bottom pair: the fp32 seed, deflated, ~2e-6
-//    relative, meets the 1e-4 tolerance), the rare all-close case, and the Newton start.
-//    Common in the standard form (depth noise dominates: lam_max >> lam_2 ~ lam_min): two
-//    fp64 Newton steps on det(C - l I) on lam_max from its seed when the top gap is the
-//    better separated one (then deflate: lam_1 + lam_2 = t - lam_max, lam_1 lam_2 =
-//    det / lam_max), else on lam_min from below.
+// step with its own (independent chains, half the latency):
+//  * curv_seed: the Newton start -- lam_min from just below its fp32 seed when the bottom
+//    pair is >= 5% apart (nearly every window), else lam_max (then deflate: lam_1 + lam_2 =
+//    t - lam_max, lam_1 lam_2 = det / lam_max); both pairs close: out of line;
+//  * curv_newton: one fp64 Newton step on det(C - l I);
+//  * curv_finish: the ratio, the deflation, or the out-of-line path.
 struct CurvSeed {
-  bool top, fast, close;
+  bool top, close, slow_top;
   double x;
 };
 __device__ __forceinline__ CurvSeed curv_seed(float k1, float k2, float k3) {
   CurvSeed c;
-  c.top = (k3 - k2) * k2 > (k2 - k1) * k3;  // top gap better separated
-  c.fast = !c.top && (k2 - k1) >= 0.2f * k2;
-  c.close = c.top ? (k3 - k2) < 0.05f * k3 : (k2 - k1) < 0.05f * k2;
+  // bottom pair separated by >= 5%: Newton on lam_min from just below the fp32 seed
+  // (seed error <~ 1e-4, one step leaves < 1e-6 relative); otherwise Newton on lam_max
+  // and deflation; both pairs close: out of line (curvature_slow)
+  const bool bclose = (k2 - k1) < 0.05f * k2;
+  const bool tclose = (k3 - k2) < 0.05f * k3;
+  c.top = bclose;
+  c.close = bclose && tclose;
+  c.slow_top = (k3 - k2) * k2 > (k2 - k1) * k3;  // the better separated side
   c.x = (double)(c.top ? k3 : k1 * (1.0f - 1e-5f));  // one conversion
   return c;
 }
@@ -165,8 +169,7 @@ __device__ __forceinline__ double curv_newton(double t, double c1, double det, d
 }
 __device__ __forceinline__ float curv_finish(const CurvSeed& c, double t, double c1, double det, float ft,
                                              float k1, float k2, float k3) {
-  if (c.fast) return t > 0.0 ? k1 * frcp(ft) : 0.0f;
-  if (c.close) return curvature_slow(t, c1, det, ft, k1, k2, k3, c.top);  // out of line, rare
+  if (c.close) return curvature_slow(t, c1, det, ft, k1, k2, k3, c.slow_top);  // out of line, rare
   float kmin = (float)c.x;
   if (c.top) {
     const double S = t - c.x;
@@ -180,7 +183,7 @@ __device__ __forceinline__ float curv_finish(const CurvSeed& c, double t, double
 __device__ __forceinline__ float curvature_from(double t, double c1, double det, float ft, float k1,
                                                 float k2, float k3) {
   CurvSeed c = curv_seed(k1, k2, k3);
-  if (!c.fast && !c.close) {
+  if (!c.close) {
     c.x = curv_newton(t, c1, det, c.x);
     c.x = curv_newton(t, c1, det, c.x);
   }
