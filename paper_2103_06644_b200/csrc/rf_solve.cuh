@@ -303,6 +303,7 @@ static __device__ __noinline__ void tie_deflation(double q3, double q2, double q
 // dominant column of adj(C - lam (I + beta mu mu^T)).
 // Curvature lam_min(C)/tr(C) uses the same seeds/Newton/
 // deflation on det(C - l I).
+template <bool MID_SEED = false>
 __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1, double m2,
                                              double n, WindowFit& out) {
   const double c00 = C.c00, c01 = C.c01, c02 = C.c02, c11 = C.c11, c12 = C.c12, c22 = C.c22;
@@ -356,14 +357,26 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
     return G * rcp_approx(dG);
   };
   CurvSeed cs = curv_seed(k1, k2, k3);
-  double l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
+  double l;
+  if constexpr (MID_SEED) {
+    // seed at the middle of [g1 (1 - g1/n), g1]: error <= grel/2 + the fp32 seed error, so
+    // one step leaves < 1e-7 relative for grel <= 1e-5 (every disparity-form window of the
+    // BASELINE scenes up to C3); the standard form's larger lam/n would make the second
+    // step a warp-divergent branch, so it keeps the two-step form below
+    l = (double)(g1 * fmaf(-0.5f, grel, 1.0f));
     l -= newton(l);
-    // one step suffices for the curvature: outside the close (< 5% gap) cases, which
-    // take curvature_slow, the fp32 seed is within ~1e-4 and one quadratic step leaves
-    // < 1e-6 relative
-    if (it == 0) cs.x = curv_newton(t, c1, det, cs.x);
+    cs.x = curv_newton(t, c1, det, cs.x);
+    if (grel > 1e-5f) l -= newton(l);
+  } else {
+    l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      l -= newton(l);
+      // one step suffices for the curvature: outside the close (< 5% gap) cases, which
+      // take curvature_slow, the fp32 seed is within ~1e-4 and one quadratic step leaves
+      // < 1e-6 relative
+      if (it == 0) cs.x = curv_newton(t, c1, det, cs.x);
+    }
   }
   if (!tie) {
     if (grel > 1e-4f) l -= newton(l);
