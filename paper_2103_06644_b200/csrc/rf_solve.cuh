@@ -224,7 +224,10 @@ __device__ __forceinline__ void explicit_solve(const Sym3& C, double m0, double 
   out.a = fma(C.c11, C.c02, -C.c01 * C.c12) * idet;
   out.b = fma(C.c00, C.c12, -C.c01 * C.c02) * idet;
   out.c = m2 - out.a * m0 - out.b * m1;
-  out.ss = C.c22 - (out.a * C.c02 + out.b * C.c12);
+  // three samples (MIN_SAMPLES of the explicit fits): the plane interpolates them, the residual
+  // is exactly 0 -- the centred difference below would only return the cancellation of an
+  // ill-conditioned 2x2 solve (e.g. nearly collinear X-Y positions)
+  out.ss = n == 3.0 ? 0.0 : C.c22 - (out.a * C.c02 + out.b * C.c12);
   // uncentred matrix and its Cholesky pivots
   const double M00 = fma(n * m0, m0, C.c00), M01 = fma(n * m0, m1, C.c01), M11 = fma(n * m1, m1, C.c11);
   const double M02 = n * m0, M12 = n * m1;
