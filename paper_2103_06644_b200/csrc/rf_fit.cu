@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
           f.lam = C.c00 + C.c11; f.u0 = mu0 + C.c01; f.u1 = mu1 + C.c02; f.u2 = mu2 + C.c12; f.s = C.c22;
           f.kappa = 0.1f; f.degenerate = false;
 #else
-          solve_window<VAR == VAR_DF>(C, mu0, mu1, mu2, nd, f);
+          solve_window<true>(C, mu0, mu1, mu2, nd, f);
 #endif
 #if RF_ABLATE >= 2
           nx = (float)f.u0; ny = (float)f.u1; nz = (float)f.u2; off = (float)f.s;

@@ -363,13 +363,12 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
   double l;
   if constexpr (MID_SEED) {
     // seed at the middle of [g1 (1 - g1/n), g1]: error <= grel/2 + the fp32 seed error, so
-    // one step leaves < 1e-7 relative for grel <= 1e-5 (every disparity-form window of the
-    // BASELINE scenes up to C3); the standard form's larger lam/n would make the second
-    // step a warp-divergent branch, so it keeps the two-step form below
+    // one step leaves e^2 / gap < 1e-7 relative for grel <= 1e-4 (99% of the C2 windows of
+    // both forms); above, two more steps (and iteration to convergence beyond 1e-3) follow
     l = (double)(g1 * fmaf(-0.5f, grel, 1.0f));
     l -= newton(l);
     cs.x = curv_newton(t, c1, det, cs.x);
-    if (grel > 1e-5f) l -= newton(l);
+    if (grel > 1e-4f) l -= newton(l);
   } else {
     l = (double)(g1 * fmaf(-1.0f, grel, 1.0f - 1e-4f));
 #pragma unroll
