@@ -109,10 +109,8 @@ rf_status rf_tables_destroy(rf_tables* tables);
  * (DepthImage(values, valid=mask), synth.py:88-94) or NULL.  outs: array of
  * RF_NUM_FORMULATIONS output sets indexed by RF_FORM_*; only the requested entries
  * are read.  The implicit and explicit fits of one space share one kernel launch
- * (one pass over the window moments); one more small launch per call refits, from direct
- * window sums, the rare windows whose running sums carried residue from far larger
- * departed samples.  That worklist lives in the tables handle: calls sharing one handle
- * must be ordered on one stream (use one handle per concurrent stream).
+ * (one pass over the window moments).  The tables are immutable: any number of streams may
+ * share one handle concurrently.
  * stream: a cudaStream_t (NULL = legacy default). */
 rf_status rf_fit_pixels(const rf_tables* tables, const void* depth, int dtype, int64_t batch,
                         int32_t height, int32_t width, int64_t row_pitch, const uint8_t* mask,
@@ -159,13 +157,8 @@ rf_status rf_max_residuals(const rf_tables* tables, const void* depth, int dtype
                            double* out, void* stream);
 
 /* Number of kernel launches rf_fit_pixels issues for a given formulation mask (one tile
- * kernel per space plus the refit launch). */
+ * kernel per space). */
 int32_t rf_launches_per_call(int32_t formulation_mask);
-
-/* Diagnostics: 4-pixel segments the last completed rf_fit_pixels call on these tables
- * refit from direct window sums (the sliding-sum guard); synchronises
- * the device.  -1 on error. */
-int64_t rf_last_refit_segments(const rf_tables* tables);
 
 /* Thread-local message describing the last non-RF_OK status. */
 const char* rf_last_error(void);

@@ -65,7 +65,6 @@ EXPORTED_SYMBOLS = (
     "rf_render_planes",
     "rf_max_residuals",
     "rf_launches_per_call",
-    "rf_last_refit_segments",
     "rf_last_error",
     "rf_abi_version",
 )
@@ -143,8 +142,6 @@ def load() -> ctypes.CDLL:
     L.rf_max_residuals.restype = ctypes.c_int
     L.rf_launches_per_call.argtypes = [ctypes.c_int32]
     L.rf_launches_per_call.restype = ctypes.c_int32
-    L.rf_last_refit_segments.argtypes = [ctypes.c_void_p]
-    L.rf_last_refit_segments.restype = ctypes.c_int64
     L.rf_last_error.argtypes = []
     L.rf_last_error.restype = ctypes.c_char_p
     L.rf_abi_version.argtypes = []

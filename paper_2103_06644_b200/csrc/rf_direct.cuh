@@ -1,6 +1,6 @@
 // rf_direct.cuh -- one output pixel fitted from its window summed directly (no sliding
-// sums): the distortion-lattice fallback kernel's body (rf_lattice.cu) and the tile
-// kernels' sliding-sum guard fix-up (rf_fit.cu / rf_lattice.cu).  Window moments are
+// sums): the distortion-lattice fallback kernel's body and the lattice tile kernel's
+// sliding-sum guard fix-up (rf_lattice.cu).  Window moments are
 // fp64 q-moments relative to the pixel's own tan values (rf_general.cuh), then the same
 // solve / canonical output as the tile kernels (rf_solve.cuh).
 #pragma once
@@ -102,16 +102,6 @@ __device__ __forceinline__ void fit_pixel_direct(const rf_tile::KParams& P, cons
   }
   if (P.do_imp) store_fit(P.imp, p, nx, ny, nz, off, res, cur, st);
   if (EXP && P.do_exp) store_fit(P.exp, p, ex, ey, ez, eo, eres, ecur, stx);
-}
-
-// Sliding-sum guard: queue pixels x + j (bit j of `bits`) of row y for the direct refit
-// launched after the tile kernel (launch_refit).  Beyond the worklist's capacity the count
-// still grows, which tells the refit kernel to refit every pixel of the launch instead.
-__device__ __forceinline__ void queue_refit(const rf_tile::KParams& P, int64_t frame, int y, int x,
-                                            unsigned bits) {
-  const unsigned i = atomicAdd(P.fix_ctr, 1u);
-  if (i < P.fix_cap)
-    P.fix_list[i] = ((unsigned long long)(frame * P.out_frame + (int64_t)y * P.W + x) << 4) | bits;
 }
 
 }  // namespace rf_dev

@@ -41,6 +41,10 @@ namespace {
 using namespace rf_dev;
 using namespace rf_tile;
 
+#ifdef RF_COUNT_SLOW
+__device__ unsigned long long g_slow_count[256];
+#endif
+
 // compile-time radii whose halo tile is not staged as fp64 in shared memory (see NOPRIM)
 __host__ __device__ constexpr bool noprim_radius(int rt) { return rt == 15; }
 
@@ -136,6 +140,211 @@ __device__ __forceinline__ void convert_halo(double* prim, const T* raw, int HW_
   }
 }
 
+// slow-pass queue of one tile (row pass -> slow_pixel): tile-local pixel index, with
+// Q_DIRECT when the window must be re-summed directly (sliding-sum guard)
+constexpr int QCAP = 128;
+constexpr int Q_DIRECT = 0x8000;
+
+// running horizontal sums of one space: fp64 moments and exact integer geometry
+template <int VAR> struct HSums {
+  static constexpr int NH = VAR == VAR_DF ? 4 : 9;
+  static constexpr int NHI = VAR == VAR_DF ? 6 : 1;
+};
+
+// add (sgn = +1) or remove (sgn = -1) one column's vertical sums at offset dx from the
+// horizontal origin: disparity form w, w^2, dy w (fp64) and the valid count, dy, dy^2
+// (int); standard form Z, Z^2, dy Z, dy Z^2, dy^2 Z^2 (fp64) and the valid count
+template <int VAR>
+__device__ __forceinline__ void accum_column(double* h, int* hi, const double* vrow, const int* irow, int vstride,
+                                             int c, int dx, double sgn) {
+  const double fdx = (double)dx * sgn;
+  if (VAR == VAR_DF) {
+    const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
+    const int m = irow[c], my = irow[vstride + c], myy = irow[2 * vstride + c];
+    h[0] = fma(sgn, w, h[0]);    // sum w
+    h[1] = fma(sgn, ww, h[1]);   // sum w^2
+    h[2] = fma(sgn, yw, h[2]);   // sum dy w
+    h[3] = fma(fdx, w, h[3]);    // sum dx w
+    const int sm = sgn > 0 ? m : -m, smy = sgn > 0 ? my : -my;
+    hi[0] += sm;                 // n
+    hi[1] += dx * sm;            // sum dx
+    hi[2] += smy;                // sum dy
+    hi[3] += dx * dx * sm;       // sum dx^2
+    hi[4] += dx * smy;           // sum dx dy
+    hi[5] += sgn > 0 ? myy : -myy;  // sum dy^2
+  } else {
+    const double z = vrow[c], z2 = vrow[vstride + c], yz = vrow[2 * vstride + c],
+                 yz2 = vrow[3 * vstride + c], y2z2 = vrow[4 * vstride + c];
+    const double fdx2 = fdx * (double)dx;
+    h[0] = fma(sgn, z, h[0]);     // S3  = sum Z
+    h[1] = fma(sgn, z2, h[1]);    // S33 = sum Z^2
+    h[2] = fma(sgn, yz, h[2]);    // S2  = sum dy Z
+    h[3] = fma(sgn, yz2, h[3]);   // S23 = sum dy Z^2
+    h[4] = fma(sgn, y2z2, h[4]);  // S22 = sum dy^2 Z^2
+    h[5] = fma(fdx, z, h[5]);     // S1  = sum dx Z
+    h[6] = fma(fdx, z2, h[6]);    // S13 = sum dx Z^2
+    h[7] = fma(fdx, yz2, h[7]);   // S12 = sum dx dy Z^2
+    h[8] = fma(fdx2, z2, h[8]);   // S11 = sum dx^2 Z^2
+    hi[0] += sgn > 0 ? irow[c] : -irow[c];
+  }
+}
+
+// one valid sample p (disparity form 1/Z, standard Z) at (dx, dy) from the origin, added
+// directly (the slow pass's re-summed windows)
+template <int VAR>
+__device__ __forceinline__ void accum_sample(double* h, int* hi, double p, int dx, int dy) {
+  const double fdx = (double)dx, fdy = (double)dy;
+  if (VAR == VAR_DF) {
+    h[0] += p;
+    h[1] = fma(p, p, h[1]);
+    h[2] = fma(fdy, p, h[2]);
+    h[3] = fma(fdx, p, h[3]);
+    hi[0] += 1;
+    hi[1] += dx;
+    hi[2] += dy;
+    hi[3] += dx * dx;
+    hi[4] += dx * dy;
+    hi[5] += dy * dy;
+  } else {
+    const double p2 = p * p;
+    h[0] += p;
+    h[1] += p2;
+    h[2] = fma(fdy, p, h[2]);
+    h[3] = fma(fdy, p2, h[3]);
+    h[4] = fma(fdy * fdy, p2, h[4]);
+    h[5] = fma(fdx, p, h[5]);
+    h[6] = fma(fdx, p2, h[6]);
+    h[7] = fma(fdx * fdy, p2, h[7]);
+    h[8] = fma(fdx * fdx, p2, h[8]);
+    hi[0] += 1;
+  }
+}
+
+// window moments -> centred scatter C (3x3) and mean mu of the space's monomials
+// (scatter_from_integrals / accumulate_scatter_naive, fitting.py:339-533, centred); txo, tyo:
+// tan of the dx / dy origin
+template <int VAR>
+__device__ __forceinline__ void assemble(const double* h, const int* hi, double txo, double tyo, double ifx,
+                                         double ify, double invn, Sym3& C, double& mu0, double& mu1, double& mu2) {
+  if (VAR == VAR_DF) {
+    const long long n = hi[0], sx = hi[1], sy = hi[2], sxx = hi[3], sxy = hi[4], syy = hi[5];
+    const double cq00 = (double)(n * sxx - sx * sx) * invn;
+    const double cq01 = (double)(n * sxy - sx * sy) * invn;
+    const double cq11 = (double)(n * syy - sy * sy) * invn;
+    const double mw = h[0] * invn;
+    const double fsx = (double)sx, fsy = (double)sy;
+    const double cq02 = fma(-fsx, mw, h[3]);
+    const double cq12 = fma(-fsy, mw, h[2]);
+    const double cq22 = fma(-h[0], mw, h[1]);
+    C.c00 = cq00 * (ifx * ifx);
+    C.c01 = cq01 * (ifx * ify);
+    C.c11 = cq11 * (ify * ify);
+    C.c02 = cq02 * ifx;
+    C.c12 = cq12 * ify;
+    C.c22 = cq22;
+    mu0 = fma(fsx * invn, ifx, txo);
+    mu1 = fma(fsy * invn, ify, tyo);
+    mu2 = mw;
+  } else {
+    // q = (dx Z, dy Z, Z): sums S1=h5, S2=h2, S3=h0, S11=h8, S12=h7, S22=h4,
+    // S13=h6, S23=h3, S33=h1; C_q = S_ab - S_a S_b / n
+    const double q0 = h[5] * invn, q1 = h[2] * invn, q2 = h[0] * invn;
+    const double k00 = fma(-h[5], q0, h[8]);
+    const double k01 = fma(-h[5], q1, h[7]);
+    const double k02 = fma(-h[5], q2, h[6]);
+    const double k11 = fma(-h[2], q1, h[4]);
+    const double k12 = fma(-h[2], q2, h[3]);
+    const double k22 = fma(-h[0], q2, h[1]);
+    // m = L q, L = [[ifx, 0, txo], [0, ify, tyo], [0, 0, 1]]
+    const double r00 = fma(ifx, k00, txo * k02), r01 = fma(ifx, k01, txo * k12),
+                 r02 = fma(ifx, k02, txo * k22);
+    const double r11 = fma(ify, k11, tyo * k12), r12 = fma(ify, k12, tyo * k22);
+    C.c00 = fma(ifx, r00, txo * r02);
+    C.c01 = fma(ify, r01, tyo * r02);
+    C.c02 = r02;
+    C.c11 = fma(ify, r11, tyo * r12);
+    C.c12 = r12;
+    C.c22 = k22;
+    mu0 = fma(ifx, q0, txo * q2);
+    mu1 = fma(ify, q1, tyo * q2);
+    mu2 = q2;
+  }
+}
+
+// The slow pass for one queued pixel of the tile: its window re-summed from the column sums
+// (directly, no running update) or -- Q_DIRECT with running column sums -- from the
+// primaries themselves, the robust solve (solve_window), and scalar stores that overwrite
+// what the row pass wrote for it.  Q_DIRECT entries (the sliding-sum guard) redo the
+// explicit fits as well; other entries only refresh the explicit curvature (it is shared).
+template <int VAR, int RT, bool EXP, bool NOPRIM, typename PrimFn>
+__device__ __forceinline__ void slow_pixel(const KParams& P, int e, int64_t frame, int x0, int y0, int r, int VQ,
+                                           int VRS, const double* vd, const int* vi, PrimFn primary) {
+  constexpr bool CENTRED = RT > 0 && RT <= 3;
+  const int pix = e & (Q_DIRECT - 1);
+  const bool direct = (e & Q_DIRECT) != 0;
+  const int orow = pix / TW, xl = pix % TW;
+  const int gy = y0 + orow, gx = x0 + xl;
+  if (gy >= P.H || gx >= P.W) return;
+  if (!(primary(orow + r, xl + r) > 0.0)) return;  // centre invalid: nothing was fitted
+  double h[HSums<VAR>::NH];
+  int hi[HSums<VAR>::NHI];
+  for (int k = 0; k < HSums<VAR>::NH; ++k) h[k] = 0.0;
+  for (int k = 0; k < HSums<VAR>::NHI; ++k) hi[k] = 0;
+  double tyo;
+  if (direct && !CENTRED) {
+    tyo = __ldg(P.tan_y + gy);
+    for (int dy = -r; dy <= r; ++dy)
+      for (int dx = -r; dx <= r; ++dx) {
+        const double p = primary(orow + r + dy, xl + r + dx);
+        if (p > 0.0) accum_sample<VAR>(h, hi, p, dx, dy);
+      }
+  } else {
+    tyo = __ldg(P.tan_y + (CENTRED ? gy : y0));
+    const double* vrow = vd + orow * VRS;
+    const int* irow = vi + orow * VRS;
+    for (int k = 0; k <= 2 * r; ++k) {
+      const int col = xl + k;
+      accum_column<VAR>(h, hi, vrow, irow, TH * VRS, (col & 3) * VQ + (col >> 2), k - r, 1.0);
+    }
+  }
+  const double txo = __ldg(P.tan_x + gx);
+  const int nwin = hi[0];
+  if (nwin < (EXP && P.do_exp ? 3 : 4)) return;
+  const double nd = (double)nwin;
+  const double invn = 1.0 / nd;
+  Sym3 C;
+  double mu0, mu1, mu2;
+  assemble<VAR>(h, hi, txo, tyo, P.ifx, P.ify, invn, C, mu0, mu1, mu2);
+  const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
+  float kap = 0.0f;
+  bool have_kap = false;
+  if (P.do_imp && nwin >= 4) {
+    WindowFit f;
+    solve_window<true>(C, mu0, mu1, mu2, nd, f);
+    float nx, ny, nz, off;
+    if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
+    else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
+    store_fit(P.imp, p, nx, ny, nz, off, fsqrt(fmaxf((float)(f.lam * invn), 0.0f)), f.kappa,
+              RF_PIX_INPUT_VALID | RF_PIX_FIT | (f.degenerate ? RF_PIX_DEGENERATE : 0));
+    kap = f.kappa;
+    have_kap = true;
+  }
+  if (EXP && P.do_exp) {
+    if (!have_kap) kap = curvature_only(C);
+    if (direct) {
+      ExplicitFit ex;
+      explicit_solve(C, mu0, mu1, mu2, nd, ex);
+      float a, b, c, d;
+      if (VAR == VAR_DF) finish_plane(ex.a, ex.b, ex.c, -1.0, a, b, c, d);
+      else finish_plane(ex.a, ex.b, -1.0, ex.c, a, b, c, d);
+      store_fit(P.exp, p, a, b, c, d, fsqrt(fmaxf((float)(ex.ss * invn), 0.0f)), kap,
+                RF_PIX_INPUT_VALID | RF_PIX_FIT | (ex.degenerate ? RF_PIX_DEGENERATE : 0));
+    } else {
+      P.exp.curvature[p] = kap;
+    }
+  }
+}
+
 // One persistent CTA walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
 // With USE_TMA the raw halo tile of the NEXT tile is fetched by TMA into the
 // other of two shared buffers while this tile's column and row passes run.
@@ -187,10 +396,12 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   // sums (p >= 0, so high words order like the values), double-buffered by tile parity; the
   // sliding-sum guard's departed-mass bound at the end of the row pass
   __shared__ unsigned s_dmax[2];
-  if (!CENTRED) {
-    if (tid == 0) s_dmax[0] = s_dmax[1] = 0u;
-    __syncthreads();
-  }
+  // slow-pass queue (QCAP tile-local pixel indices) and its fill count
+  __shared__ unsigned short s_q[QCAP];
+  __shared__ int s_qn;
+  constexpr int NH = HSums<VAR>::NH, NHI = HSums<VAR>::NHI;
+  if (tid == 0) s_dmax[0] = s_dmax[1] = 0u, s_qn = 0;
+  __syncthreads();
 
   if (USE_TMA) {
     if (tid == 0) {
@@ -427,49 +638,18 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       const int vstride = TH * VRS;
       if (!CENTRED && tid == 0) s_dmax[(it + 1) & 1] = 0u;  // read by the previous tile, written by the next
       // running horizontal sums (origin: segment start xs, tile row y0)
-      double h[VAR == VAR_DF ? 4 : 9];
-      int hi[VAR == VAR_DF ? 6 : 1];
+      double h[NH];
+      int hi[NHI];
     #pragma unroll
-      for (int k = 0; k < (VAR == VAR_DF ? 4 : 9); ++k) h[k] = 0.0;
+      for (int k = 0; k < NH; ++k) h[k] = 0.0;
     #pragma unroll
-      for (int k = 0; k < (VAR == VAR_DF ? 6 : 1); ++k) hi[k] = 0;
+      for (int k = 0; k < NHI; ++k) hi[k] = 0;
 
       // k: column offset from the segment start xs (xs is a multiple of 4, so the
       // residue-major position of column xs + k is a compile-time offset from vbase)
       const int vbase = xs >> 2;
       auto accum = [&](int k, double sgn) {
-        const int dx = k - r;
-        const int c = vbase + (k & 3) * VQ + (k >> 2);
-        const double fdx = (double)dx * sgn;
-        if (VAR == VAR_DF) {
-          const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
-          const int m = irow[c], my = irow[vstride + c], myy = irow[2 * vstride + c];
-          h[0] = fma(sgn, w, h[0]);    // sum w
-          h[1] = fma(sgn, ww, h[1]);   // sum w^2
-          h[2] = fma(sgn, yw, h[2]);   // sum dy w
-          h[3] = fma(fdx, w, h[3]);    // sum dx w
-          const int sm = sgn > 0 ? m : -m, smy = sgn > 0 ? my : -my;
-          hi[0] += sm;                 // n
-          hi[1] += dx * sm;            // sum dx
-          hi[2] += smy;                // sum dy
-          hi[3] += dx * dx * sm;       // sum dx^2
-          hi[4] += dx * smy;           // sum dx dy
-          hi[5] += sgn > 0 ? myy : -myy;  // sum dy^2
-        } else {
-          const double z = vrow[c], z2 = vrow[vstride + c], yz = vrow[2 * vstride + c],
-                       yz2 = vrow[3 * vstride + c], y2z2 = vrow[4 * vstride + c];
-          const double fdx2 = fdx * (double)dx;
-          h[0] = fma(sgn, z, h[0]);     // S3  = sum Z
-          h[1] = fma(sgn, z2, h[1]);    // S33 = sum Z^2
-          h[2] = fma(sgn, yz, h[2]);    // S2  = sum dy Z
-          h[3] = fma(sgn, yz2, h[3]);   // S23 = sum dy Z^2
-          h[4] = fma(sgn, y2z2, h[4]);  // S22 = sum dy^2 Z^2
-          h[5] = fma(fdx, z, h[5]);     // S1  = sum dx Z
-          h[6] = fma(fdx, z2, h[6]);    // S13 = sum dx Z^2
-          h[7] = fma(fdx, yz2, h[7]);   // S12 = sum dx dy Z^2
-          h[8] = fma(fdx2, z2, h[8]);   // S11 = sum dx^2 Z^2
-          hi[0] += sgn > 0 ? irow[c] : -irow[c];
-        }
+        accum_column<VAR>(h, hi, vrow, irow, vstride, vbase + (k & 3) * VQ + (k >> 2), k - r, sgn);
       };
 
       if constexpr (RT > 0) {
@@ -479,10 +659,8 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         for (int k = 0; k <= 2 * r; ++k) accum(k, 1.0);
       }
 
-    #if RF_STAGE_OUTPUTS
       float o_n[KSEG][3], o_off[KSEG], o_res[KSEG], o_cur[KSEG];
       uint8_t o_st[KSEG];
-    #endif
 
     #pragma unroll
       for (int j = 0; j < KSEG; ++j) {
@@ -503,58 +681,26 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
           const double invn = rcp_fast(nd);
           Sym3 C;
           double mu0, mu1, mu2;
-          if (VAR == VAR_DF) {
-            const long long n = hi[0], sx = hi[1], sy = hi[2], sxx = hi[3], sxy = hi[4], syy = hi[5];
-            const double cq00 = (double)(n * sxx - sx * sx) * invn;
-            const double cq01 = (double)(n * sxy - sx * sy) * invn;
-            const double cq11 = (double)(n * syy - sy * sy) * invn;
-            const double mw = h[0] * invn;
-            const double fsx = (double)sx, fsy = (double)sy;
-            const double cq02 = fma(-fsx, mw, h[3]);
-            const double cq12 = fma(-fsy, mw, h[2]);
-            const double cq22 = fma(-h[0], mw, h[1]);
-            C.c00 = cq00 * (ifx * ifx);
-            C.c01 = cq01 * (ifx * ify);
-            C.c11 = cq11 * (ify * ify);
-            C.c02 = cq02 * ifx;
-            C.c12 = cq12 * ify;
-            C.c22 = cq22;
-            mu0 = fma(fsx * invn, ifx, txo);
-            mu1 = fma(fsy * invn, ify, tyo);
-            mu2 = mw;
-          } else {
-            // q = (dx Z, dy Z, Z): sums S1=h5, S2=h2, S3=h0, S11=h8, S12=h7, S22=h4,
-            // S13=h6, S23=h3, S33=h1; C_q = S_ab - S_a S_b / n
-            const double q0 = h[5] * invn, q1 = h[2] * invn, q2 = h[0] * invn;
-            const double k00 = fma(-h[5], q0, h[8]);
-            const double k01 = fma(-h[5], q1, h[7]);
-            const double k02 = fma(-h[5], q2, h[6]);
-            const double k11 = fma(-h[2], q1, h[4]);
-            const double k12 = fma(-h[2], q2, h[3]);
-            const double k22 = fma(-h[0], q2, h[1]);
-            // m = L q, L = [[ifx, 0, txo], [0, ify, tyo], [0, 0, 1]]
-            const double r00 = fma(ifx, k00, txo * k02), r01 = fma(ifx, k01, txo * k12),
-                         r02 = fma(ifx, k02, txo * k22);
-            const double r11 = fma(ify, k11, tyo * k12), r12 = fma(ify, k12, tyo * k22);
-            C.c00 = fma(ifx, r00, txo * r02);
-            C.c01 = fma(ify, r01, tyo * r02);
-            C.c02 = r02;
-            C.c11 = fma(ify, r11, tyo * r12);
-            C.c12 = r12;
-            C.c22 = k22;
-            mu0 = fma(ifx, q0, txo * q2);
-            mu1 = fma(ify, q1, tyo * q2);
-            mu2 = q2;
-          }
+          assemble<VAR>(h, hi, txo, tyo, ifx, ify, invn, C, mu0, mu1, mu2);
           float kap = 0.0f;
           if (P.do_imp && nwin >= 4) {
           WindowFit f;
 #if RF_ABLATE >= 1
           f.lam = C.c00 + C.c11; f.u0 = mu0 + C.c01; f.u1 = mu1 + C.c02; f.u2 = mu2 + C.c12; f.s = C.c22;
           f.kappa = 0.1f; f.degenerate = false;
+          const bool fast = true;
 #else
-          solve_window<true>(C, mu0, mu1, mu2, nd, f);
+          const bool fast = solve_fast(C, mu0, mu1, mu2, nd, __int2float_rn(nwin), f);
 #endif
+          // windows the fast path declines are solved again by the robust path after the row
+          // pass (slow_pixel), whose outputs overwrite these
+          if (!fast) {
+#ifdef RF_COUNT_SLOW
+            atomicAdd(&g_slow_count[VAR], 1ull);
+#endif
+            const int qi = atomicAdd(&s_qn, 1);
+            if (qi < QCAP) s_q[qi] = (unsigned short)(orow * TW + xs + j);
+          }
 #if RF_ABLATE >= 2
           nx = (float)f.u0; ny = (float)f.u1; nz = (float)f.u2; off = (float)f.s;
 #else
@@ -598,7 +744,6 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
           }
           reinterpret_cast<uint8_t*>(xs_ + 24)[j] = stx;
         }
-    #if RF_STAGE_OUTPUTS
         o_n[j][0] = nx;
         o_n[j][1] = ny;
         o_n[j][2] = nz;
@@ -606,18 +751,6 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         o_res[j] = res;
         o_cur[j] = cur;
         o_st[j] = st;
-    #else
-        if (gx < P.W) {
-          const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
-          P.imp.normal[3 * p + 0] = nx;
-          P.imp.normal[3 * p + 1] = ny;
-          P.imp.normal[3 * p + 2] = nz;
-          P.imp.offset[p] = off;
-          P.imp.residual[p] = res;
-          P.imp.curvature[p] = cur;
-          P.imp.status[p] = st;
-        }
-    #endif
       }
 
       if (EXP && P.do_exp) {  // staged explicit outputs -> global, as vectors when aligned
@@ -647,7 +780,6 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
           }
         }
       }
-    #if RF_STAGE_OUTPUTS
       // ---- stores
       if (P.do_imp) {
       const int64_t pix0 = frame * P.out_frame + (int64_t)gy * P.W + gxs;
@@ -676,7 +808,6 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         }
       }
       }
-    #endif
       {
         // Sliding-sum guard.  A running sum keeps the rounding residue (~eps x value) of
         // every sample that has left it, so a window far smaller than the samples that slid
@@ -690,11 +821,11 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         // the centre sample (columns whose exact valid count is 0 belong to unfitted pixels
         // and are skipped: their running sums hold nothing but residue).  When the departed
         // mass exceeds 2^20 x that bound (millimetre depths next to metres; realistic scenes
-        // stay orders of magnitude below: bench.py's configs queue nothing), the segment is
-        // queued for a direct refit after this kernel (queue_refit / refit_kernel,
-        // rf_direct.cuh / rf_lattice.cu).  All of it runs after the unrolled loop (no register
-        // held through the solve), in whole exponent steps on the high words of the
-        // non-negative doubles (they order like the values; orders of magnitude suffice).
+        // stay orders of magnitude below: bench.py's configs queue nothing), the segment's
+        // pixels are queued for the slow pass with direct window sums (slow_pixel).  All of
+        // it runs after the unrolled loop (no register held through the solve), in whole
+        // exponent steps on the high words of the non-negative doubles (they order like the
+        // values; orders of magnitude suffice).
         // column xs + k of this row sits at vbase + (k & 3) VQ + (k >> 2): compile-time offsets
         // from one base (xs is a multiple of 4)
         const int* vhi = reinterpret_cast<const int*>(vd + (TH + orow) * VRS + vbase) + 1;  // channel 1
@@ -718,12 +849,32 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
           const int w = col_hi(j + r);
           h1min = min(h1min, col_n(j + r) > 0 ? w : 0x7fffffff);  // exact valid count
         }
-        if (h1min < thr)
-          queue_refit(P, frame, gy, gxs, (1u << min(KSEG, P.W - gxs)) - 1u);
+        if (h1min < thr) {
+          const int qi = atomicAdd(&s_qn, KSEG);
+          for (int j = 0; j < KSEG && qi + j < QCAP; ++j)
+            s_q[qi + j] = (unsigned short)(Q_DIRECT | (orow * TW + xs + j));
+        }
       }
       }
     }
+    __syncthreads();  // queue complete
+    // ---- 5. the robust path for the windows the fast solve declined (and the guard's
+    // segments, with direct sums), one queued pixel per thread; an overflowing queue (more
+    // than QCAP such windows in one tile: hostile inputs) redoes the whole tile that way
+    {
+      const int nq = s_qn;
+      if (nq > 0) {
+        const bool all = nq > QCAP;
+        for (int q = tid; q < (all ? TW * TH : nq); q += NTHREADS) {
+          const int e = all ? (Q_DIRECT | q) : s_q[q];
+          slow_pixel<VAR, RT, EXP, NOPRIM>(P, e, frame, x0, y0, r, VQ, VRS, vd, vi, [&](int row, int col) {
+            return NOPRIM ? raw_primary(row, col) : prim[row * HW_ + col];
+          });
+        }
+      }
+    }
     __syncthreads();  // prim / vd are rewritten by the next tile
+    if (tid == 0) s_qn = 0;
   }
 }
 
@@ -861,19 +1012,23 @@ extern "C" {
 
 int32_t rf_abi_version(void) { return RF_ABI_VERSION; }
 
+#ifdef RF_COUNT_SLOW
+// experiment builds only: windows per space (0 standard, 1 rgbd) that left the fast solve
+int32_t rf_debug_slow_counts(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_slow_count, sizeof(unsigned long long) * 256) != cudaSuccess) return 3;
+  if (reset) {
+    static const unsigned long long z[256] = {};
+    cudaMemcpyToSymbol(g_slow_count, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
 const char* rf_last_error(void) { return g_err; }
 
-int64_t rf_last_refit_segments(const rf_tables* t) {
-  if (!t) return -1;
-  const rf_device_guard guard(t->device);
-  unsigned c[8];
-  if (cudaMemcpy(c, t->fix_ctr, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return (int64_t)c[2] + (int64_t)c[6];  // entries of each space's last refit
-}
-
 int32_t rf_launches_per_call(int32_t formulation_mask) {
-  // per space: the tile kernel + the sliding-sum guard's refit (programmatic dependent launch)
-  return 2 * (((formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) ? 1 : 0) +
+  // one tile kernel per space
+  return (((formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) ? 1 : 0) +
               ((formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) ? 1 : 0));
 }
 
@@ -925,9 +1080,6 @@ rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const
   }
   e = cudaMalloc(&t->tan_x, sizeof(double) * in->width);
   if (e == cudaSuccess) e = cudaMalloc(&t->tan_y, sizeof(double) * in->height);
-  if (e == cudaSuccess) e = cudaMalloc(&t->fix_ctr, sizeof(unsigned) * 8);
-  if (e == cudaSuccess) e = cudaMemset(t->fix_ctr, 0, sizeof(unsigned) * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&t->fix_list, sizeof(unsigned long long) * 2 * RF_FIX_CAP);
   if (e == cudaSuccess) {
     const int m = in->width > in->height ? in->width : in->height;
     tan_table_kernel<<<(m + 255) / 256, 256>>>(t->tan_x, t->tan_y, in->width, in->height, in->fx,
@@ -941,8 +1093,6 @@ rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const
     cudaFree(t->tan_y);
     cudaFree(t->lat_x);
     cudaFree(t->lat_y);
-    cudaFree(t->fix_ctr);
-    cudaFree(t->fix_list);
     delete t;
     return fail(RF_ERR_CUDA, "rf_tables_create: %s", cudaGetErrorString(e));
   }
@@ -956,8 +1106,6 @@ rf_status rf_tables_destroy(rf_tables* t) {
   cudaFree(t->tan_y);
   cudaFree(t->lat_x);
   cudaFree(t->lat_y);
-  cudaFree(t->fix_ctr);
-  cudaFree(t->fix_list);
   delete t;
   return RF_OK;
 }
@@ -1045,9 +1193,6 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     if (di) P.imp = OutPlanes{outs[fi].normal, outs[fi].offset, outs[fi].residual, outs[fi].curvature, outs[fi].status};
     if (de) P.exp = OutPlanes{outs[fe].normal, outs[fe].offset, outs[fe].residual, outs[fe].curvature, outs[fe].status};
     P.batch = batch;
-    P.fix_ctr = t->fix_ctr + (var == VAR_STD ? 0 : 4);
-    P.fix_list = t->fix_list + (size_t)var * RF_FIX_CAP;
-    P.fix_cap = RF_FIX_CAP;
     const size_t sm = smem_bytes(var, r, tma, esz, de);
     cudaError_t e;
     const cudaStream_t ls = (fork && var == VAR_DF) ? fs->aux : s;
@@ -1057,7 +1202,6 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
       e = tma ? launch_radius<VAR_STD>(P, tmap, sm, tiles, ls) : launch_var<VAR_STD, false, 0>(P, tmap, sm, tiles, ls);
     else
       e = tma ? launch_radius<VAR_DF>(P, tmap, sm, tiles, ls) : launch_var<VAR_DF, false, 0>(P, tmap, sm, tiles, ls);
-    if (e == cudaSuccess) e = launch_refit(var, P, t->lat_x, t->lat_y, ls);
     if (e != cudaSuccess) {
       if (fork) {  // keep the caller's stream joined even on failure
         cudaEventRecord(fs->join, fs->aux);

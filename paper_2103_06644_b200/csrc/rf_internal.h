@@ -2,7 +2,8 @@
 #pragma once
 #include "../../include/rangefit_b200.h"
 
-// per-camera device tables (opaque in the public header)
+// per-camera device tables (opaque in the public header); immutable after rf_tables_create,
+// so one handle serves any number of concurrent streams
 struct rf_tables {
   rf_intrinsics intr;
   int device;
@@ -12,13 +13,7 @@ struct rf_tables {
   // (x + delta_x - cx) / fx and (y + delta_y - cy) / fy, [H][W] device; null when separable
   double* lat_x;
   double* lat_y;
-  // sliding-sum guard worklists (rf_fit.cu row pass), one per space: counters [2][4] =
-  // (entries, refit blocks done, entries of the last call, unused) and RF_FIX_CAP entries per
-  // space; reset by the refit kernel, so fits sharing one handle must be ordered on one stream
-  unsigned* fix_ctr;
-  unsigned long long* fix_list;
 };
-constexpr unsigned RF_FIX_CAP = 1u << 18;
 
 // tan_x / tan_y of pixel (x, y): the lattice when the camera has distortion offsets
 #ifdef __CUDACC__

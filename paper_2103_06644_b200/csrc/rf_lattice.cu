@@ -236,68 +236,14 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
             const int c = xs + j + r;
             wmin = min(wmin, crow[(c & 3) * VQ + (c >> 2)] > 0 ? colq(c) : 0x7fffffff);  // exact count
           }
-          if (wmin < thr) queue_refit(P, frame, gy, gxs, (1u << min(KSEG, P.W - gxs)) - 1u);
+          // rare (never on realistic scenes): refit the segment from direct window sums here
+          if (wmin < thr)
+            for (int j = 0; j < KSEG && gxs + j < P.W; ++j) fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, gy, gxs + j);
         }
       }
     }
     __syncthreads();  // vd / vc are rewritten by the next tile
   }
-}
-
-// Sliding-sum guard refit (rf_direct.cuh) of one space: one thread per queued (entry, pixel
-// bit); on worklist overflow every pixel of the launch.  Launched right behind the space's
-// tile kernel on the same stream as a programmatic dependent launch: its blocks are resident
-// while the tile kernel drains and wait (griddepcontrol.wait) for its completion, so an empty
-// list costs about a kernel's exit, not a launch.  The last block to finish resets the
-// counters (P.fix_ctr: entries, blocks done, entries of the last call).
-template <int VAR, bool EXP>
-__global__ void __launch_bounds__(128) refit_kernel(const KParams P, const double* lat_x, const double* lat_y) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const unsigned n = P.fix_ctr[0];
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (n > P.fix_cap) {
-    for (int64_t p = i0; p < P.batch * P.out_frame; p += stride) {
-      const int64_t frame = p / P.out_frame;
-      const int rem = (int)(p - frame * P.out_frame);
-      const int y = rem / P.W;
-      fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, y, rem - y * P.W);
-    }
-  } else {
-    for (int64_t i = i0; i < 4 * (int64_t)n; i += stride) {
-      const unsigned long long e = P.fix_list[i >> 2];
-      const int bit = (int)(i & 3);
-      if (!((e >> bit) & 1ull)) continue;
-      const int64_t p = (int64_t)(e >> 4);
-      const int64_t frame = p / P.out_frame;
-      const int rem = (int)(p - frame * P.out_frame);
-      const int y = rem / P.W;
-      fit_pixel_direct<VAR, EXP>(P, lat_x, lat_y, frame, y, rem - y * P.W + bit);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(P.fix_ctr + 1, 1u) == gridDim.x - 1) {
-      P.fix_ctr[2] = n;
-      P.fix_ctr[0] = 0u;
-      P.fix_ctr[1] = 0u;
-    }
-  }
-}
-
-template <int VAR, bool EXP>
-cudaError_t launch_refit_pdl(const KParams& P, const double* lat_x, const double* lat_y, int blocks, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)blocks);
-  cfg.blockDim = dim3(128);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, refit_kernel<VAR, EXP>, P, lat_x, lat_y);
 }
 
 template <int VAR>
@@ -330,15 +276,6 @@ cudaError_t launch_lattice_var(const KParams& P, const double* lat_x, const doub
 }  // namespace
 
 namespace rf_tile {
-cudaError_t launch_refit(int var, const KParams& P, const double* lat_x, const double* lat_y, cudaStream_t s) {
-  const int blocks = 16;  // usually an empty list: a small launch
-  if (var == VAR_STD)
-    return P.do_exp ? launch_refit_pdl<VAR_STD, true>(P, lat_x, lat_y, blocks, s)
-                    : launch_refit_pdl<VAR_STD, false>(P, lat_x, lat_y, blocks, s);
-  return P.do_exp ? launch_refit_pdl<VAR_DF, true>(P, lat_x, lat_y, blocks, s)
-                  : launch_refit_pdl<VAR_DF, false>(P, lat_x, lat_y, blocks, s);
-}
-
 cudaError_t launch_lattice(int var, const KParams& P, const double* lat_x, const double* lat_y,
                            cudaStream_t s) {
   return var == VAR_STD ? launch_lattice_var<VAR_STD>(P, lat_x, lat_y, s)

@@ -455,6 +455,127 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
   out.kappa = curv_finish(cs, t, c1, det, ft, k1, k2, k3);
 }
 
+// Common-case path of solve_window<true> as straight-line code: the same seeds, quartic
+// Newton steps from the middle of the seed bracket (one when lam/n <= 1e-4, two up to 1e-3,
+// three up to 1e-2), one curvature Newton step (from below lam_min, or -- close bottom pair
+// -- from above lam_max followed by the deflation), the dominant adjugate column.  Returns
+// false when the window needs the robust path (solve_window): a pencil near-tie (< 5% gap),
+// a curvature spectrum with both pairs close, lam/n above 1e-2, an adjugate of rank 0, a
+// non-positive upper spectrum, or a gap small enough to ask the degenerate test
+// (fitting.py:552-554).  `out` is then unspecified.
+__device__ __forceinline__ bool solve_fast(const Sym3& C, double m0, double m1, double m2, double n, float fn,
+                                           WindowFit& out) {
+  const double c00 = C.c00, c01 = C.c01, c02 = C.c02, c11 = C.c11, c12 = C.c12, c22 = C.c22;
+  const double A00 = c11 * c22 - c12 * c12;
+  const double A11 = c00 * c22 - c02 * c02;
+  const double A22 = c00 * c11 - c01 * c01;
+  const double A01 = c02 * c12 - c01 * c22;
+  const double A02 = c01 * c12 - c02 * c11;
+  const double A12 = c01 * c02 - c00 * c12;
+  const double t = c00 + c11 + c22;
+  const double c1 = A00 + A11 + A22;
+  const double det = c00 * A00 + c01 * A01 + c02 * A02;
+  const double nu = m0 * m0 + m1 * m1 + m2 * m2;
+  const double Cm0 = c00 * m0 + c01 * m1 + c02 * m2;
+  const double Cm1 = c01 * m0 + c11 * m1 + c12 * m2;
+  const double Cm2 = c02 * m0 + c12 * m1 + c22 * m2;
+  const double mm = m0 * Cm0 + m1 * Cm1 + m2 * Cm2;
+  const double Am0 = A00 * m0 + A01 * m1 + A02 * m2;
+  const double Am1 = A01 * m0 + A11 * m1 + A12 * m2;
+  const double Am2 = A02 * m0 + A12 * m1 + A22 * m2;
+  const double aa = m0 * Am0 + m1 * Am1 + m2 * Am2;
+  const double q3 = n + t + n * nu;
+  const double q2 = fma(n, t, c1) + n * (t * nu - mm);
+  const double q1 = fma(n, c1, det) + n * aa;
+  const double q0 = n * det;
+
+  float g1, g2, g3, k1, k2, k3;
+  const float ft = (float)t, fdet = (float)det;
+  {
+    const float inv = frcp(1.0f + (float)nu);
+    trig_cubic((float)(t + t * nu - mm) * inv, (float)(c1 + aa) * inv, fdet * inv, g1, g2, g3);
+    trig_cubic(ft, (float)c1, fdet, k1, k2, k3);
+  }
+  const float grel = g1 * frcp(fn);
+  // curvature: Newton on lam_min from just below k1, or on lam_max from k3 when the bottom
+  // pair is close (then lam_1 from lam_1 + lam_2 = t - lam_max, lam_1 lam_2 = det / lam_max)
+  const bool top = !((k2 - k1) >= 0.05f * k2);
+  // NaN-safe: every comparison is written so that NaN fails it
+  bool ok = ((g2 - g1) >= 0.05f * g2) & (grel <= 1e-2f) & (k2 > 0.0f) & (!top | ((k3 - k2) >= 0.05f * k3));
+
+  auto newton = [&](double x) {
+    const double x2 = x * x;
+    const double G = fma(fma(x - q3, x, q2), x2, fma(-q1, x, q0));
+    const double dG = fma(fma(fma(4.0, x, -3.0 * q3), x, 2.0 * q2), x, -q1);
+    return G * rcp_approx(dG);
+  };
+  // quartic Newton from the middle of [g1 (1 - g1/n), g1] and the curvature step
+  // (independent chains, interleaved)
+  double l = (double)(g1 * fmaf(-0.5f, grel, 1.0f));
+  double x = (double)(top ? k3 : k1 * (1.0f - 1e-5f));
+  {
+    const double P = fma(fma(t - x, x, -c1), x, det);
+    const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
+    l -= newton(l);
+    x -= P * rcp_approx(dP);
+  }
+  if (grel > 1e-4f) l -= newton(l);
+  if (grel > 1e-3f) l -= newton(l);
+  const double lam = l;
+
+  double beta;
+  {
+    const double dn = n - lam;
+    double r = rcp_approx(dn);
+    r = fma(r, fma(-dn, r, 1.0), r);
+    beta = fma(lam, r, 1.0);
+  }
+  const double gam = lam * beta;
+  const double E00 = c00 - lam - gam * m0 * m0;
+  const double E11 = c11 - lam - gam * m1 * m1;
+  const double E22 = c22 - lam - gam * m2 * m2;
+  const double E01 = c01 - gam * m0 * m1;
+  const double E02 = c02 - gam * m0 * m2;
+  const double E12 = c12 - gam * m1 * m2;
+  const double B00 = E11 * E22 - E12 * E12;
+  const double B11 = E00 * E22 - E02 * E02;
+  const double B22 = E00 * E11 - E01 * E01;
+  const double B01 = E02 * E12 - E01 * E22;
+  const double B02 = E01 * E12 - E02 * E11;
+  const double B12 = E01 * E02 - E00 * E12;
+  const double a0 = fabs(B00), a1 = fabs(B11), a2 = fabs(B22);
+  const bool s0 = a0 >= a1 && a0 >= a2;
+  const bool s1 = !s0 && a1 >= a2;
+  const double u0 = s0 ? B00 : s1 ? B01 : B02;
+  const double u1 = s0 ? B01 : s1 ? B11 : B12;
+  const double u2 = s0 ? B02 : s1 ? B12 : B22;
+  ok &= (s0 ? a0 : s1 ? a1 : a2) > 0.0;
+  out.u0 = u0;
+  out.u1 = u1;
+  out.u2 = u2;
+  out.s = -beta * (m0 * u0 + m1 * u1 + m2 * u2);
+  out.lam = lam;
+  // degenerate (fitting.py:552-554) cannot hold while gap > 1e-9 trace(S) >= 1e-9 ||S||_F
+  ok &= ((double)g2 - lam) > 1e-9 * q3;
+  out.degenerate = false;
+  float kmin = (float)x;
+  if (top) {
+    const double S = t - x;
+    const double Pp = det * rcp_fast(x);
+    const float D = (float)fma(S, S, -4.0 * Pp);  // (lam_2 - lam_1)^2, cancellation-free in fp64
+    kmin = 2.0f * (float)Pp * frcp((float)S + fsqrt(fmaxf(D, 0.0f)));
+  }
+  out.kappa = t > 0.0 ? kmin * frcp(ft) : 0.0f;
+  return ok;
+}
+
+// the robust solve for the windows solve_fast declines (out of line: its registers stay off
+// the fast path)
+static __device__ __noinline__ void solve_window_robust(const Sym3& C, double m0, double m1, double m2, double n,
+                                                        WindowFit& out) {
+  solve_window<true>(C, m0, m1, m2, n, out);
+}
+
 // canonical sign + unit normal / offset (fitting.py:76-94 and SURVEY A18)
 __device__ __forceinline__ void finish_plane(double a, double b, double c, double d, float& nx,
                                              float& ny, float& nz, float& off) {

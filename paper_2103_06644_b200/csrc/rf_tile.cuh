@@ -19,9 +19,6 @@ constexpr int MAX_RADIUS = 32;
 #ifndef RF_ABLATE
 #define RF_ABLATE 0
 #endif
-#ifndef RF_STAGE_OUTPUTS
-#define RF_STAGE_OUTPUTS 1
-#endif
 #ifndef RF_MIN_BLOCKS
 #define RF_MIN_BLOCKS 2
 #endif
@@ -50,11 +47,6 @@ struct KParams {
   int H, W, r, dtype;
   int do_imp, do_exp;  // implicit / explicit fit of this kernel's space requested
   OutPlanes imp, exp;  // implicit-* / explicit-* output planes of the space
-  // sliding-sum guard worklist of this space (rf_tables, rf_direct.cuh): fix_ctr[0] = entries
-  // appended, fix_ctr[1] = refit blocks done; entry = (first pixel index << 4) | pixel bits
-  unsigned* fix_ctr;
-  unsigned long long* fix_list;
-  unsigned fix_cap;
 };
 
 // bytes per depth element
@@ -95,10 +87,6 @@ __device__ __forceinline__ TileGeom tile_of(int64_t t, int ntx, int nty) {
 }
 
 // launch the per-pixel fits of one space on cameras with distortion lattices (rf_lattice.cu)
-// direct refit of the pixels the tile kernel's sliding-sum guard appended to P.fix_list: a
-// small programmatic dependent launch right behind the tile kernel, same stream; resets the
-// worklist
-cudaError_t launch_refit(int var, const KParams& P, const double* lat_x, const double* lat_y, cudaStream_t s);
 cudaError_t launch_lattice(int var, const KParams& P, const double* lat_x, const double* lat_y,
                            cudaStream_t s);
 

@@ -340,15 +340,6 @@ class HostPipeline:
         return self._host_out
 
 
-def last_refit_segments(maps: "TanAngleMaps") -> int:
-    """4-pixel segments the last completed fit_pixels call with these tables refit from direct
-    window sums (the sliding-sum guard; 0 on ordinary scenes).  Synchronises the device."""
-    n = int(N.load().rf_last_refit_segments(maps.handle))
-    if n < 0:
-        raise RuntimeError("rf_last_refit_segments failed")
-    return n
-
-
 def launches_per_call(formulations=PIXEL_FORMULATIONS) -> int:
     fmask = 0
     for f in formulations:

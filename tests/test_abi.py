@@ -36,12 +36,12 @@ def test_library_exports_every_symbol():
 def test_launch_count():
     # per space: the tile kernel plus the sliding-sum guard's refit launch
     lib = N.load()
-    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD) == 2
-    assert lib.rf_launches_per_call(N.RF_IMPLICIT_RGBD) == 2
-    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_IMPLICIT_RGBD) == 4
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD) == 1
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_RGBD) == 1
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_IMPLICIT_RGBD) == 2
     # the implicit and explicit fits of one space share a launch
-    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_EXPLICIT_STANDARD) == 2
-    assert lib.rf_launches_per_call(15) == 4
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_EXPLICIT_STANDARD) == 1
+    assert lib.rf_launches_per_call(15) == 2
 
 
 @pytest.mark.parametrize("fx,fy,cx,cy,w,h,msg", [
