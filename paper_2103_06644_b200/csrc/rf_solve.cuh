@@ -78,6 +78,62 @@ __device__ __forceinline__ void trig_cubic(float a2, float a1, float a0, float& 
   l1 = sd > 0.0f ? 2.0f * P * frcp(sd) : 0.0f;
 }
 
+// ---- packed fp32 pairs (sm_100 FFMA2 / FMUL2 / FADD2): the two seed cubics of a window
+// (pencil, curvature) run in lock step, one instruction for both
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 neg2(float2 a) { return f2(-a.x, -a.y); }
+__device__ __forceinline__ float2 max2(float2 a, float b) { return f2(fmaxf(a.x, b), fmaxf(a.y, b)); }
+
+// positive normal double (2^-126 <= x < 2^128) -> float, truncated, on the integer pipe (no
+// F2F): rebias the exponent and funnel-shift the top mantissa bits
+__device__ __forceinline__ float pos_d2f(double x) {
+  return __int_as_float(__funnelshift_l((unsigned)__double2loint(x), (unsigned)(__double2hiint(x) - 0x38000000), 3));
+}
+// positive normal float -> double (exact), on the integer pipe
+__device__ __forceinline__ double pos_f2d(float f) {
+  const unsigned b = __float_as_uint(f);
+  return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
+}
+
+// cos(acos(c) / 3) for c in [-1, 1] (the trigonometric cubic's largest-root factor):
+// with u = sqrt((1 + c) / 2) = cos(3 theta / 2) it is cos(2/3 acos u), analytic on [0, 1];
+// degree-7 fit, |error| < 6e-8 (replaces an acos polynomial plus a cosine)
+__device__ __forceinline__ float2 cos_third_acos2(float2 c) {
+  const float2 v = fma2(c, f2(0.5f), f2(0.5f));
+  const float2 u = f2(fsqrt(v.x), fsqrt(v.y));
+  float2 y = fma2(u, f2(0.0011383f), f2(-0.00610606f));
+  y = fma2(u, y, f2(0.01603623f));
+  y = fma2(u, y, f2(-0.03019835f));
+  y = fma2(u, y, f2(0.05281415f));
+  y = fma2(u, y, f2(-0.11103019f));
+  y = fma2(u, y, f2(0.57734591f));
+  return fma2(u, y, f2(0.50000006f));
+}
+
+// trig_cubic for two cubics at once (x: one, y: the other)
+__device__ __forceinline__ void trig_cubic2(float2 a2, float2 a1, float2 a0, float2& l1, float2& l2, float2& l3) {
+  const float2 q = mul2(a2, f2(1.0f / 3.0f));
+  const float2 p = max2(fma2(q, q, mul2(a1, f2(-1.0f / 3.0f))), 1e-37f);
+  const float2 isp = f2(frsqrt(p.x), frsqrt(p.y));
+  const float2 sp = mul2(p, isp);
+  const float2 h = fma2(fma2(q, q, mul2(a1, f2(-0.5f))), q, mul2(a0, f2(0.5f)));
+  const float2 c0 = mul2(mul2(h, isp), mul2(isp, isp));
+  const float2 c = f2(fminf(fmaxf(c0.x, -1.0f), 1.0f), fminf(fmaxf(c0.y, -1.0f), 1.0f));
+  l3 = max2(fma2(add2(sp, sp), cos_third_acos2(c), q), 1e-37f);
+  const float2 il3 = f2(frcp(l3.x), frcp(l3.y));
+  const float2 P = mul2(a0, il3);
+  const float2 S = mul2(add2(a1, neg2(P)), il3);
+  const float2 D = max2(fma2(S, S, mul2(P, f2(-4.0f))), 0.0f);
+  const float2 sd = add2(S, f2(fsqrt(D.x), fsqrt(D.y)));
+  l2 = mul2(sd, f2(0.5f));
+  const float2 t = mul2(add2(P, P), f2(frcp(sd.x), frcp(sd.y)));
+  l1 = f2(sd.x > 0.0f ? t.x : 0.0f, sd.y > 0.0f ? t.y : 0.0f);
+}
+
 struct Sym3 {
   double c00, c01, c02, c11, c12, c22;
 };
@@ -489,12 +545,18 @@ __device__ __forceinline__ bool solve_fast(const Sym3& C, double m0, double m1, 
   const double q1 = fma(n, c1, det) + n * aa;
   const double q0 = n * det;
 
+  // fp32 seeds, both cubics in lock step: x = the pencil at beta = 1 (normalised by 1 + nu),
+  // y = det(C - l I).  t, nu and t + t nu - mm (>= t) are positive: integer-pipe conversions
   float g1, g2, g3, k1, k2, k3;
-  const float ft = (float)t, fdet = (float)det;
+  const float ft = pos_d2f(t), fdet = (float)det;
   {
-    const float inv = frcp(1.0f + (float)nu);
-    trig_cubic((float)(t + t * nu - mm) * inv, (float)(c1 + aa) * inv, fdet * inv, g1, g2, g3);
-    trig_cubic(ft, (float)c1, fdet, k1, k2, k3);
+    const float inv = frcp(1.0f + pos_d2f(nu));
+    const float2 A2 = mul2(f2(pos_d2f(t + t * nu - mm), ft), f2(inv, 1.0f));
+    const float2 A1 = mul2(f2((float)(c1 + aa), (float)c1), f2(inv, 1.0f));
+    const float2 A0 = mul2(f2(fdet), f2(inv, 1.0f));
+    float2 r1, r2, r3;
+    trig_cubic2(A2, A1, A0, r1, r2, r3);
+    g1 = r1.x, g2 = r2.x, g3 = r3.x, k1 = r1.y, k2 = r2.y, k3 = r3.y;
   }
   const float grel = g1 * frcp(fn);
   // curvature: Newton on lam_min from just below k1, or on lam_max from k3 when the bottom
@@ -511,8 +573,8 @@ __device__ __forceinline__ bool solve_fast(const Sym3& C, double m0, double m1, 
   };
   // quartic Newton from the middle of [g1 (1 - g1/n), g1] and the curvature step
   // (independent chains, interleaved)
-  double l = (double)(g1 * fmaf(-0.5f, grel, 1.0f));
-  double x = (double)(top ? k3 : k1 * (1.0f - 1e-5f));
+  double l = pos_f2d(fmaxf(g1 * fmaf(-0.5f, grel, 1.0f), 1e-30f));
+  double x = pos_f2d(fmaxf(top ? k3 : k1 * (1.0f - 1e-5f), 1e-30f));
   {
     const double P = fma(fma(t - x, x, -c1), x, det);
     const double dP = fma(fma(-3.0, x, 2.0 * t), x, -c1);
@@ -530,6 +592,9 @@ __device__ __forceinline__ bool solve_fast(const Sym3& C, double m0, double m1, 
     r = fma(r, fma(-dn, r, 1.0), r);
     beta = fma(lam, r, 1.0);
   }
+  // eigenvector: the dominant column of adj(C - lam B), B = I + beta mu mu^T (error
+  // ~ eps ||C|| / gap; the cheaper adj(C - lam I) mu, also parallel to it, amplifies an
+  // error in lam by |mu| |u| / |mu.u|, which noise-dominated windows make large)
   const double gam = lam * beta;
   const double E00 = c00 - lam - gam * m0 * m0;
   const double E11 = c11 - lam - gam * m1 * m1;
