@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define RF_ABI_VERSION 3
+#define RF_ABI_VERSION 4
 
 typedef enum rf_status {
   RF_OK = 0,
@@ -108,9 +108,9 @@ rf_status rf_tables_destroy(rf_tables* tables);
  * (frame stride = H*row_pitch).  mask: optional device uint8 [batch,H,W]
  * (DepthImage(values, valid=mask), synth.py:88-94) or NULL.  outs: array of
  * RF_NUM_FORMULATIONS output sets indexed by RF_FORM_*; only the requested entries
- * are read.  The implicit and explicit fits of one space share one kernel launch
- * (one pass over the window moments).  The tables are immutable: any number of streams may
- * share one handle concurrently.
+ * are read.  The implicit and explicit fits of one space share one pass over its window
+ * moments; small batches fit both spaces in one launch (rf_launches_per_call).  The tables
+ * are immutable: any number of streams may share one handle concurrently.
  * stream: a cudaStream_t (NULL = legacy default). */
 rf_status rf_fit_pixels(const rf_tables* tables, const void* depth, int dtype, int64_t batch,
                         int32_t height, int32_t width, int64_t row_pitch, const uint8_t* mask,
@@ -156,9 +156,12 @@ rf_status rf_max_residuals(const rf_tables* tables, const void* depth, int dtype
                            const rf_rect* rects, int64_t nrects, int32_t formulation, const double* coefs,
                            double* out, void* stream);
 
-/* Number of kernel launches rf_fit_pixels issues for a given formulation mask (one tile
- * kernel per space). */
-int32_t rf_launches_per_call(int32_t formulation_mask);
+/* Number of kernel launches rf_fit_pixels issues on the current device for a formulation
+ * mask, window, depth dtype and batch shape with separable tables: one tile kernel for both
+ * spaces on small batches (up to four waves of tiles) when two of its CTAs fit per SM, else
+ * one per space. */
+int32_t rf_launches_per_call(int32_t formulation_mask, int32_t window, int32_t dtype, int64_t batch,
+                             int32_t height, int32_t width);
 
 /* Thread-local message describing the last non-RF_OK status. */
 const char* rf_last_error(void);

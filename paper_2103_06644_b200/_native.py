@@ -34,7 +34,7 @@ RF_IMPLICIT_STANDARD = 1 << RF_FORM_IMPLICIT_STANDARD
 RF_IMPLICIT_RGBD = 1 << RF_FORM_IMPLICIT_RGBD
 RF_EXPLICIT_STANDARD = 1 << RF_FORM_EXPLICIT_STANDARD
 RF_EXPLICIT_RGBD = 1 << RF_FORM_EXPLICIT_RGBD
-RF_ABI_VERSION = 3
+RF_ABI_VERSION = 4
 
 RF_PIX_INPUT_VALID = 1
 RF_PIX_FIT = 2
@@ -140,7 +140,8 @@ def load() -> ctypes.CDLL:
         vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp,
     ]
     L.rf_max_residuals.restype = ctypes.c_int
-    L.rf_launches_per_call.argtypes = [ctypes.c_int32]
+    L.rf_launches_per_call.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64,
+                                        ctypes.c_int32, ctypes.c_int32]
     L.rf_launches_per_call.restype = ctypes.c_int32
     L.rf_last_error.argtypes = []
     L.rf_last_error.restype = ctypes.c_char_p

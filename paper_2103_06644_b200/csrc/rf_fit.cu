@@ -82,68 +82,82 @@ __device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* tmap
       : "memory");
 }
 
-// depth element -> fp64 primary p (0 = invalid): DepthImage validity (synth.py:84, 111-114)
-template <int VAR>
-__device__ __forceinline__ double primary_of(float zf) {
-  const bool valid = (zf > 0.0f) && (zf <= 3.402823466e38f);  // isfinite & > 0
-  const double z = (double)zf;
-  return valid ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
-}
-template <int VAR>
-__device__ __forceinline__ double primary_of(double z) {  // float64 metres (RF64 ingest)
-  const bool valid = (z > 0.0) && (z <= 1.7976931348623157e308);
-  return valid ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
-}
-template <int VAR>
-__device__ __forceinline__ double primary_of(unsigned short mm) {
-  // mm / 1000.0 correctly rounded, as the reference divides: q = mm * RN(1/1000) and one
-  // exact-remainder correction (fma(-q, 1000, mm) is exact); checked for all 65535 codes
-  const double m = (double)mm;
-  const double q0 = m * 1e-3;
-  const double z = fma(fma(-q0, 1000.0, m), 1e-3, q0);
-  return mm > 0 ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
-}
-template <int VAR, typename T>
-__device__ __forceinline__ double primary_masked(T v, bool mask_ok) {
-  return mask_ok ? primary_of<VAR>(v) : 0.0;
-}
-
-// Halo tile (raw TMA box, element (row, col) at raw[(row + sy) * HWP + col + sx]) ->
-// prim[row * HW_ + col].  The plain loop covers interior tiles without a mask; image
-// edges (negative shift: rows/columns left of or above the image) and masks take the
-// checked loop.
-template <int VAR, typename T>
-__device__ __forceinline__ void convert_halo(double* prim, const T* raw, int HW_, int HH_, int HWP, int sx,
-                                             int sy, const KParams& P, int64_t frame, int x0, int y0, int r,
-                                             int tid) {
-  const int n = HH_ * HW_;
-  if (!P.mask && (sx | sy) >= 0) {
-#pragma unroll 2
-    for (int e = tid; e < n; e += NTHREADS) {
-      const int row = e / HW_, col = e - row * HW_;
-      prim[e] = primary_of<VAR>(raw[(row + sy) * HWP + col + sx]);
-    }
-  } else {
-    for (int e = tid; e < n; e += NTHREADS) {
-      const int row = e / HW_, col = e - row * HW_;
-      double p = 0.0;
-      if (row + sy >= 0 && col + sx >= 0) {
-        bool mask_ok = true;
-        if (P.mask) {
-          const int y = y0 - r + row, x = x0 - r + col;
-          mask_ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
-        }
-        p = primary_masked<VAR>(raw[(row + sy) * HWP + col + sx], mask_ok);
-      }
-      prim[e] = p;
-    }
-  }
-}
+// ------------------------------------------------------------------ tile kernel
+// One launch fits every requested formulation of both spaces (SP bit 0: standard, bit 1:
+// disparity form).  A persistent CTA owns a TW x TH tile of output pixels of one frame at a
+// time; the TMA halo of the next tile streams in while the current one is processed:
+//   1. convert : depth -> validity (synth.py:84, 111-114) -> fp64 primaries, 1/Z for the
+//                disparity form (integral.py:211-214) and Z for the standard form, 0 where
+//                invalid, both from one read of the halo;
+//   then per space: 2. column pass (vertical window sums) -> 3. row pass (horizontal sums,
+//   fast solve, outputs) -> 4. slow pass (the windows the fast solve declined).
+// Column sums of the two spaces share one buffer (the space passes run one after the
+// other); the valid-count geometry is summed once per tile.
 
 // slow-pass queue of one tile (row pass -> slow_pixel): tile-local pixel index, with
 // Q_DIRECT when the window must be re-summed directly (sliding-sum guard)
 constexpr int QCAP = 128;
 constexpr int Q_DIRECT = 0x8000;
+
+// depth element -> Z (metres) and validity (DepthImage, synth.py:84, 111-114)
+__device__ __forceinline__ double depth_z(float zf, bool& valid) {
+  valid = (zf > 0.0f) && (zf <= 3.402823466e38f);  // isfinite & > 0
+  return (double)zf;
+}
+__device__ __forceinline__ double depth_z(double z, bool& valid) {  // float64 metres (RF64 ingest)
+  valid = (z > 0.0) && (z <= 1.7976931348623157e308);
+  return z;
+}
+__device__ __forceinline__ double depth_z(unsigned short mm, bool& valid) {
+  // mm / 1000.0 correctly rounded, as the reference divides: q = mm * RN(1/1000) and one
+  // exact-remainder correction (fma(-q, 1000, mm) is exact); checked for all 65535 codes
+  valid = mm > 0;
+  const double m = (double)mm;
+  const double q0 = m * 1e-3;
+  return fma(fma(-q0, 1000.0, m), 1e-3, q0);
+}
+// the space's primary: 1/Z (disparity form) or Z (standard), 0 when invalid
+template <int VAR, typename T>
+__device__ __forceinline__ double primary_of(T v, bool mask_ok) {
+  bool valid;
+  const double z = depth_z(v, valid);
+  return (valid && mask_ok) ? (VAR == VAR_DF ? rcp_fast(z) : z) : 0.0;
+}
+
+// Halo tile (raw TMA box, element (row, col) at raw[(row + sy) * HWP + col + sx]) -> the
+// primaries of the requested spaces, [row * HW_ + col].  The plain loop covers interior
+// tiles without a mask; image edges (negative shift: rows/columns left of or above the
+// image) and masks take the checked loop.
+template <int SP, typename T>
+__device__ __forceinline__ void convert_halo(double* pw, double* pz, const T* raw, int HW_, int HH_, int HWP, int sx,
+                                             int sy, const KParams& P, int64_t frame, int x0, int y0, int r,
+                                             int tid) {
+  const int n = HH_ * HW_;
+  auto put = [&](int e, T v, bool ok) {
+    bool valid;
+    const double z = depth_z(v, valid);
+    valid = valid && ok;
+    if (SP & 2) pw[e] = valid ? rcp_fast(z) : 0.0;
+    if (SP & 1) pz[e] = valid ? z : 0.0;
+  };
+  if (!P.mask && (sx | sy) >= 0) {
+#pragma unroll 2
+    for (int e = tid; e < n; e += NTHREADS) {
+      const int row = e / HW_, col = e - row * HW_;
+      put(e, raw[(row + sy) * HWP + col + sx], true);
+    }
+  } else {
+    for (int e = tid; e < n; e += NTHREADS) {
+      const int row = e / HW_, col = e - row * HW_;
+      bool ok = row + sy >= 0 && col + sx >= 0;
+      if (ok && P.mask) {
+        const int y = y0 - r + row, x = x0 - r + col;
+        ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
+      }
+      put(e, ok ? raw[(row + sy) * HWP + col + sx] : T(0), ok);
+    }
+  }
+}
 
 // running horizontal sums of one space: fp64 moments and exact integer geometry
 template <int VAR> struct HSums {
@@ -151,16 +165,21 @@ template <int VAR> struct HSums {
   static constexpr int NHI = VAR == VAR_DF ? 6 : 1;
 };
 
+// valid-count geometry of one column sum: x = count | (sum dy) << 16, y = sum dy^2
+__device__ __forceinline__ int2 pack_counts(int m, int my, int myy) { return make_int2((m & 0xffff) | (my << 16), myy); }
+
 // add (sgn = +1) or remove (sgn = -1) one column's vertical sums at offset dx from the
 // horizontal origin: disparity form w, w^2, dy w (fp64) and the valid count, dy, dy^2
 // (int); standard form Z, Z^2, dy Z, dy Z^2, dy^2 Z^2 (fp64) and the valid count
 template <int VAR>
-__device__ __forceinline__ void accum_column(double* h, int* hi, const double* vrow, const int* irow, int vstride,
+__device__ __forceinline__ void accum_column(double* h, int* hi, const double* vrow, const int2* irow, int vstride,
                                              int c, int dx, double sgn) {
   const double fdx = (double)dx * sgn;
+  const int2 g = irow[c];
+  const int m = g.x & 0xffff;
   if (VAR == VAR_DF) {
     const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
-    const int m = irow[c], my = irow[vstride + c], myy = irow[2 * vstride + c];
+    const int my = g.x >> 16, myy = g.y;
     h[0] = fma(sgn, w, h[0]);    // sum w
     h[1] = fma(sgn, ww, h[1]);   // sum w^2
     h[2] = fma(sgn, yw, h[2]);   // sum dy w
@@ -185,7 +204,7 @@ __device__ __forceinline__ void accum_column(double* h, int* hi, const double* v
     h[6] = fma(fdx, z2, h[6]);    // S13 = sum dx Z^2
     h[7] = fma(fdx, yz2, h[7]);   // S12 = sum dx dy Z^2
     h[8] = fma(fdx2, z2, h[8]);   // S11 = sum dx^2 Z^2
-    hi[0] += sgn > 0 ? irow[c] : -irow[c];
+    hi[0] += sgn > 0 ? m : -m;
   }
 }
 
@@ -271,21 +290,178 @@ __device__ __forceinline__ void assemble(const double* h, const int* hi, double 
   }
 }
 
+// Per-tile context shared by the space passes: geometry, shared-memory views, the raw
+// halo (NOPRIM reads primaries straight from it).
+struct TileCtx {
+  const KParams* P;
+  int r, HW_, HH_, HWP, VQ, VRS, sx, sy, esz, it, tid;
+  int64_t frame;
+  int x0, y0;
+  const unsigned char* raw;
+  double* pw;   // [HH_][HW_] 1/Z (disparity form)
+  double* pz;   // [HH_][HW_] Z (standard)
+  double* vd;   // [NVD][TH][VRS] column sums of the current space
+  int2* vi;     // [TH][VRS] valid-count geometry (both spaces)
+  float* xstage;
+};
+
+// primary of halo element (row, col) of the tile for space VAR: from the converted tile, or
+// (NOPRIM) converted from the raw TMA box on the fly
+template <int VAR, bool NOPRIM>
+__device__ __forceinline__ double primary_at(const TileCtx& T, int row, int col) {
+  if (!NOPRIM) return (VAR == VAR_DF ? T.pw : T.pz)[row * T.HW_ + col];
+  if (row + T.sy < 0 || col + T.sx < 0) return 0.0;  // left / top of the image
+  const KParams& P = *T.P;
+  bool mask_ok = true;
+  if (P.mask) {
+    const int y = T.y0 - T.r + row, x = T.x0 - T.r + col;
+    mask_ok = y < P.H && x < P.W && __ldg(P.mask + T.frame * P.out_frame + (int64_t)y * P.W + x) != 0;
+  }
+  const int ri = (row + T.sy) * T.HWP + col + T.sx;
+  return T.esz == 2   ? primary_of<VAR>(reinterpret_cast<const unsigned short*>(T.raw)[ri], mask_ok)
+         : T.esz == 8 ? primary_of<VAR>(reinterpret_cast<const double*>(T.raw)[ri], mask_ok)
+                      : primary_of<VAR>(reinterpret_cast<const float*>(T.raw)[ri], mask_ok);
+}
+
+// ---- 2. vertical window sums of space VAR (and, for the tile's first space, the
+// valid-count geometry).  Small compile-time radii: every (column, output row) pair sums
+// its 2r+1 rows directly (short independent chains, all threads busy), dy centred on the
+// output row.  Otherwise each halo column is split into `parts` row segments that warm up on
+// their 2r leading rows and then slide down, dy relative to the tile's first output row.
+template <int VAR, int RT, bool NOPRIM, bool COUNTS>
+__device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) {
+  constexpr int NVD = VAR == VAR_DF ? 3 : 5;
+  constexpr bool CENTRED = RT > 0 && RT <= 3;
+  const int r = T.r, VRS = T.VRS, VQ = T.VQ, tid = T.tid;
+  double* vd = T.vd;
+  if constexpr (CENTRED) {
+    // dy = k - RT (compile-time): the dy-weighted sums fold into symmetric differences
+    constexpr int HWc = TW + 2 * RT;
+    constexpr int K = 2 * RT + 1;
+    const double* prim = VAR == VAR_DF ? T.pw : T.pz;
+    for (int e = tid; e < TH * HWc; e += NTHREADS) {
+      const int o = e / HWc, col = e - o * HWc;
+      double p[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) p[k] = prim[(o + k) * HWc + col];
+      double a[NVD];
+      double s0 = p[0];
+#pragma unroll
+      for (int k = 1; k < K; ++k) s0 += p[k];
+      double s2 = p[RT + 1] - p[RT - 1];
+#pragma unroll
+      for (int d = 2; d <= RT; ++d) s2 = fma((double)d, p[RT + d] - p[RT - d], s2);
+      if (VAR == VAR_DF) {
+        double s1 = p[0] * p[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) s1 = fma(p[k], p[k], s1);
+        a[0] = s0;
+        a[1] = s1;
+        a[2] = s2;
+      } else {
+        double q[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) q[k] = p[k] * p[k];
+        double s1 = q[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) s1 += q[k];
+        double s3 = q[RT + 1] - q[RT - 1], s4 = q[RT + 1] + q[RT - 1];
+#pragma unroll
+        for (int d = 2; d <= RT; ++d) {
+          s3 = fma((double)d, q[RT + d] - q[RT - d], s3);
+          s4 = fma((double)(d * d), q[RT + d] + q[RT - d], s4);
+        }
+        a[0] = s0;
+        a[1] = s1;
+        a[2] = s2;
+        a[3] = s3;
+        a[4] = s4;
+      }
+      const int cpos = (col & 3) * VQ + (col >> 2);
+#pragma unroll
+      for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * VRS + cpos] = a[k];
+      if (COUNTS) {
+        int m = 0, my = 0, myy = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) m += p[k] > 0.0 ? 1 : 0;
+#pragma unroll
+        for (int d = 1; d <= RT; ++d) {
+          const int vp = p[RT + d] > 0.0 ? 1 : 0, vm = p[RT - d] > 0.0 ? 1 : 0;
+          my += d * (vp - vm);
+          myy += d * d * (vp + vm);
+        }
+        T.vi[o * VRS + cpos] = pack_counts(m, my, myy);
+      }
+    }
+  } else {
+    const int HW_ = T.HW_;
+    const int parts = max(1, min(NTHREADS / HW_, TH));
+    const int col = tid % HW_;
+    const int part = tid / HW_;
+    int dm = 0;  // high word of the largest primary that left this thread's sums
+    if (part < parts) {
+      const int o0 = (part * TH) / parts, o1 = ((part + 1) * TH) / parts;  // output rows [o0, o1)
+      double a[NVD];
+      int m = 0, my = 0, myy = 0;
+#pragma unroll
+      for (int k = 0; k < NVD; ++k) a[k] = 0.0;
+      // dy of input row ii is ii - r (origin: the tile's first output row)
+      auto add = [&](int ii, double fdy, int dy, double sg) {
+        const double p = primary_at<VAR, NOPRIM>(T, ii, col);
+        if (sg < 0.0) dm = max(dm, __double2hiint(p));  // p >= 0: high words order like values
+        if (VAR == VAR_DF) {
+          a[0] = fma(sg, p, a[0]);
+          a[1] = fma(sg * p, p, a[1]);
+          a[2] = fma(sg * fdy, p, a[2]);
+        } else {
+          const double p2 = p * p;
+          const double sfdy = sg * fdy;
+          a[0] = fma(sg, p, a[0]);
+          a[1] = fma(sg, p2, a[1]);
+          a[2] = fma(sfdy, p, a[2]);
+          a[3] = fma(sfdy, p2, a[3]);
+          a[4] = fma(sfdy * fdy, p2, a[4]);
+        }
+        if (COUNTS) {
+          const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
+          m += v;
+          my += v * dy;
+          myy += v * dy * dy;
+        }
+      };
+      // window of output row o covers input rows [o, o + 2r]
+      double fdy = (double)(o0 - r);
+      for (int ii = o0; ii < o0 + 2 * r; ++ii, fdy += 1.0) add(ii, fdy, ii - r, 1.0);
+      double fdy_lo = (double)(o0 - r);
+      const int cpos = (col & 3) * VQ + (col >> 2);
+      for (int o = o0; o < o1; ++o, fdy += 1.0, fdy_lo += 1.0) {
+        add(o + 2 * r, fdy, o + r, 1.0);
+#pragma unroll
+        for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * VRS + cpos] = a[k];
+        if (COUNTS) T.vi[o * VRS + cpos] = pack_counts(m, my, myy);
+        add(o, fdy_lo, o - r, -1.0);
+      }
+    }
+    const unsigned b = __reduce_max_sync(0xffffffffu, (unsigned)dm);  // dm >= 0
+    if ((tid & 31) == 0) atomicMax(&s_dmax[T.it & 1], b);
+  }
+}
+
 // The slow pass for one queued pixel of the tile: its window re-summed from the column sums
 // (directly, no running update) or -- Q_DIRECT with running column sums -- from the
 // primaries themselves, the robust solve (solve_window), and scalar stores that overwrite
 // what the row pass wrote for it.  Q_DIRECT entries (the sliding-sum guard) redo the
 // explicit fits as well; other entries only refresh the explicit curvature (it is shared).
-template <int VAR, int RT, bool EXP, bool NOPRIM, typename PrimFn>
-__device__ __forceinline__ void slow_pixel(const KParams& P, int e, int64_t frame, int x0, int y0, int r, int VQ,
-                                           int VRS, const double* vd, const int* vi, PrimFn primary) {
+template <int VAR, int RT, bool EXP, bool NOPRIM>
+__device__ __forceinline__ void slow_pixel(const TileCtx& T, const KParams& P, int e) {
   constexpr bool CENTRED = RT > 0 && RT <= 3;
+  const int r = T.r;
   const int pix = e & (Q_DIRECT - 1);
   const bool direct = (e & Q_DIRECT) != 0;
   const int orow = pix / TW, xl = pix % TW;
-  const int gy = y0 + orow, gx = x0 + xl;
+  const int gy = T.y0 + orow, gx = T.x0 + xl;
   if (gy >= P.H || gx >= P.W) return;
-  if (!(primary(orow + r, xl + r) > 0.0)) return;  // centre invalid: nothing was fitted
+  if (!(primary_at<VAR, NOPRIM>(T, orow + r, xl + r) > 0.0)) return;  // centre invalid: nothing was fitted
   double h[HSums<VAR>::NH];
   int hi[HSums<VAR>::NHI];
   for (int k = 0; k < HSums<VAR>::NH; ++k) h[k] = 0.0;
@@ -295,16 +471,16 @@ __device__ __forceinline__ void slow_pixel(const KParams& P, int e, int64_t fram
     tyo = __ldg(P.tan_y + gy);
     for (int dy = -r; dy <= r; ++dy)
       for (int dx = -r; dx <= r; ++dx) {
-        const double p = primary(orow + r + dy, xl + r + dx);
+        const double p = primary_at<VAR, NOPRIM>(T, orow + r + dy, xl + r + dx);
         if (p > 0.0) accum_sample<VAR>(h, hi, p, dx, dy);
       }
   } else {
-    tyo = __ldg(P.tan_y + (CENTRED ? gy : y0));
-    const double* vrow = vd + orow * VRS;
-    const int* irow = vi + orow * VRS;
+    tyo = __ldg(P.tan_y + (CENTRED ? gy : T.y0));
+    const double* vrow = T.vd + orow * T.VRS;
+    const int2* irow = T.vi + orow * T.VRS;
     for (int k = 0; k <= 2 * r; ++k) {
       const int col = xl + k;
-      accum_column<VAR>(h, hi, vrow, irow, TH * VRS, (col & 3) * VQ + (col >> 2), k - r, 1.0);
+      accum_column<VAR>(h, hi, vrow, irow, TH * T.VRS, (col & 3) * T.VQ + (col >> 2), k - r, 1.0);
     }
   }
   const double txo = __ldg(P.tan_x + gx);
@@ -315,7 +491,7 @@ __device__ __forceinline__ void slow_pixel(const KParams& P, int e, int64_t fram
   Sym3 C;
   double mu0, mu1, mu2;
   assemble<VAR>(h, hi, txo, tyo, P.ifx, P.ify, invn, C, mu0, mu1, mu2);
-  const int64_t p = frame * P.out_frame + (int64_t)gy * P.W + gx;
+  const int64_t p = T.frame * P.out_frame + (int64_t)gy * P.W + gx;
   float kap = 0.0f;
   bool have_kap = false;
   if (P.do_imp && nwin >= 4) {
@@ -345,62 +521,323 @@ __device__ __forceinline__ void slow_pixel(const KParams& P, int e, int64_t fram
   }
 }
 
-// One persistent CTA walks tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
-// With USE_TMA the raw halo tile of the NEXT tile is fetched by TMA into the
-// other of two shared buffers while this tile's column and row passes run.
-// RT > 0: compile-time window radius (all halo geometry and shared-memory offsets
-// fold to constants); RT == 0: runtime radius P.r.
-// EXP: explicit fits compiled in (false keeps the implicit-only kernel lean).
-template <int VAR, bool USE_TMA, int RT, bool EXP>
+// ---- 3. horizontal running sums + per-window fast solve + outputs of space VAR; each
+// thread owns KSEG consecutive pixels of one output row.  Windows the fast solve declines
+// and segments the sliding-sum guard flags are queued for the slow pass.
+template <int VAR, int RT, bool EXP, bool NOPRIM>
+__device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, unsigned* s_dmax,
+                                         unsigned short* s_q, int* s_qn) {
+  constexpr bool CENTRED = RT > 0 && RT <= 3;
+  constexpr int NH = HSums<VAR>::NH, NHI = HSums<VAR>::NHI;
+  const int r = T.r, VQ = T.VQ, VRS = T.VRS, tid = T.tid;
+  const int orow = tid / (TW / KSEG);
+  const int xs = (tid % (TW / KSEG)) * KSEG;  // tile-local x of the segment's first pixel
+  const int gy = T.y0 + orow;
+  const int gxs = T.x0 + xs;
+  if (gy >= P.H || gxs >= P.W) return;
+  const double txo = __ldg(P.tan_x + gxs);
+  const double tyo = __ldg(P.tan_y + (CENTRED ? gy : T.y0));  // origin row of dy
+  const double ifx = P.ifx, ify = P.ify;
+  const double* vrow = T.vd + orow * VRS;
+  const int2* irow = T.vi + orow * VRS;
+  const int vstride = TH * VRS;
+  if (!CENTRED && tid == 0) s_dmax[(T.it + 1) & 1] = 0u;  // read by the previous tile, written by the next
+  // running horizontal sums (origin: segment start xs, tile row y0)
+  double h[NH];
+  int hi[NHI];
+#pragma unroll
+  for (int k = 0; k < NH; ++k) h[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < NHI; ++k) hi[k] = 0;
+  // k: column offset from the segment start xs (xs is a multiple of 4, so the
+  // residue-major position of column xs + k is a compile-time offset from vbase)
+  const int vbase = xs >> 2;
+  auto accum = [&](int k, double sgn) {
+    accum_column<VAR>(h, hi, vrow, irow, vstride, vbase + (k & 3) * VQ + (k >> 2), k - r, sgn);
+  };
+  if constexpr (RT > 0) {
+#pragma unroll
+    for (int k = 0; k <= 2 * RT; ++k) accum(k, 1.0);
+  } else {
+    for (int k = 0; k <= 2 * r; ++k) accum(k, 1.0);
+  }
+
+#if RF_ROW_UNROLL
+  float o_n[KSEG][3], o_off[KSEG], o_res[KSEG], o_cur[KSEG];
+  uint8_t o_st[KSEG];
+#pragma unroll
+#else
+  // one copy of the solve code per space (a fully unrolled segment loop quadruples the
+  // kernel's instruction footprint: instruction-fetch stalls); outputs stored per pixel
+#pragma unroll 1
+#endif
+  for (int j = 0; j < KSEG; ++j) {
+#if RF_ABLATE < 3
+    if (j > 0) {
+      accum(j + 2 * r, 1.0);
+      accum(j - 1, -1.0);
+    }
+#endif
+    const int gx = gxs + j;
+    const double pc = primary_at<VAR, NOPRIM>(T, orow + r, xs + j + r);
+    uint8_t st = pc > 0.0 ? RF_PIX_INPUT_VALID : 0;
+    const int nwin = (int)hi[0];
+    float nx = __int_as_float(0x7fc00000), ny = nx, nz = nx, off = nx, res = nx, cur = nx;
+    uint8_t stx = st;  // explicit-fit status (MIN_SAMPLES 3 instead of 4)
+    if (st && nwin >= (EXP ? 3 : 4) && gx < P.W) {
+      const double nd = (double)nwin;
+      const double invn = rcp_fast(nd);
+      Sym3 C;
+      double mu0, mu1, mu2;
+      assemble<VAR>(h, hi, txo, tyo, ifx, ify, invn, C, mu0, mu1, mu2);
+      float kap = 0.0f;
+      if (P.do_imp && nwin >= 4) {
+        WindowFit f;
+#if RF_ABLATE >= 1
+        f.lam = C.c00 + C.c11; f.u0 = mu0 + C.c01; f.u1 = mu1 + C.c02; f.u2 = mu2 + C.c12; f.s = C.c22;
+        f.kappa = 0.1f; f.degenerate = false;
+        const bool fast = true;
+#else
+        const bool fast = solve_fast(C, mu0, mu1, mu2, nd, __int2float_rn(nwin), f);
+#endif
+        // windows the fast path declines are solved again by the robust path after the row
+        // pass (slow_pixel), whose outputs overwrite these
+        if (!fast) {
+#ifdef RF_COUNT_SLOW
+          atomicAdd(&g_slow_count[VAR], 1ull);
+#endif
+          const int qi = atomicAdd(s_qn, 1);
+          if (qi < QCAP) s_q[qi] = (unsigned short)(orow * TW + xs + j);
+        }
+#if RF_ABLATE >= 2
+        nx = (float)f.u0; ny = (float)f.u1; nz = (float)f.u2; off = (float)f.s;
+#else
+        if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
+        else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
+#endif
+        res = fsqrt(fmaxf((float)(f.lam * invn), 0.0f));
+        cur = f.kappa;
+        kap = f.kappa;
+        st |= RF_PIX_FIT;
+        if (f.degenerate) st |= RF_PIX_DEGENERATE;
+      }
+      if (EXP && P.do_exp) {
+        if (!(P.do_imp && nwin >= 4)) kap = curvature_only(C);
+        ExplicitFit e;
+        explicit_solve(C, mu0, mu1, mu2, nd, e);
+        float ex, ey, ez, eo;
+        // explicit_to_implicit (fitting.py:729-739): standard (a, b, -1, c), rgbd (a, b, c, -1)
+        if (VAR == VAR_DF) finish_plane(e.a, e.b, e.c, -1.0, ex, ey, ez, eo);
+        else finish_plane(e.a, e.b, -1.0, e.c, ex, ey, ez, eo);
+        stx |= RF_PIX_FIT | (e.degenerate ? RF_PIX_DEGENERATE : 0);
+        float* xs_ = T.xstage + 28 * tid;
+        xs_[3 * j + 0] = ex;
+        xs_[3 * j + 1] = ey;
+        xs_[3 * j + 2] = ez;
+        xs_[12 + j] = eo;
+        xs_[16 + j] = fsqrt(fmaxf((float)(e.ss * invn), 0.0f));
+        xs_[20 + j] = kap;
+      }
+    }
+    if (EXP && P.do_exp) {
+      float* xs_ = T.xstage + 28 * tid;
+      if (!(stx & RF_PIX_FIT)) {
+        const float qn = __int_as_float(0x7fc00000);
+        xs_[3 * j + 0] = qn;
+        xs_[3 * j + 1] = qn;
+        xs_[3 * j + 2] = qn;
+        xs_[12 + j] = qn;
+        xs_[16 + j] = qn;
+        xs_[20 + j] = qn;
+      }
+      reinterpret_cast<uint8_t*>(xs_ + 24)[j] = stx;
+    }
+#if RF_ROW_UNROLL
+    o_n[j][0] = nx;
+    o_n[j][1] = ny;
+    o_n[j][2] = nz;
+    o_off[j] = off;
+    o_res[j] = res;
+    o_cur[j] = cur;
+    o_st[j] = st;
+#else
+    if (P.do_imp && gx < P.W) store_fit(P.imp, T.frame * P.out_frame + (int64_t)gy * P.W + gx, nx, ny, nz, off, res, cur, st);
+#endif
+  }
+
+  const int64_t pix0 = T.frame * P.out_frame + (int64_t)gy * P.W + gxs;
+  const bool vec = ((P.W & (KSEG - 1)) == 0) && (gxs + KSEG <= P.W);
+  if (EXP && P.do_exp) {  // staged explicit outputs -> global, as vectors when aligned
+    const float* xs_ = T.xstage + 28 * tid;
+    if (vec) {
+      const float4* sv = reinterpret_cast<const float4*>(xs_);
+      float4* pn = reinterpret_cast<float4*>(P.exp.normal + 3 * pix0);
+      pn[0] = sv[0];
+      pn[1] = sv[1];
+      pn[2] = sv[2];
+      *reinterpret_cast<float4*>(P.exp.offset + pix0) = sv[3];
+      *reinterpret_cast<float4*>(P.exp.residual + pix0) = sv[4];
+      *reinterpret_cast<float4*>(P.exp.curvature + pix0) = sv[5];
+      *reinterpret_cast<uchar4*>(P.exp.status + pix0) = *reinterpret_cast<const uchar4*>(xs_ + 24);
+    } else {
+      for (int j = 0; j < KSEG; ++j) {
+        if (gxs + j >= P.W) break;
+        const int64_t p = pix0 + j;
+        P.exp.normal[3 * p + 0] = xs_[3 * j + 0];
+        P.exp.normal[3 * p + 1] = xs_[3 * j + 1];
+        P.exp.normal[3 * p + 2] = xs_[3 * j + 2];
+        P.exp.offset[p] = xs_[12 + j];
+        P.exp.residual[p] = xs_[16 + j];
+        P.exp.curvature[p] = xs_[20 + j];
+        P.exp.status[p] = reinterpret_cast<const uint8_t*>(xs_ + 24)[j];
+      }
+    }
+  }
+#if RF_ROW_UNROLL
+  if (P.do_imp) {
+    if (vec) {
+      float4* pn = reinterpret_cast<float4*>(P.imp.normal + 3 * pix0);
+      pn[0] = make_float4(o_n[0][0], o_n[0][1], o_n[0][2], o_n[1][0]);
+      pn[1] = make_float4(o_n[1][1], o_n[1][2], o_n[2][0], o_n[2][1]);
+      pn[2] = make_float4(o_n[2][2], o_n[3][0], o_n[3][1], o_n[3][2]);
+      *reinterpret_cast<float4*>(P.imp.offset + pix0) = make_float4(o_off[0], o_off[1], o_off[2], o_off[3]);
+      *reinterpret_cast<float4*>(P.imp.residual + pix0) = make_float4(o_res[0], o_res[1], o_res[2], o_res[3]);
+      *reinterpret_cast<float4*>(P.imp.curvature + pix0) = make_float4(o_cur[0], o_cur[1], o_cur[2], o_cur[3]);
+      *reinterpret_cast<uchar4*>(P.imp.status + pix0) = make_uchar4(o_st[0], o_st[1], o_st[2], o_st[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < KSEG; ++j) {
+        if (gxs + j >= P.W) break;
+        const int64_t p = pix0 + j;
+        P.imp.normal[3 * p + 0] = o_n[j][0];
+        P.imp.normal[3 * p + 1] = o_n[j][1];
+        P.imp.normal[3 * p + 2] = o_n[j][2];
+        P.imp.offset[p] = o_off[j];
+        P.imp.residual[p] = o_res[j];
+        P.imp.curvature[p] = o_cur[j];
+        P.imp.status[p] = o_st[j];
+      }
+    }
+  }
+#endif
+  {
+    // Sliding-sum guard.  A running sum keeps the rounding residue (~eps x value) of every
+    // sample that has left it, so a window far smaller than the samples that slid through its
+    // sums (a few millimetre depths in a column that just held metres) would inherit an error
+    // the reference's direct sums do not have.  Mass that passed through one of this
+    // segment's window sums outside the window: the row pass's 3 leading columns (their
+    // vertical sums of p^2, read back), and with running column sums also the (o - o0)
+    // leading rows of the column segment over 2r + 4 columns, each sample <= the largest p^2
+    // that has left the tile's column sums (s_dmax).  A lower bound of a fitted window's own
+    // sum of p^2 is its centre column's vertical sum, which holds the centre sample (columns
+    // whose exact valid count is 0 belong to unfitted pixels and are skipped: their running
+    // sums hold nothing but residue).  When the departed mass exceeds 2^20 x that bound
+    // (millimetre depths next to metres; realistic scenes stay orders of magnitude below),
+    // the segment's pixels are queued for the slow pass with direct window sums.  All of it
+    // runs after the unrolled loop (no register held through the solve), in whole exponent
+    // steps on the high words of the non-negative doubles (they order like the values).
+    const int* vhi = reinterpret_cast<const int*>(T.vd + (TH + orow) * VRS + vbase) + 1;  // channel 1
+    const int2* cnt = irow + vbase;
+    auto col_hi = [&](int k) { return vhi[2 * ((k & 3) * VQ + (k >> 2))]; };
+    auto col_n = [&](int k) { return cnt[(k & 3) * VQ + (k >> 2)].x & 0xffff; };
+    // log2 of the departed mass, rounded up: 3 x the largest departed column sum ...
+    int te = (max(col_hi(0), max(col_hi(1), col_hi(2))) >> 20) - 1023 + 2;
+    if (!CENTRED) {  // ... and the (o - o0) x (2r + 4) samples that left the column sums
+      // this row's column segment starts at o0 = floor(p TH / parts), p = its segment
+      const int parts = max(1, min(NTHREADS / T.HW_, TH));
+      const int seg = ((orow + 1) * parts + TH - 1) / TH - 1;
+      const int rows = (orow - (seg * TH) / parts) * (2 * r + KSEG);
+      if (rows > 0) te = max(te, 2 * ((int)(s_dmax[T.it & 1] >> 20) - 1023) + 32 - __clz(rows)) + 1;
+    }
+    te -= 20;  // / 2^20
+    const int thr = te < -1022 ? 0 : te > 1023 ? 0x7ff00000 : (te + 1023) << 20;
+    int h1min = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < KSEG; ++j) {
+      const int w = col_hi(j + r);
+      h1min = min(h1min, col_n(j + r) > 0 ? w : 0x7fffffff);  // exact valid count
+    }
+    if (h1min < thr) {
+      const int qi = atomicAdd(s_qn, KSEG);
+      for (int j = 0; j < KSEG && qi + j < QCAP; ++j) s_q[qi + j] = (unsigned short)(Q_DIRECT | (orow * TW + xs + j));
+    }
+  }
+}
+
+// ---- 4. the robust path for the windows the fast solve declined (and the guard's
+// segments, with direct sums), one queued pixel per thread; an overflowing queue (more than
+// QCAP such windows in one tile: hostile inputs) redoes the whole tile that way.  The queue
+// count is read after the barrier that closes the row pass.
+template <int VAR, int RT, bool EXP, bool NOPRIM>
+__device__ __forceinline__ void slow_pass(const TileCtx& T, const KParams& P, const unsigned short* s_q, int nq) {
+  if (nq <= 0) return;
+  const bool all = nq > QCAP;
+  for (int q = T.tid; q < (all ? TW * TH : nq); q += NTHREADS)
+    slow_pixel<VAR, RT, EXP, NOPRIM>(T, P, all ? (Q_DIRECT | q) : s_q[q]);
+}
+
+// Persistent tile kernel.  SP: spaces (bit 0 standard, bit 1 disparity form); USE_TMA;
+// RT > 0: compile-time window radius (all halo geometry and shared-memory offsets fold to
+// constants), RT == 0: runtime radius; EXP: explicit fits compiled in.  Ps / Pd: the
+// standard / disparity-form space's parameters (the same input and geometry, their own
+// outputs and requested formulations).
+template <int SP, bool USE_TMA, int RT, bool EXP>
 __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
-    fit_tile_kernel(const KParams P, const __grid_constant__ CUtensorMap tmap) {
+    fit_tile_kernel(const __grid_constant__ KParams Ps, const __grid_constant__ KParams Pd,
+                    const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_dyn[];
+  const KParams& P = (SP & 1) ? Ps : Pd;  // input and geometry (identical in both)
   // TMA destinations must be 128-byte aligned: align the dynamic base explicitly
   // (pointer arithmetic on the __shared__ array, not integer casts, so every derived
   // pointer stays in the shared window and compiles to LDS/STS rather than generic LD/ST)
   unsigned char* smem_raw = smem_dyn + ((128u - (smem_u32(smem_dyn) & 127u)) & 127u);
+  TileCtx T;
+  T.P = &P;
   const int r = RT > 0 ? RT : P.r;
-  const int HW_ = TW + 2 * r;  // halo width
-  const int HH_ = TH + 2 * r;  // halo height
-  constexpr int NVD = VAR == VAR_DF ? 3 : 5;  // fp64 vertical channels
-  constexpr int NVI = VAR == VAR_DF ? 3 : 1;  // int vertical channels
-  // small compile-time radii: direct column sums with dy centred on each output row;
-  // otherwise running column sums with dy relative to the tile's first row
-  constexpr bool CENTRED = RT > 0 && RT <= 3;
-  const int esz = elem_size(P.dtype);
+  T.r = r;
+  T.HW_ = TW + 2 * r;  // halo width
+  T.HH_ = TH + 2 * r;  // halo height
+  const int HW_ = T.HW_, HH_ = T.HH_;
+  constexpr int NVD = (SP & 1) ? 5 : 3;  // fp64 column-sum channels of the larger space
+  T.esz = elem_size(P.dtype);
+  const int esz = T.esz;
   const int al = 16 / esz;  // TMA box x origin must be 16-byte aligned
-  const int HWP = (HW_ + al - 1 + 7) & ~7;  // TMA box width (covers the alignment shift)
+  T.HWP = (HW_ + al - 1 + 7) & ~7;  // TMA box width (covers the alignment shift)
+  const int HWP = T.HWP;
   const int raw_bytes = USE_TMA ? ((HH_ * HWP * esz + 127) & ~127) : 0;
   unsigned char* raw0 = smem_raw;
   unsigned char* raw1 = smem_raw + raw_bytes;
   // NOPRIM (large compile-time radius): no converted halo tile in shared memory -- the
   // column pass converts raw elements as it reads them, so two CTAs fit per SM
   constexpr bool NOPRIM = noprim_radius(RT) && USE_TMA;
-  double* prim = reinterpret_cast<double*>(smem_raw + 2 * raw_bytes);  // [HH_][HW_]
+  const int nprim = NOPRIM ? 0 : HH_ * HW_;
+  T.pw = reinterpret_cast<double*>(smem_raw + 2 * raw_bytes);  // [HH_][HW_]
+  T.pz = T.pw + ((SP & 2) ? nprim : 0);                         // [HH_][HW_]
   // column sums are stored residue-major: column c at (c % 4) * VQ + c / 4, so the row
   // pass (threads 4 columns apart) reads consecutive addresses -- no bank conflicts.
-  const int VQ = NOPRIM ? (HW_ + 3) / 4 : vq_of(HW_);
-  const int VRS = 4 * VQ;                                                // row stride
-  double* vd = prim + (NOPRIM ? 0 : HH_ * HW_);                          // [NVD][TH][VRS]
-  int* vi = reinterpret_cast<int*>(vd + NVD * TH * VRS);                 // [NVI][TH][VRS]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vi + NVI * TH * VRS + ((NVI * TH * VRS) & 1));
+  T.VQ = NOPRIM ? (HW_ + 3) / 4 : vq_of(HW_);
+  T.VRS = 4 * T.VQ;
+  const int VRS = T.VRS;
+  T.vd = T.pz + ((SP & 1) ? nprim : 0);                              // [NVD][TH][VRS]
+  T.vi = reinterpret_cast<int2*>(T.vd + NVD * TH * VRS);             // [TH][VRS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(T.vi + TH * VRS);
   // explicit fits stage their 4 pixels' outputs in shared memory (7 float4 per thread: the
   // implicit outputs already hold the register budget) and store them as vectors
-  float* xstage = reinterpret_cast<float*>(bars + 2 + ((smem_u32(bars + 2) & 15u) ? 1 : 0));
+  T.xstage = reinterpret_cast<float*>(bars + 2);
 
   const int tid = threadIdx.x;
+  T.tid = tid;
   const int ntx = (P.W + TW - 1) / TW, nty = (P.H + TH - 1) / TH;
   const int64_t total = (int64_t)ntx * nty * P.batch;
   const uint32_t box_bytes = (uint32_t)(HH_ * HWP * esz);
   // running column sums: high word of the largest primary that has left the tile's column
-  // sums (p >= 0, so high words order like the values), double-buffered by tile parity; the
-  // sliding-sum guard's departed-mass bound at the end of the row pass
-  __shared__ unsigned s_dmax[2];
+  // sums (p >= 0, so high words order like the values), per space and double-buffered by
+  // tile parity; the sliding-sum guard's departed-mass bound at the end of the row pass
+  __shared__ unsigned s_dmax[2][2];
   // slow-pass queue (QCAP tile-local pixel indices) and its fill count
   __shared__ unsigned short s_q[QCAP];
   __shared__ int s_qn;
-  constexpr int NH = HSums<VAR>::NH, NHI = HSums<VAR>::NHI;
-  if (tid == 0) s_dmax[0] = s_dmax[1] = 0u, s_qn = 0;
+  if (tid == 0) s_dmax[0][0] = s_dmax[0][1] = s_dmax[1][0] = s_dmax[1][1] = 0u, s_qn = 0;
   __syncthreads();
 
   if (USE_TMA) {
@@ -420,52 +857,34 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   int it = 0;
   for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
     const TileGeom g = tile_of(t, ntx, nty);
+    T.frame = g.frame;
+    T.x0 = g.x0;
+    T.y0 = g.y0;
+    T.it = it;
     const int64_t frame = g.frame;
     const int x0 = g.x0, y0 = g.y0;
+    T.raw = (it & 1) ? raw1 : raw0;
+    T.sx = (x0 - r) - box_x(x0 - r, al);  // raw index shift
+    T.sy = (y0 - r) - max(y0 - r, 0);
 
-    // raw halo element (row, col) of this tile -> fp64 primary (NOPRIM path)
-    const unsigned char* raw = (it & 1) ? raw1 : raw0;
-    const int sx = (x0 - r) - box_x(x0 - r, al), sy = (y0 - r) - max(y0 - r, 0);  // raw index shift
-    auto raw_primary = [&](int row, int col) -> double {
-      if (row + sy < 0 || col + sx < 0) return 0.0;  // left / top of the image
-      bool mask_ok = true;
-      if (P.mask) {
-        const int y = y0 - r + row, x = x0 - r + col;
-        mask_ok = y < P.H && x < P.W && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
-      }
-      const int ri = (row + sy) * HWP + col + sx;
-      return esz == 2   ? primary_masked<VAR>(reinterpret_cast<const unsigned short*>(raw)[ri], mask_ok)
-             : esz == 8 ? primary_masked<VAR>(reinterpret_cast<const double*>(raw)[ri], mask_ok)
-                        : primary_masked<VAR>(reinterpret_cast<const float*>(raw)[ri], mask_ok);
-    };
-
-    // ---- 1. halo tile -> primary
-    if (USE_TMA && NOPRIM) {
+    // ---- 1. halo tile -> primaries
+    if (USE_TMA) {
       const int b = it & 1;
       mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
+      if (!NOPRIM) {
+        if (esz == 2)
+          convert_halo<SP>(T.pw, T.pz, reinterpret_cast<const unsigned short*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P,
+                           frame, x0, y0, r, tid);
+        else if (esz == 8)
+          convert_halo<SP>(T.pw, T.pz, reinterpret_cast<const double*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
+                           x0, y0, r, tid);
+        else
+          convert_halo<SP>(T.pw, T.pz, reinterpret_cast<const float*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
+                           x0, y0, r, tid);
+        __syncthreads();
+      }
       // the other buffer was consumed by the previous tile (its last reads precede the
       // end-of-tile barrier): prefetch the next tile into it now
-      if (tid == 0 && t + gridDim.x < total) {
-        const TileGeom gn = tile_of(t + gridDim.x, ntx, nty);
-        unsigned char* dst = b ? raw0 : raw1;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bars[b ^ 1], box_bytes);
-        tma_load_tile(dst, &tmap, box_x(gn.x0 - r, al), max(gn.y0 - r, 0), (int)gn.frame, &bars[b ^ 1]);
-      }
-    } else if (USE_TMA) {
-      const int b = it & 1;
-      mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
-      if (esz == 2)
-        convert_halo<VAR>(prim, reinterpret_cast<const unsigned short*>(raw), HW_, HH_, HWP, sx, sy, P, frame,
-                          x0, y0, r, tid);
-      else if (esz == 8)
-        convert_halo<VAR>(prim, reinterpret_cast<const double*>(raw), HW_, HH_, HWP, sx, sy, P, frame, x0, y0,
-                          r, tid);
-      else
-        convert_halo<VAR>(prim, reinterpret_cast<const float*>(raw), HW_, HH_, HWP, sx, sy, P, frame, x0, y0,
-                          r, tid);
-      __syncthreads();
-      // the other buffer was consumed in the previous iteration: prefetch the next tile into it
       if (tid == 0 && t + gridDim.x < total) {
         const TileGeom gn = tile_of(t + gridDim.x, ntx, nty);
         unsigned char* dst = b ? raw0 : raw1;
@@ -479,401 +898,46 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
         const bool yin = y >= 0 && y < P.H;
         for (int col = tid & 31; col < HW_; col += 32) {
           const int x = x0 - r + col;
-          double p = 0.0;
+          bool valid = false;
+          double z = 0.0;
           if (yin && x >= 0 && x < P.W) {
             const int64_t off = frame * P.frame_stride + (int64_t)y * P.row_pitch + x;
-            const bool mask_ok =
-                !P.mask || __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
-            p = esz == 2   ? primary_masked<VAR>(__ldg(reinterpret_cast<const unsigned short*>(P.depth) + off), mask_ok)
-                : esz == 8 ? primary_masked<VAR>(__ldg(reinterpret_cast<const double*>(P.depth) + off), mask_ok)
-                           : primary_masked<VAR>(__ldg(reinterpret_cast<const float*>(P.depth) + off), mask_ok);
+            z = esz == 2   ? depth_z(__ldg(reinterpret_cast<const unsigned short*>(P.depth) + off), valid)
+                : esz == 8 ? depth_z(__ldg(reinterpret_cast<const double*>(P.depth) + off), valid)
+                           : depth_z(__ldg(reinterpret_cast<const float*>(P.depth) + off), valid);
+            if (P.mask) valid = valid && __ldg(P.mask + frame * P.out_frame + (int64_t)y * P.W + x) != 0;
           }
-          prim[row * HW_ + col] = p;
+          if (SP & 2) T.pw[row * HW_ + col] = valid ? rcp_fast(z) : 0.0;
+          if (SP & 1) T.pz[row * HW_ + col] = valid ? z : 0.0;
         }
       }
       __syncthreads();
     }
 
-    int dm = 0;  // running column sums: high word of the largest primary that left this thread's sums
-#if RF_ABLATE >= 4
-    if (false)
+    // ---- 2-4 per space: disparity form first, then standard (one column-sum buffer)
+    if constexpr ((SP & 2) != 0) {
+#if RF_ABLATE < 4
+      column_pass<VAR_DF, RT, NOPRIM, true>(T, s_dmax[VAR_DF]);
 #endif
-    // ---- 2. vertical window sums.  Small compile-time radii: every (column,
-    // output row) pair sums its 2r+1 rows directly (short independent chains,
-    // all threads busy).  Otherwise each halo column is split into `parts` row
-    // segments that warm up on their 2r leading rows and then slide down.
-    if constexpr (CENTRED) {
-      // dy is centred on the output row (dy = k - RT, compile-time): the dy-weighted
-      // sums fold into symmetric differences d * (p[RT + d] - p[RT - d]).
-      constexpr int HWc = TW + 2 * RT;
-      constexpr int K = 2 * RT + 1;
-      for (int e = tid; e < TH * HWc; e += NTHREADS) {
-        const int o = e / HWc, col = e - o * HWc;
-        double p[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) p[k] = prim[(o + k) * HWc + col];
-        double a[NVD];
-        int bb[NVI];
-        int m = 0;
-        double s0 = p[0];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          m += p[k] > 0.0 ? 1 : 0;
-          if (k > 0) s0 += p[k];
-        }
-        double s2 = p[RT + 1] - p[RT - 1];
-#pragma unroll
-        for (int d = 2; d <= RT; ++d) s2 = fma((double)d, p[RT + d] - p[RT - d], s2);
-        if (VAR == VAR_DF) {
-          double s1 = p[0] * p[0];
-#pragma unroll
-          for (int k = 1; k < K; ++k) s1 = fma(p[k], p[k], s1);
-          int my = 0, myy = 0;
-#pragma unroll
-          for (int d = 1; d <= RT; ++d) {
-            const int vp = p[RT + d] > 0.0 ? 1 : 0, vm = p[RT - d] > 0.0 ? 1 : 0;
-            my += d * (vp - vm);
-            myy += d * d * (vp + vm);
-          }
-          a[0] = s0;
-          a[1] = s1;
-          a[2] = s2;
-          bb[0] = m;
-          bb[1] = my;
-          bb[2] = myy;
-        } else {
-          double q[K];
-#pragma unroll
-          for (int k = 0; k < K; ++k) q[k] = p[k] * p[k];
-          double s1 = q[0];
-#pragma unroll
-          for (int k = 1; k < K; ++k) s1 += q[k];
-          double s3 = q[RT + 1] - q[RT - 1], s4 = q[RT + 1] + q[RT - 1];
-#pragma unroll
-          for (int d = 2; d <= RT; ++d) {
-            s3 = fma((double)d, q[RT + d] - q[RT - d], s3);
-            s4 = fma((double)(d * d), q[RT + d] + q[RT - d], s4);
-          }
-          a[0] = s0;
-          a[1] = s1;
-          a[2] = s2;
-          a[3] = s3;
-          a[4] = s4;
-          bb[0] = m;
-        }
-        const int cpos = (col & 3) * VQ + (col >> 2);
-#pragma unroll
-        for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * VRS + cpos] = a[k];
-#pragma unroll
-        for (int k = 0; k < NVI; ++k) vi[(k * TH + o) * VRS + cpos] = bb[k];
-      }
-    } else {
-      const int parts = max(1, min(NTHREADS / HW_, TH));
-      const int col = tid % HW_;
-      const int part = tid / HW_;
-      if (part < parts) {
-        const int o0 = (part * TH) / parts, o1 = ((part + 1) * TH) / parts;  // output rows [o0, o1)
-        double a[NVD];
-        int bb[NVI];
-#pragma unroll
-        for (int k = 0; k < NVD; ++k) a[k] = 0.0;
-#pragma unroll
-        for (int k = 0; k < NVI; ++k) bb[k] = 0;
-        // dy of input row ii is ii - r (origin: the tile's first output row)
-        auto add = [&](int ii, double fdy, int dy, double sg) {
-          const double p = NOPRIM ? raw_primary(ii, col) : prim[ii * HW_ + col];
-          const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
-          if (sg < 0.0) dm = max(dm, __double2hiint(p));  // p >= 0: high words order like values
-          if (VAR == VAR_DF) {
-            a[0] = fma(sg, p, a[0]);
-            a[1] = fma(sg * p, p, a[1]);
-            a[2] = fma(sg * fdy, p, a[2]);
-            bb[0] += v;
-            bb[1] += v * dy;
-            bb[2] += v * dy * dy;
-          } else {
-            const double p2 = p * p;
-            const double sfdy = sg * fdy;
-            a[0] = fma(sg, p, a[0]);
-            a[1] = fma(sg, p2, a[1]);
-            a[2] = fma(sfdy, p, a[2]);
-            a[3] = fma(sfdy, p2, a[3]);
-            a[4] = fma(sfdy * fdy, p2, a[4]);
-            bb[0] += v;
-          }
-        };
-        // window of output row o covers input rows [o, o + 2r]
-        double fdy = (double)(o0 - r);
-        for (int ii = o0; ii < o0 + 2 * r; ++ii, fdy += 1.0) add(ii, fdy, ii - r, 1.0);
-        double fdy_lo = (double)(o0 - r);
-        const int cpos = (col & 3) * VQ + (col >> 2);
-        for (int o = o0; o < o1; ++o, fdy += 1.0, fdy_lo += 1.0) {
-          add(o + 2 * r, fdy, o + r, 1.0);
-#pragma unroll
-          for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * VRS + cpos] = a[k];
-#pragma unroll
-          for (int k = 0; k < NVI; ++k) vi[(k * TH + o) * VRS + cpos] = bb[k];
-          add(o, fdy_lo, o - r, -1.0);
-        }
+      __syncthreads();
+      row_pass<VAR_DF, RT, EXP, NOPRIM>(T, Pd, s_dmax[VAR_DF], s_q, &s_qn);
+      __syncthreads();  // queue complete
+      slow_pass<VAR_DF, RT, EXP, NOPRIM>(T, Pd, s_q, s_qn);
+      if constexpr ((SP & 1) != 0) {
+        __syncthreads();  // column sums and queue are reused by the standard space
+        if (tid == 0) s_qn = 0;
       }
     }
-    if constexpr (!CENTRED) {
-      const unsigned b = __reduce_max_sync(0xffffffffu, (unsigned)dm);  // dm >= 0
-      if ((tid & 31) == 0) atomicMax(&s_dmax[it & 1], b);
+    if constexpr ((SP & 1) != 0) {
+#if RF_ABLATE < 4
+      column_pass<VAR_STD, RT, NOPRIM, (SP & 2) == 0>(T, s_dmax[VAR_STD]);
+#endif
+      __syncthreads();
+      row_pass<VAR_STD, RT, EXP, NOPRIM>(T, Ps, s_dmax[VAR_STD], s_q, &s_qn);
+      __syncthreads();  // queue complete
+      slow_pass<VAR_STD, RT, EXP, NOPRIM>(T, Ps, s_q, s_qn);
     }
-    __syncthreads();
-
-    // ---- 3/4. horizontal running sums + per-window solve
-    {
-      const int orow = tid / (TW / KSEG);
-      const int xs = (tid % (TW / KSEG)) * KSEG;  // tile-local x of the segment's first pixel
-      const int gy = y0 + orow;
-      const int gxs = x0 + xs;
-      if (gy < P.H && gxs < P.W) {
-      const double txo = __ldg(P.tan_x + gxs);
-      const double tyo = __ldg(P.tan_y + (CENTRED ? gy : y0));  // origin row of dy
-      const double ifx = P.ifx, ify = P.ify;
-      const double* vrow = vd + orow * VRS;
-      const int* irow = vi + orow * VRS;
-      const int vstride = TH * VRS;
-      if (!CENTRED && tid == 0) s_dmax[(it + 1) & 1] = 0u;  // read by the previous tile, written by the next
-      // running horizontal sums (origin: segment start xs, tile row y0)
-      double h[NH];
-      int hi[NHI];
-    #pragma unroll
-      for (int k = 0; k < NH; ++k) h[k] = 0.0;
-    #pragma unroll
-      for (int k = 0; k < NHI; ++k) hi[k] = 0;
-
-      // k: column offset from the segment start xs (xs is a multiple of 4, so the
-      // residue-major position of column xs + k is a compile-time offset from vbase)
-      const int vbase = xs >> 2;
-      auto accum = [&](int k, double sgn) {
-        accum_column<VAR>(h, hi, vrow, irow, vstride, vbase + (k & 3) * VQ + (k >> 2), k - r, sgn);
-      };
-
-      if constexpr (RT > 0) {
-#pragma unroll
-        for (int k = 0; k <= 2 * RT; ++k) accum(k, 1.0);
-      } else {
-        for (int k = 0; k <= 2 * r; ++k) accum(k, 1.0);
-      }
-
-      float o_n[KSEG][3], o_off[KSEG], o_res[KSEG], o_cur[KSEG];
-      uint8_t o_st[KSEG];
-
-    #pragma unroll
-      for (int j = 0; j < KSEG; ++j) {
-#if RF_ABLATE < 3
-        if (j > 0) {
-          accum(j + 2 * r, 1.0);
-          accum(j - 1, -1.0);
-        }
-#endif
-        const int gx = gxs + j;
-        const double pc = NOPRIM ? raw_primary(orow + r, xs + j + r) : prim[(orow + r) * HW_ + xs + j + r];
-        uint8_t st = pc > 0.0 ? RF_PIX_INPUT_VALID : 0;
-        const int nwin = (int)hi[0];
-        float nx = __int_as_float(0x7fc00000), ny = nx, nz = nx, off = nx, res = nx, cur = nx;
-        uint8_t stx = st;  // explicit-fit status (MIN_SAMPLES 3 instead of 4)
-        if (st && nwin >= (EXP ? 3 : 4) && gx < P.W) {
-          const double nd = (double)nwin;
-          const double invn = rcp_fast(nd);
-          Sym3 C;
-          double mu0, mu1, mu2;
-          assemble<VAR>(h, hi, txo, tyo, ifx, ify, invn, C, mu0, mu1, mu2);
-          float kap = 0.0f;
-          if (P.do_imp && nwin >= 4) {
-          WindowFit f;
-#if RF_ABLATE >= 1
-          f.lam = C.c00 + C.c11; f.u0 = mu0 + C.c01; f.u1 = mu1 + C.c02; f.u2 = mu2 + C.c12; f.s = C.c22;
-          f.kappa = 0.1f; f.degenerate = false;
-          const bool fast = true;
-#else
-          const bool fast = solve_fast(C, mu0, mu1, mu2, nd, __int2float_rn(nwin), f);
-#endif
-          // windows the fast path declines are solved again by the robust path after the row
-          // pass (slow_pixel), whose outputs overwrite these
-          if (!fast) {
-#ifdef RF_COUNT_SLOW
-            atomicAdd(&g_slow_count[VAR], 1ull);
-#endif
-            const int qi = atomicAdd(&s_qn, 1);
-            if (qi < QCAP) s_q[qi] = (unsigned short)(orow * TW + xs + j);
-          }
-#if RF_ABLATE >= 2
-          nx = (float)f.u0; ny = (float)f.u1; nz = (float)f.u2; off = (float)f.s;
-#else
-          if (VAR == VAR_DF) finish_plane(f.u0, f.u1, f.s, f.u2, nx, ny, nz, off);
-          else finish_plane(f.u0, f.u1, f.u2, f.s, nx, ny, nz, off);
-#endif
-          res = fsqrt(fmaxf((float)(f.lam * invn), 0.0f));
-          cur = f.kappa;
-          kap = f.kappa;
-          st |= RF_PIX_FIT;
-          if (f.degenerate) st |= RF_PIX_DEGENERATE;
-          }
-          if (EXP && P.do_exp) {
-            if (!(P.do_imp && nwin >= 4)) kap = curvature_only(C);
-            ExplicitFit e;
-            explicit_solve(C, mu0, mu1, mu2, nd, e);
-            float ex, ey, ez, eo;
-            // explicit_to_implicit (fitting.py:729-739): standard (a, b, -1, c), rgbd (a, b, c, -1)
-            if (VAR == VAR_DF) finish_plane(e.a, e.b, e.c, -1.0, ex, ey, ez, eo);
-            else finish_plane(e.a, e.b, -1.0, e.c, ex, ey, ez, eo);
-            stx |= RF_PIX_FIT | (e.degenerate ? RF_PIX_DEGENERATE : 0);
-            float* xs_ = xstage + 28 * tid;
-            xs_[3 * j + 0] = ex;
-            xs_[3 * j + 1] = ey;
-            xs_[3 * j + 2] = ez;
-            xs_[12 + j] = eo;
-            xs_[16 + j] = fsqrt(fmaxf((float)(e.ss * invn), 0.0f));
-            xs_[20 + j] = kap;
-          }
-        }
-        if (EXP && P.do_exp) {
-          float* xs_ = xstage + 28 * tid;
-          if (!(stx & RF_PIX_FIT)) {
-            const float qn = __int_as_float(0x7fc00000);
-            xs_[3 * j + 0] = qn;
-            xs_[3 * j + 1] = qn;
-            xs_[3 * j + 2] = qn;
-            xs_[12 + j] = qn;
-            xs_[16 + j] = qn;
-            xs_[20 + j] = qn;
-          }
-          reinterpret_cast<uint8_t*>(xs_ + 24)[j] = stx;
-        }
-        o_n[j][0] = nx;
-        o_n[j][1] = ny;
-        o_n[j][2] = nz;
-        o_off[j] = off;
-        o_res[j] = res;
-        o_cur[j] = cur;
-        o_st[j] = st;
-      }
-
-      if (EXP && P.do_exp) {  // staged explicit outputs -> global, as vectors when aligned
-        const float* xs_ = xstage + 28 * tid;
-        const int64_t pix0 = frame * P.out_frame + (int64_t)gy * P.W + gxs;
-        if (((P.W & (KSEG - 1)) == 0) && (gxs + KSEG <= P.W)) {
-          const float4* sv = reinterpret_cast<const float4*>(xs_);
-          float4* pn = reinterpret_cast<float4*>(P.exp.normal + 3 * pix0);
-          pn[0] = sv[0];
-          pn[1] = sv[1];
-          pn[2] = sv[2];
-          *reinterpret_cast<float4*>(P.exp.offset + pix0) = sv[3];
-          *reinterpret_cast<float4*>(P.exp.residual + pix0) = sv[4];
-          *reinterpret_cast<float4*>(P.exp.curvature + pix0) = sv[5];
-          *reinterpret_cast<uchar4*>(P.exp.status + pix0) = *reinterpret_cast<const uchar4*>(xs_ + 24);
-        } else {
-          for (int j = 0; j < KSEG; ++j) {
-            if (gxs + j >= P.W) break;
-            const int64_t p = pix0 + j;
-            P.exp.normal[3 * p + 0] = xs_[3 * j + 0];
-            P.exp.normal[3 * p + 1] = xs_[3 * j + 1];
-            P.exp.normal[3 * p + 2] = xs_[3 * j + 2];
-            P.exp.offset[p] = xs_[12 + j];
-            P.exp.residual[p] = xs_[16 + j];
-            P.exp.curvature[p] = xs_[20 + j];
-            P.exp.status[p] = reinterpret_cast<const uint8_t*>(xs_ + 24)[j];
-          }
-        }
-      }
-      // ---- stores
-      if (P.do_imp) {
-      const int64_t pix0 = frame * P.out_frame + (int64_t)gy * P.W + gxs;
-      const bool vec = ((P.W & (KSEG - 1)) == 0) && (gxs + KSEG <= P.W);
-      if (vec) {
-        float4* pn = reinterpret_cast<float4*>(P.imp.normal + 3 * pix0);
-        pn[0] = make_float4(o_n[0][0], o_n[0][1], o_n[0][2], o_n[1][0]);
-        pn[1] = make_float4(o_n[1][1], o_n[1][2], o_n[2][0], o_n[2][1]);
-        pn[2] = make_float4(o_n[2][2], o_n[3][0], o_n[3][1], o_n[3][2]);
-        *reinterpret_cast<float4*>(P.imp.offset + pix0) = make_float4(o_off[0], o_off[1], o_off[2], o_off[3]);
-        *reinterpret_cast<float4*>(P.imp.residual + pix0) = make_float4(o_res[0], o_res[1], o_res[2], o_res[3]);
-        *reinterpret_cast<float4*>(P.imp.curvature + pix0) = make_float4(o_cur[0], o_cur[1], o_cur[2], o_cur[3]);
-        *reinterpret_cast<uchar4*>(P.imp.status + pix0) = make_uchar4(o_st[0], o_st[1], o_st[2], o_st[3]);
-      } else {
-    #pragma unroll
-        for (int j = 0; j < KSEG; ++j) {
-          if (gxs + j >= P.W) break;
-          const int64_t p = pix0 + j;
-          P.imp.normal[3 * p + 0] = o_n[j][0];
-          P.imp.normal[3 * p + 1] = o_n[j][1];
-          P.imp.normal[3 * p + 2] = o_n[j][2];
-          P.imp.offset[p] = o_off[j];
-          P.imp.residual[p] = o_res[j];
-          P.imp.curvature[p] = o_cur[j];
-          P.imp.status[p] = o_st[j];
-        }
-      }
-      }
-      {
-        // Sliding-sum guard.  A running sum keeps the rounding residue (~eps x value) of
-        // every sample that has left it, so a window far smaller than the samples that slid
-        // through its sums (a few millimetre depths in a column that just held metres) would
-        // inherit an error the reference's direct sums do not have.  Mass that passed through
-        // one of this segment's window sums outside the window: the row pass's 3 leading
-        // columns (their vertical sums of p^2, read back), and with running column sums also
-        // the (o - o0) leading rows of the column segment over 2r + 4 columns, each sample
-        // <= the largest p^2 that has left the tile's column sums (s_dmax).  A lower bound of
-        // a fitted window's own sum of p^2 is its centre column's vertical sum, which holds
-        // the centre sample (columns whose exact valid count is 0 belong to unfitted pixels
-        // and are skipped: their running sums hold nothing but residue).  When the departed
-        // mass exceeds 2^20 x that bound (millimetre depths next to metres; realistic scenes
-        // stay orders of magnitude below: bench.py's configs queue nothing), the segment's
-        // pixels are queued for the slow pass with direct window sums (slow_pixel).  All of
-        // it runs after the unrolled loop (no register held through the solve), in whole
-        // exponent steps on the high words of the non-negative doubles (they order like the
-        // values; orders of magnitude suffice).
-        // column xs + k of this row sits at vbase + (k & 3) VQ + (k >> 2): compile-time offsets
-        // from one base (xs is a multiple of 4)
-        const int* vhi = reinterpret_cast<const int*>(vd + (TH + orow) * VRS + vbase) + 1;  // channel 1
-        const int* cnt = irow + vbase;
-        auto col_hi = [&](int k) { return vhi[2 * ((k & 3) * VQ + (k >> 2))]; };
-        auto col_n = [&](int k) { return cnt[(k & 3) * VQ + (k >> 2)]; };
-        // log2 of the departed mass, rounded up: 3 x the largest departed column sum ...
-        int te = (max(col_hi(0), max(col_hi(1), col_hi(2))) >> 20) - 1023 + 2;
-        if (!CENTRED) {  // ... and the (o - o0) x (2r + 4) samples that left the column sums
-          // this row's column segment starts at o0 = floor(p TH / parts), p = its segment
-          const int parts = max(1, min(NTHREADS / HW_, TH));
-          const int seg = ((orow + 1) * parts + TH - 1) / TH - 1;
-          const int rows = (orow - (seg * TH) / parts) * (2 * r + KSEG);
-          if (rows > 0) te = max(te, 2 * ((int)(s_dmax[it & 1] >> 20) - 1023) + 32 - __clz(rows)) + 1;
-        }
-        te -= 20;  // / 2^20
-        const int thr = te < -1022 ? 0 : te > 1023 ? 0x7ff00000 : (te + 1023) << 20;
-        int h1min = 0x7fffffff;
-#pragma unroll
-        for (int j = 0; j < KSEG; ++j) {
-          const int w = col_hi(j + r);
-          h1min = min(h1min, col_n(j + r) > 0 ? w : 0x7fffffff);  // exact valid count
-        }
-        if (h1min < thr) {
-          const int qi = atomicAdd(&s_qn, KSEG);
-          for (int j = 0; j < KSEG && qi + j < QCAP; ++j)
-            s_q[qi + j] = (unsigned short)(Q_DIRECT | (orow * TW + xs + j));
-        }
-      }
-      }
-    }
-    __syncthreads();  // queue complete
-    // ---- 5. the robust path for the windows the fast solve declined (and the guard's
-    // segments, with direct sums), one queued pixel per thread; an overflowing queue (more
-    // than QCAP such windows in one tile: hostile inputs) redoes the whole tile that way
-    {
-      const int nq = s_qn;
-      if (nq > 0) {
-        const bool all = nq > QCAP;
-        for (int q = tid; q < (all ? TW * TH : nq); q += NTHREADS) {
-          const int e = all ? (Q_DIRECT | q) : s_q[q];
-          slow_pixel<VAR, RT, EXP, NOPRIM>(P, e, frame, x0, y0, r, VQ, VRS, vd, vi, [&](int row, int col) {
-            return NOPRIM ? raw_primary(row, col) : prim[row * HW_ + col];
-          });
-        }
-      }
-    }
-    __syncthreads();  // prim / vd are rewritten by the next tile
+    __syncthreads();  // primaries / column sums are rewritten by the next tile
     if (tid == 0) s_qn = 0;
   }
 }
@@ -897,15 +961,17 @@ __attribute__((format(printf, 2, 3))) rf_status fail(rf_status s, const char* fm
   return s;
 }
 
-size_t smem_bytes(int var, int r, bool tma, int esz, bool exp = false) {
+// dynamic shared memory of fit_tile_kernel<SP, tma, r> (the kernel's own layout)
+size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false) {
   const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
-  const int nvd = var == VAR_DF ? 3 : 5, nvi = var == VAR_DF ? 3 : 1;
+  const int nvd = (sp & 1) ? 5 : 3;
+  const int nsp = (sp & 1) + ((sp >> 1) & 1);
   const bool noprim = tma && noprim_radius(r);  // matches the kernel's NOPRIM (RT == r)
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
   const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
-  return 2 * raw + sizeof(double) * ((noprim ? 0 : (size_t)hh * hw) + (size_t)nvd * TH * vrs) +
-         sizeof(int) * (size_t)nvi * TH * vrs + 8 /* align */ + 2 * sizeof(uint64_t) + 128 /* base align */ +
-         (exp ? (size_t)28 * sizeof(float) * NTHREADS + 16 : 0);
+  return 2 * raw + sizeof(double) * ((noprim ? 0 : (size_t)nsp * hh * hw) + (size_t)nvd * TH * vrs) +
+         sizeof(int2) * (size_t)TH * vrs + 2 * sizeof(uint64_t) + 128 /* base align */ +
+         (exp ? (size_t)28 * sizeof(float) * NTHREADS : 0);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
@@ -949,59 +1015,92 @@ bool make_depth_tmap(CUtensorMap* m, const void* depth, int dtype, int64_t batch
   return res == CUDA_SUCCESS;
 }
 
-template <int VAR, bool TMA, int RT>
-cudaError_t launch_var(const KParams& P, const CUtensorMap& tmap, size_t sm, int64_t tiles, cudaStream_t s) {
-  auto kern = P.do_exp ? fit_tile_kernel<VAR, TMA, RT, true> : fit_tile_kernel<VAR, TMA, RT, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, sm);
-  if (per_sm < 1) per_sm = 1;
+// per kernel instantiation: the opt-in shared memory it was last configured for and its
+// occupancy at that size (cudaFuncSetAttribute / the occupancy query run once, not per call)
+struct KernelCache {
+  std::mutex mu;
+  size_t smem = 0;
+  int per_sm = 0;
+};
+
+template <int SP, bool TMA, int RT, bool EXP>
+cudaError_t launch_sp(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, size_t sm, int64_t tiles,
+                      int sms, cudaStream_t s) {
+  auto kern = fit_tile_kernel<SP, TMA, RT, EXP>;
+  static KernelCache kc;
+  int per_sm;
+  {
+    std::lock_guard<std::mutex> lock(kc.mu);
+    if (sm > kc.smem) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      kc.smem = sm;
+      kc.per_sm = 0;
+    }
+    if (kc.per_sm == 0 || sm != kc.smem) {
+      int n = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, NTHREADS, sm);
+      per_sm = n < 1 ? 1 : n;
+      if (sm == kc.smem) kc.per_sm = per_sm;
+    } else {
+      per_sm = kc.per_sm;
+    }
+  }
   const int64_t grid = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
-  kern<<<(unsigned)grid, NTHREADS, sm, s>>>(P, tmap);
+  kern<<<(unsigned)grid, NTHREADS, sm, s>>>(Ps, Pd, tmap);
   return cudaGetLastError();
 }
 
+template <int SP, bool TMA, int RT>
+cudaError_t launch_var(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, size_t sm, int64_t tiles,
+                       int sms, cudaStream_t s) {
+  const bool exp = ((SP & 1) && Ps.do_exp) || ((SP & 2) && Pd.do_exp);
+  return exp ? launch_sp<SP, TMA, RT, true>(Ps, Pd, tmap, sm, tiles, sms, s)
+             : launch_sp<SP, TMA, RT, false>(Ps, Pd, tmap, sm, tiles, sms, s);
+}
+
 // compile-time radii for the BASELINE windows 3, 5, 7, 9, 11, 15, 31; others run generic
-template <int VAR>
-cudaError_t launch_radius(const KParams& P, const CUtensorMap& tmap, size_t sm, int64_t tiles, cudaStream_t s) {
-  switch (P.r) {
-    case 1: return launch_var<VAR, true, 1>(P, tmap, sm, tiles, s);
-    case 2: return launch_var<VAR, true, 2>(P, tmap, sm, tiles, s);
-    case 3: return launch_var<VAR, true, 3>(P, tmap, sm, tiles, s);
-    case 4: return launch_var<VAR, true, 4>(P, tmap, sm, tiles, s);
-    case 5: return launch_var<VAR, true, 5>(P, tmap, sm, tiles, s);
-    case 7: return launch_var<VAR, true, 7>(P, tmap, sm, tiles, s);
-    case 15: return launch_var<VAR, true, 15>(P, tmap, sm, tiles, s);
-    default: return launch_var<VAR, true, 0>(P, tmap, sm, tiles, s);
+template <int SP>
+cudaError_t launch_radius(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, bool tma, size_t sm,
+                          int64_t tiles, int sms, cudaStream_t s) {
+  if (!tma) return launch_var<SP, false, 0>(Ps, Pd, tmap, sm, tiles, sms, s);
+  switch (Ps.r) {
+    case 1: return launch_var<SP, true, 1>(Ps, Pd, tmap, sm, tiles, sms, s);
+    case 2: return launch_var<SP, true, 2>(Ps, Pd, tmap, sm, tiles, sms, s);
+    case 3: return launch_var<SP, true, 3>(Ps, Pd, tmap, sm, tiles, sms, s);
+    case 4: return launch_var<SP, true, 4>(Ps, Pd, tmap, sm, tiles, sms, s);
+    case 5: return launch_var<SP, true, 5>(Ps, Pd, tmap, sm, tiles, sms, s);
+    case 7: return launch_var<SP, true, 7>(Ps, Pd, tmap, sm, tiles, sms, s);
+    case 15: return launch_var<SP, true, 15>(Ps, Pd, tmap, sm, tiles, sms, s);
+    default: return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s);
   }
+}
+
+// per-device attributes, queried once
+struct DeviceInfo {
+  int sms = 0, smem_optin = 0, smem_sm = 0;
+};
+DeviceInfo g_dev_info[64];
+std::mutex g_dev_mu;
+DeviceInfo device_info(int dev) {
+  DeviceInfo d;
+  if (dev >= 0 && dev < 64) {
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    if (g_dev_info[dev].sms == 0) {
+      cudaDeviceGetAttribute(&g_dev_info[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaDeviceGetAttribute(&g_dev_info[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaDeviceGetAttribute(&g_dev_info[dev].smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    }
+    d = g_dev_info[dev];
+  } else {
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&d.smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  }
+  return d;
 }
 
 }  // namespace
-
-// Small batches (a few waves of tiles): the two spaces' kernels run concurrently -- the
-// second on a per-device side stream forked from and joined back into the caller's stream --
-// so that each kernel's tail wave overlaps the other's.  The fork/join enqueue is serialised
-// by a mutex so concurrent callers never wait on each other's fork event.
-struct ForkStream {
-  cudaStream_t aux = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-ForkStream g_fork[64];
-std::mutex g_fork_mu;
-
-bool fork_stream(int dev, ForkStream*& fs) {
-  if (dev < 0 || dev >= 64) return false;
-  fs = &g_fork[dev];
-  if (!fs->aux) {
-    if (cudaStreamCreateWithFlags(&fs->aux, cudaStreamNonBlocking) != cudaSuccess) return false;
-    if (cudaEventCreateWithFlags(&fs->fork, cudaEventDisableTiming) != cudaSuccess) return false;
-    if (cudaEventCreateWithFlags(&fs->join, cudaEventDisableTiming) != cudaSuccess) return false;
-  }
-  return true;
-}
 
 rf_status rf_set_error(rf_status s, const char* msg) {
   snprintf(g_err, sizeof(g_err), "%s", msg);
@@ -1026,10 +1125,23 @@ int32_t rf_debug_slow_counts(unsigned long long* out, int reset) {
 
 const char* rf_last_error(void) { return g_err; }
 
-int32_t rf_launches_per_call(int32_t formulation_mask) {
-  // one tile kernel per space
-  return (((formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) ? 1 : 0) +
-              ((formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) ? 1 : 0));
+int32_t rf_launches_per_call(int32_t formulation_mask, int32_t window, int32_t dtype, int64_t batch,
+                             int32_t height, int32_t width) {
+  // one tile kernel for both spaces on small batches when two such CTAs fit per SM (TMA
+  // path, current device; rf_fit_pixels), else one per space
+  const bool want_std = (formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) != 0;
+  const bool want_df = (formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) != 0;
+  if (!(want_std && want_df)) return (want_std || want_df) ? 1 : 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const DeviceInfo di = device_info(dev);
+  const bool want_exp = (formulation_mask & (RF_EXPLICIT_STANDARD | RF_EXPLICIT_RGBD)) != 0;
+  const size_t sm = smem_bytes(3, window / 2, true, elem_size(dtype), want_exp);
+  const int64_t tiles = (int64_t)((width + TW - 1) / TW) * ((height + TH - 1) / TH) * batch;
+  const bool fused = 2 * (sm + 1024) <= (size_t)di.smem_sm &&
+                     (tiles <= (int64_t)4 * 2 * di.sms || getenv("RF_FUSE") != nullptr) &&
+                     getenv("RF_NO_FUSE") == nullptr;
+  return fused ? 1 : 2;
 }
 
 rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const double* delta_y,
@@ -1137,43 +1249,16 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   const int r = window / 2;
   const int64_t tiles = (int64_t)((W + TW - 1) / TW) * ((H + TH - 1) / TH) * batch;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  CUtensorMap tmap;
-  memset(&tmap, 0, sizeof(tmap));
+  const DeviceInfo di = device_info(t->device);
   const int esz = elem_size(dtype);
-  // TMA double buffers only when both spaces' shared-memory footprint still fits the
-  // opt-in limit (large radii with wide elements fall back to the LDG halo path)
-  int dev = 0, smem_optin = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const bool want_exp = (fmask & (RF_EXPLICIT_STANDARD | RF_EXPLICIT_RGBD)) != 0;
-  const bool tma_fits = smem_bytes(VAR_STD, r, true, esz, want_exp) <= (size_t)smem_optin &&
-                        smem_bytes(VAR_DF, r, true, esz, want_exp) <= (size_t)smem_optin;
-  const bool tma = getenv("RF_DISABLE_TMA") == nullptr && tma_fits &&
-                   make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
-  // one launch per space: standard (implicit/explicit-standard), rgbd (implicit/explicit-rgbd)
-  const bool both = (fmask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) &&
-                    (fmask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD));
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  ForkStream* fs = nullptr;
-  std::unique_lock<std::mutex> fork_lock(g_fork_mu, std::defer_lock);
-  bool fork = both && tiles <= (int64_t)8 * nsm && getenv("RF_NO_FORK") == nullptr;
-  if (fork) {
-    fork_lock.lock();
-    fork = fork_stream(dev, fs);  // no side stream (e.g. device index >= 64): launch in order
-    if (fork) {
-      cudaEventRecord(fs->fork, s);
-      cudaStreamWaitEvent(fs->aux, fs->fork, 0);
-    } else {
-      fork_lock.unlock();
-    }
-  }
+  const bool want_std = (fmask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) != 0;
+  const bool want_df = (fmask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) != 0;
+  // the two spaces' parameters: same input and geometry, their own outputs
+  KParams Pv[2];
   for (int var = 0; var < 2; ++var) {
     const int fi = var == VAR_STD ? RF_FORM_IMPLICIT_STANDARD : RF_FORM_IMPLICIT_RGBD;
     const int fe = var == VAR_STD ? RF_FORM_EXPLICIT_STANDARD : RF_FORM_EXPLICIT_RGBD;
-    const bool di = (fmask >> fi) & 1, de = (fmask >> fe) & 1;
-    if (!di && !de) continue;
-    KParams P;
+    KParams& P = Pv[var];
     memset(&P, 0, sizeof(P));
     P.depth = depth;
     P.mask = mask;
@@ -1188,32 +1273,48 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     P.W = W;
     P.r = r;
     P.dtype = dtype;
-    P.do_imp = di;
-    P.do_exp = de;
-    if (di) P.imp = OutPlanes{outs[fi].normal, outs[fi].offset, outs[fi].residual, outs[fi].curvature, outs[fi].status};
-    if (de) P.exp = OutPlanes{outs[fe].normal, outs[fe].offset, outs[fe].residual, outs[fe].curvature, outs[fe].status};
     P.batch = batch;
-    const size_t sm = smem_bytes(var, r, tma, esz, de);
-    cudaError_t e;
-    const cudaStream_t ls = (fork && var == VAR_DF) ? fs->aux : s;
-    if (t->lat_x)  // non-separable tan maps
-      e = launch_lattice(var, P, t->lat_x, t->lat_y, ls);
-    else if (var == VAR_STD)
-      e = tma ? launch_radius<VAR_STD>(P, tmap, sm, tiles, ls) : launch_var<VAR_STD, false, 0>(P, tmap, sm, tiles, ls);
-    else
-      e = tma ? launch_radius<VAR_DF>(P, tmap, sm, tiles, ls) : launch_var<VAR_DF, false, 0>(P, tmap, sm, tiles, ls);
-    if (e != cudaSuccess) {
-      if (fork) {  // keep the caller's stream joined even on failure
-        cudaEventRecord(fs->join, fs->aux);
-        cudaStreamWaitEvent(s, fs->join, 0);
-      }
-      return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-    }
+    P.do_imp = (fmask >> fi) & 1;
+    P.do_exp = (fmask >> fe) & 1;
+    if (P.do_imp) P.imp = OutPlanes{outs[fi].normal, outs[fi].offset, outs[fi].residual, outs[fi].curvature, outs[fi].status};
+    if (P.do_exp) P.exp = OutPlanes{outs[fe].normal, outs[fe].offset, outs[fe].residual, outs[fe].curvature, outs[fe].status};
   }
-  if (fork) {
-    cudaEventRecord(fs->join, fs->aux);
-    cudaStreamWaitEvent(s, fs->join, 0);
+  cudaError_t e = cudaSuccess;
+  if (t->lat_x) {  // non-separable tan maps: one lattice launch per space
+    if (want_df) e = launch_lattice(VAR_DF, Pv[VAR_DF], t->lat_x, t->lat_y, s);
+    if (e == cudaSuccess && want_std) e = launch_lattice(VAR_STD, Pv[VAR_STD], t->lat_x, t->lat_y, s);
+    return e == cudaSuccess ? RF_OK : fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   }
+  const bool want_exp = (fmask & (RF_EXPLICIT_STANDARD | RF_EXPLICIT_RGBD)) != 0;
+  // TMA when the shared-memory footprint fits the opt-in limit (large radii with wide
+  // elements fall back to the LDG halo path) and the tensor map can address the input
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  const int sp_all = (want_std ? 1 : 0) | (want_df ? 2 : 0);
+  const bool tma = getenv("RF_DISABLE_TMA") == nullptr &&
+                   smem_bytes(sp_all, r, true, esz, want_exp) <= (size_t)di.smem_optin &&
+                   make_depth_tmap(&tmap, depth, dtype, batch, H, W, row_pitch, r);
+  // Both spaces in one launch (one read and conversion of the input, one launch) for small
+  // batches -- at most four waves of tiles, where the launch count and tail waves dominate
+  // (a single frame) -- when two such CTAs still fit per SM.  Large batches run one launch
+  // per space (disparity form first): measured on C2 (64 frames, w5) the fused kernel's
+  // doubled instruction footprint costs more in instruction-fetch stalls (11.6% vs 3.5% of
+  // warp samples) than the shared halo saves (1.20-1.23 vs 1.15 ms per step).
+  const size_t sm_both = smem_bytes(3, r, tma, esz, want_exp);
+  const bool fused = sp_all == 3 && 2 * (sm_both + 1024) <= (size_t)di.smem_sm &&
+                     (tiles <= (int64_t)4 * 2 * di.sms || getenv("RF_FUSE") != nullptr) &&
+                     getenv("RF_NO_FUSE") == nullptr;
+  if (fused) {
+    e = launch_radius<3>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, sm_both, tiles, di.sms, s);
+  } else {
+    if (want_df)
+      e = launch_radius<2>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, smem_bytes(2, r, tma, esz, Pv[VAR_DF].do_exp), tiles,
+                           di.sms, s);
+    if (e == cudaSuccess && want_std)
+      e = launch_radius<1>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, smem_bytes(1, r, tma, esz, Pv[VAR_STD].do_exp), tiles,
+                           di.sms, s);
+  }
+  if (e != cudaSuccess) return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return RF_OK;
 }
 

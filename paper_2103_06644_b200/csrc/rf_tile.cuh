@@ -19,6 +19,9 @@ constexpr int MAX_RADIUS = 32;
 #ifndef RF_ABLATE
 #define RF_ABLATE 0
 #endif
+#ifndef RF_ROW_UNROLL
+#define RF_ROW_UNROLL 1
+#endif
 #ifndef RF_MIN_BLOCKS
 #define RF_MIN_BLOCKS 2
 #endif

@@ -340,8 +340,13 @@ class HostPipeline:
         return self._host_out
 
 
-def launches_per_call(formulations=PIXEL_FORMULATIONS) -> int:
+def launches_per_call(formulations=PIXEL_FORMULATIONS, window: int = 5, dtype=torch.float32,
+                      shape: tuple = (64, 480, 640)) -> int:
+    """Kernel launches one ``fit_pixels`` call over a ``shape`` = (B, H, W) batch issues
+    (separable cameras, current device)."""
     fmask = 0
     for f in formulations:
         fmask |= 1 << _FORM_ID[f]
-    return int(N.load().rf_launches_per_call(fmask))
+    code = {torch.float32: N.RF_DEPTH_F32_M, torch.float64: N.RF_DEPTH_F64_M}.get(dtype, N.RF_DEPTH_U16_MM)
+    B, H, W = shape
+    return int(N.load().rf_launches_per_call(fmask, int(window), code, int(B), int(H), int(W)))

@@ -34,14 +34,24 @@ def test_library_exports_every_symbol():
 
 
 def test_launch_count():
-    # per space: the tile kernel plus the sliding-sum guard's refit launch
+    # one tile kernel per call for one space (implicit and explicit fits share it)
     lib = N.load()
-    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD) == 1
-    assert lib.rf_launches_per_call(N.RF_IMPLICIT_RGBD) == 1
-    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_IMPLICIT_RGBD) == 2
-    # the implicit and explicit fits of one space share a launch
-    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_EXPLICIT_STANDARD) == 1
-    assert lib.rf_launches_per_call(15) == 2
+    f32 = N.RF_DEPTH_F32_M
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD, 5, f32, 64, 480, 640) == 1
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_RGBD, 5, f32, 1, 480, 640) == 1
+    assert lib.rf_launches_per_call(N.RF_IMPLICIT_STANDARD | N.RF_EXPLICIT_STANDARD, 31, f32, 1, 480, 640) == 1
+
+
+@pytest.mark.gpu
+def test_launch_count_fused():
+    # small batches: both spaces in one launch wherever two CTAs fit per SM; large: one per space
+    lib = N.load()
+    f32, u16 = N.RF_DEPTH_F32_M, N.RF_DEPTH_U16_MM
+    both = N.RF_IMPLICIT_STANDARD | N.RF_IMPLICIT_RGBD
+    for window in (3, 5, 7, 9, 11, 31):
+        assert lib.rf_launches_per_call(both, window, f32, 1, 480, 640) == 1, window
+        assert lib.rf_launches_per_call(both, window, f32, 64, 480, 640) == 2, window
+    assert lib.rf_launches_per_call(both, 15, u16, 1, 480, 640) == 1
 
 
 @pytest.mark.parametrize("fx,fy,cx,cy,w,h,msg", [
