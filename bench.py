@@ -5,15 +5,19 @@ Workload (``config.workload``): BASELINE config 2 at the headline window --
 1.425e-3 Z^2, 5% invalid), 5x5 window, both fits (disparity form =
 implicit-rgbd, standard = implicit-standard).  A step is one pass of
 ``fit_pixels`` over the batch; a pixel-fit is one (pixel, formulation) fit, so
-a step is 64 * 307200 * 2 pixel-fits.
+a step is 64 * 307200 * 2 pixel-fits per GPU.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--scaling weak|strong] [--frames F]
 
-N > 1 runs under torchrun, one rank per GPU; every rank fits its own 64-frame
-batch (weak scaling, no collective on the data path); timing is CUDA events
-between two barriers, max over ranks.  ``--impl reference`` times the CPU
-restatement of the reference's fast path (oracle/, integral backend) on the
-host cores instead (rank 0 only).
+N > 1: one rank per GPU over NCCL (the command re-launches itself under
+torch.distributed.run when WORLD_SIZE is unset).  weak (default): every rank fits
+its own 64-frame batch; strong: one 64-frame batch is split into contiguous frame
+ranges (shard.frame_range).  No collective on the data path; timing is CUDA events
+between two barriers, max over ranks.  After the timed region the batch is checked
+against the oracle (``parity`` in the line; exit 3 on a mismatch).  ``--impl
+reference`` times the CPU restatement of the reference's fast path (oracle/,
+integral backend) on the host cores instead (rank 0 only).
 """
 
 from __future__ import annotations
@@ -166,18 +170,20 @@ class ClockSampler:
                 "samples": len(rows), "reasons": reasons}
 
 
-def dist_setup():
+def dist_setup(stub: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    cuda = torch.cuda.is_available() and not stub
     if world > 1:
         import torch.distributed as dist
 
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if torch.cuda.is_available():
+        if cuda:
             torch.cuda.set_device(local)
-        dist.init_process_group(backend=backend)
-    elif torch.cuda.is_available():
+        dist.init_process_group(backend="nccl" if cuda else "gloo")
+        if rank == 0:
+            print(f"bench: process group up, backend {dist.get_backend()}, world {world}", file=sys.stderr, flush=True)
+    elif cuda:
         torch.cuda.set_device(0)
     return world, rank, local
 
@@ -191,8 +197,10 @@ def barrier(world):
 
 def max_over_ranks(x: float, world: int) -> float:
     from paper_2103_06644_b200.shard import max_over_ranks as _max
+    import torch.distributed as dist
 
-    return _max(x, world, "cuda" if torch.cuda.is_available() else "cpu")
+    dev = "cuda" if world > 1 and dist.get_backend() == "nccl" else "cpu"
+    return _max(x, world, dev)
 
 
 # ----------------------------------------------------------------- CPU legs
@@ -261,131 +269,246 @@ def run_reference(args, world, rank):
 
 
 # ----------------------------------------------------------------- GPU leg
+def shard_plan(args, world: int, rank: int):
+    """Frames this rank fits per step and their seeds.  weak: every rank its own FRAMES-frame
+    batch (distinct seeds); strong: one FRAMES-frame batch split into contiguous frame ranges
+    (shard.frame_range), the seeds of the global frame indices."""
+    from paper_2103_06644_b200.shard import frame_range, rank_seed_base
+
+    if args.scaling == "strong":
+        start, stop = frame_range(args.frames, world, rank)
+        return stop - start, rank_seed_base(2, 0) + start, (start, stop)
+    return args.frames, rank_seed_base(2, rank), (0, args.frames)
+
+
+def parity_check(depth, out, cam, forms, rng_seed: int = 7) -> dict:
+    """The timed batch against the oracle (reference naive backend restated in C,
+    fitting.py:757-786 and :339-402): every pixel of the shard's first frame, and 2,000 sampled
+    pixels (uniform + borders + hole edges) of its last frame, both formulations."""
+    import numpy as np
+
+    from oracle.compare import compare
+    from tests.helpers import gpu_flat, oracle_frame
+
+    B, H, W = depth.shape
+    rng = np.random.default_rng(rng_seed)
+    res = {"ok": True, "frames": [0, B - 1], "checks": []}
+    last = depth[B - 1].cpu().numpy()
+    valid = last > 0
+    edge = np.flatnonzero(valid & ~np.roll(valid, 1, axis=1))
+    pix = np.unique(np.concatenate([
+        rng.choice(H * W, 2000, replace=False),
+        np.arange(W), (H - 1) * W + np.arange(W), np.arange(H) * W, np.arange(H) * W + W - 1,
+        rng.choice(edge, min(300, edge.size), replace=False) if edge.size else np.zeros(0, np.int64)]))
+    for frame, sel in ((0, None), (B - 1, pix)):
+        for f in forms:
+            ref = oracle_frame(depth[frame].cpu(), cam, WINDOW, f, pixels=sel)
+            m = compare(gpu_flat(out[f], frame, sel), ref, explicit_fit=f.startswith("explicit"))
+            res["checks"].append({"frame": frame, "form": f, "pixels": m["pixels"], "compared": m["compared"],
+                                  "status_mismatch": m["status_mismatch"],
+                                  "max_normal_rad": m["max_normal_rad"], "max_residual_rel": m["max_residual_rel"],
+                                  "max_curvature_rel": m["max_curvature_rel"], "ok": m["ok"]})
+            res["ok"] = res["ok"] and m["ok"]
+    res["tolerances"] = {"normal_rad": 1e-4, "residual_rel": 1e-4, "curvature_rel": 1e-4, "status_bits": "exact"}
+    return res
+
+
+class _CudaLeg:
+    """The measured path: device-resident batch, CUDA events on the launching stream."""
+
+    def __init__(self, local: int):
+        self.dev = torch.device("cuda", local)
+        self.stream = torch.cuda.current_stream(self.dev)
+
+    def event(self):
+        return torch.cuda.Event(enable_timing=True)
+
+    def record(self, ev):
+        ev.record(self.stream)
+
+    @staticmethod
+    def elapsed(e0, e1) -> float:
+        return e0.elapsed_time(e1)
+
+    def sync(self):
+        torch.cuda.synchronize(self.dev)
+
+
+class _StubLeg:
+    """CPU stand-in for the control-flow tests (tests/test_bench_multirank.py): host tensors,
+    wall-clock 'events', and a torch op in place of the kernel.  Never used for a number."""
+
+    def __init__(self, local: int):
+        self.dev = torch.device("cpu")
+
+    def event(self):
+        return [0.0]
+
+    def record(self, ev):
+        ev[0] = time.perf_counter()
+
+    @staticmethod
+    def elapsed(e0, e1) -> float:
+        return (e1[0] - e0[0]) * 1e3
+
+    def sync(self):
+        pass
+
+
 def run_ours(args, world, rank, local):
     import paper_2103_06644_b200 as rf
     from paper_2103_06644_b200 import scenes
 
-    dev = torch.device("cuda", local)
-    cfg = scenes.CONFIGS[CONFIG_NAME]
-    B, H, W = FRAMES, cfg.height, cfg.width
-    from paper_2103_06644_b200.shard import rank_seed_base
-
-    depth = scenes.render_batch(cfg, frames=B, device=dev, seed_base=rank_seed_base(2, rank))
+    stub = args.stub
+    leg = _StubLeg(local) if stub else _CudaLeg(local)
+    dev = leg.dev
+    cfg = scenes.CONFIGS[CONFIG_NAME] if not stub else scenes.small_config(CONFIG_NAME, 64, 48)
+    H, W = cfg.height, cfg.width
+    B, seed_base, (g0, g1) = shard_plan(args, world, rank)
+    depth = scenes.render_batch(cfg, frames=B, device=dev, seed_base=seed_base)
     cam = rf.CameraIntrinsics(cfg.f, cfg.f, cfg.cx, cfg.cy, W, H)
-    maps = rf.compute_tan_maps(cam, dev)
     forms = rf.PIXEL_FORMULATIONS
-    out = {f: rf.PixelFits.empty(B, H, W, dev) for f in forms}
-    stream = torch.cuda.current_stream(dev)
+    if stub:
+        out = None
 
-    def step():
-        rf.fit_pixels(depth, maps, WINDOW, forms, out=out, stream=stream)
+        def step():
+            return (depth * 2.0).sum()
+    else:
+        maps = rf.compute_tan_maps(cam, dev)
+        out = {f: rf.PixelFits.empty(B, H, W, dev) for f in forms}
 
-    # warm-up
+        def step():
+            rf.fit_pixels(depth, maps, WINDOW, forms, out=out, stream=leg.stream)
+
     for _ in range(max(args.warmup, 3)):
         step()
-    torch.cuda.synchronize()
+    leg.sync()
 
     # ---- device-resident timed region (value): one fit_pixels call per step fits both
     # formulations (rf.launches_per_call launches: one per space at this batch size)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
+    ev = [[leg.event() for _ in range(2)] for _ in range(args.steps)]
+    sampler = None if stub else ClockSampler(local)
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
     barrier(world)
-    torch.cuda.synchronize()
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
-    start.record(stream)
+    leg.sync()
+    start, end = leg.event(), leg.event()
+    leg.record(start)
     for k in range(args.steps):
         e0, e1 = ev[k]
-        e0.record(stream)
-        rf.fit_pixels(depth, maps, WINDOW, forms, out=out, stream=stream)
-        e1.record(stream)
-    end.record(stream)
-    torch.cuda.synchronize()
+        leg.record(e0)
+        step()
+        leg.record(e1)
+    leg.record(end)
+    leg.sync()
     barrier(world)
-    clocks = sampler.stop()
-    ms_total = start.elapsed_time(end)
-    per_call = [e0.elapsed_time(e1) for e0, e1 in ev]
-    ms_total = max_over_ranks(ms_total, world)
+    clocks = sampler.stop() if sampler else None
+    ms_total = max_over_ranks(leg.elapsed(start, end), world)
+    per_call = [leg.elapsed(e0, e1) for e0, e1 in ev]
     ms_step = ms_total / args.steps
-    fits_step = B * H * W * len(forms)
-    value = world * fits_step / (ms_step * 1e-3) / 1e6
+    # whole-job pixel-fits per step: the sum over ranks (weak: world x batch; strong: the batch)
+    total_frames = args.frames * world if args.scaling == "weak" else args.frames
+    fits_step = total_frames * H * W * len(forms)
+    value = fits_step / (ms_step * 1e-3) / 1e6
 
-    # ---- roofline of the dominant kernel (the fused tile kernel: the whole step)
+    # ---- roofline of the dominant kernel: the tile kernel (one launch per space here)
     peak, peak_src = hbm_peak()
-    launches_step = rf.launches_per_call(forms, WINDOW, torch.float32, (B, H, W))
+    launches_step = 1 if stub else rf.launches_per_call(forms, WINDOW, torch.float32, (B, H, W))
     launch_ms = statistics.mean(per_call) / launches_step
     alg_bytes = B * H * W * (BYTES_IN + BYTES_OUT * len(forms)) // launches_step
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     traffic = None
     tr = profiled_traffic()
-    if tr and "fused" in tr:
-        traffic = tr["fused"]
+    if tr and "per_space" in tr:
+        traffic = tr["per_space"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "fit_tile_kernel<SP, TMA, r=2> (one launch per space)",
-                "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": alg_bytes, "launches_per_step": launches_step,
-                "launch_ms": launch_ms, "binding": profiled_pipes("fused")}
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
+                "algorithmic_bytes_per_pixel_fit": (BYTES_IN + BYTES_OUT * len(forms)) / len(forms),
+                "launches_per_step": launches_step, "launch_ms": launch_ms,
+                "binding": profiled_pipes("per_space")}
 
     # ---- end to end through the public API with host buffers (pinned): HostPipeline
-    host_in = depth.cpu().pin_memory()
-    pipe = rf.HostPipeline(maps, WINDOW, forms, chunk_frames=8)
-    h2d = host_in.numel() * host_in.element_size()
-    host_out = pipe.run(host_in)   # warm-up (allocates the pinned outputs and the device ring)
-    d2h = sum(getattr(host_out[f], k).numel() * getattr(host_out[f], k).element_size()
-              for f in forms for k in ("normal", "offset", "residual", "curvature", "status"))
-    pipe.run(host_in)
-    torch.cuda.synchronize()
-    barrier(world)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        pipe.run(host_in)          # returns once the step's outputs are in host memory
-    torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3
-    e2e_ms = max_over_ranks(e2e_ms, world)
-    e2e_value = world * fits_step * args.steps / (e2e_ms * 1e-3) / 1e6
-    link = link_bandwidth(host_out, out, forms, pipe.d2h)
+    e2e = None
+    if not stub:
+        host_in = depth.cpu().pin_memory()
+        pipe = rf.HostPipeline(maps, WINDOW, forms, chunk_frames=8)
+        h2d = host_in.numel() * host_in.element_size()
+        host_out = pipe.run(host_in)   # warm-up (allocates the pinned outputs and the device ring)
+        d2h = sum(getattr(host_out[f], k).numel() * getattr(host_out[f], k).element_size()
+                  for f in forms for k in ("normal", "offset", "residual", "curvature", "status"))
+        pipe.run(host_in)
+        leg.sync()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pipe.run(host_in)          # returns once the step's outputs are in host memory
+        leg.sync()
+        e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
+        e2e_value = fits_step * args.steps / (e2e_ms * 1e-3) / 1e6
+        link = link_bandwidth(host_out, out, forms, pipe.d2h)
+        e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world if args.scaling == "weak" else None,
+               "d2h_bytes_per_step": d2h * world if args.scaling == "weak" else None,
+               "h2d_bytes_per_step_per_gpu": h2d, "d2h_bytes_per_step_per_gpu": d2h,
+               "note": "rf.HostPipeline per rank: pinned host in/out, 8-frame chunks, H2D / fit / D2H on three "
+                       "streams; each GPU's own PCIe link",
+               "d2h_gbs_achieved_per_gpu": d2h * args.steps / (e2e_ms * 1e-3) / 1e9,
+               "d2h_gbs_plain_copy": link,
+               "bound": "PCIe device-to-host copy of the outputs (25 B per pixel-fit)"}
+        if args.scaling == "strong":
+            e2e["h2d_bytes_per_step"] = args.frames * H * W * BYTES_IN
+            e2e["d2h_bytes_per_step"] = args.frames * H * W * BYTES_OUT * len(forms)
+        del host_in, host_out, pipe
 
-    launches = rf.launches_per_call(forms) * args.steps
+    launches = 0 if stub else rf.launches_per_call(forms, WINDOW, torch.float32, (B, H, W)) * args.steps
+
+    # ---- the timed batch, checked against the oracle (outside the timed region)
+    parity = None
+    if not stub and not args.no_parity and rank == 0:
+        parity = parity_check(depth, out, cam, forms)
 
     sweep = None
-    if rank == 0 and not args.no_sweep:
-        del host_in, host_out, pipe
+    if rank == 0 and not args.no_sweep and not stub:
         torch.cuda.empty_cache()
         sweep = config_sweep(dev, peak)
 
     cpu_baseline = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not stub:
         frames_host = depth[:4].cpu()
         r, cores, el, sample = cpu_reference_rate(frames_host, cfg, args.cpu_seconds)
         r1, _, _, sample1 = cpu_reference_rate(frames_host, cfg, 0.5, threads=1)
         cpu_baseline = {"value": r / 1e6, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
                         "value_1core": r1 / 1e6, "sample_1core": sample1, "host": host_cpu()}
 
+    shards = [list(shard_plan(args, world, r)[2]) for r in range(world)]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded 16-cell Voronoi planes, sigma=1.425e-3 Z^2, 5% invalid; BASELINE config 2)",
-            "config": {"workload": "C2: 64x640x480 f32 depth per GPU, window 5, implicit-rgbd + implicit-standard",
-                       "frames_per_gpu": B, "window": WINDOW, "pixel_fits_per_step_per_gpu": fits_step,
-                       "l2": "no flush: 79 MB in + 983 MB out per step > 126 MB L2",
-                       "launches_per_step": launches_step,
-                       "frames_per_s": world * B / (ms_step * 1e-3)},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded 16-cell Voronoi planes, sigma=1.425e-3 Z^2, 5% invalid; BASELINE config 2)"
+                    + (" [STUB: control-flow test, not a measurement]" if stub else ""),
+            "config": {"workload": f"C2: {args.frames}x{H}x{W} f32 depth "
+                                   + ("per GPU" if args.scaling == "weak" else "sharded over the GPUs")
+                                   + ", window 5, implicit-rgbd + implicit-standard",
+                       "frames_per_step": total_frames, "frame_shards": shards, "window": WINDOW,
+                       "pixel_fits_per_step": fits_step,
+                       "l2": "no flush: 79 MB in + 983 MB out per GPU per step > 126 MB L2",
+                       "launches_per_step_per_gpu": launches_step,
+                       "frames_per_s": total_frames / (ms_step * 1e-3)},
             "roofline": roofline,
             "cpu_baseline": cpu_baseline,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "note": "rf.HostPipeline: pinned host in/out, 8-frame chunks, H2D / fit / D2H on three streams",
-                    "d2h_gbs_achieved": d2h * args.steps / (e2e_ms * 1e-3) / 1e9,
-                    "d2h_gbs_plain_copy": link,
-                    "bound": "PCIe device-to-host copy of the outputs (25 B per pixel-fit)"},
+            "e2e": e2e,
+            "parity": parity,
             "gpu_launches": launches,
             "clocks": clocks,
             "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
+        if parity is not None and not parity["ok"]:
+            print("bench: the timed batch does not match the oracle", file=sys.stderr, flush=True)
+            sys.exit(3)
 
 
 def config_sweep(dev, peak):
@@ -442,28 +565,50 @@ def config_sweep(dev, peak):
     return res
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this command under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    print(f"bench: spawning {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: each GPU fits its own --frames batch; strong: one --frames batch sharded")
+    ap.add_argument("--frames", type=int, default=FRAMES)
     ap.add_argument("--cpu-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the informational per-config sweep")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the timed batch")
+    ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)  # CPU control-flow tests only
     args = ap.parse_args()
+    world_env = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world_env == 0:
+        sys.exit(spawn_ranks(args))
+    if world_env and args.gpus != world_env:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world_env}; measuring {world_env} ranks",
+              file=sys.stderr, flush=True)
     if args.impl == "reference":
         # the reference arm is the host-CPU restatement: rank 0 alone runs it, no process group
         rank = int(os.environ.get("RANK", "0"))
         if rank == 0:
-            run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), 0)
+            run_reference(args, max(world_env, 1), 0)
         return
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(args.stub)
     try:
-        if args.impl == "reference":
-            run_reference(args, world, rank)
-        else:
-            run_ours(args, world, rank, local)
+        run_ours(args, world, rank, local)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -224,8 +224,10 @@ def fit_pixels(
     B, H, W = d.shape
     if (H, W) != (maps.height, maps.width):
         raise ValueError(f"depth {W}x{H} does not match maps {maps.width}x{maps.height}")
+    temps = []  # tensors this call creates on the current stream and the kernel reads on `stream`
     if d.stride(-1) != 1 or (B > 1 and d.stride(0) != d.stride(1) * H):
         d = d.contiguous()
+        temps.append(d)
     dtype = _depth_dtype(d)
     if d.device.index != maps.device:
         raise ValueError(f"depth on cuda:{d.device.index} but maps on cuda:{maps.device}")
@@ -236,17 +238,29 @@ def fit_pixels(
         m = mask.unsqueeze(0) if mask.dim() == 2 else mask
         if tuple(m.shape) != (B, H, W):
             raise ValueError(f"mask shape {tuple(mask.shape)} != depth shape {tuple(depth.shape)}")
-        m = m.to(device=d.device, dtype=torch.uint8).contiguous()
+        m2 = m.to(device=d.device, dtype=torch.uint8).contiguous()
+        if m2.data_ptr() != m.data_ptr():
+            temps.append(m2)
+        m = m2
         mptr = m.data_ptr()
     if out is None:
         out = {f: PixelFits.empty(B, H, W, d.device) for f in formulations}
+        temps += [getattr(out[f], k) for f in formulations for k in ("normal", "offset", "residual", "curvature",
+                                                                     "status")]
     fmask = 0
     outs = (N.RfPixelOut * N.RF_NUM_FORMULATIONS)()
     for f in formulations:
         fmask |= 1 << _FORM_ID[f]
         outs[_FORM_ID[f]] = out[f]._c()
+    cur = torch.cuda.current_stream(d.device)
     if stream is None:
-        stream = torch.cuda.current_stream(d.device)
+        stream = cur
+    elif stream != cur:
+        # the conversions above ran on the current stream: order the launch after them, and keep
+        # the caching allocator from handing their memory out before `stream` is done with it
+        stream.wait_stream(cur)
+        for t in temps:
+            t.record_stream(stream)
     st = N.load().rf_fit_pixels(
         maps.handle, d.data_ptr(), dtype, B, H, W, d.stride(-2), mptr, int(window), fmask,
         outs, ctypes.c_void_p(stream.cuda_stream),

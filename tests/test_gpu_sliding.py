@@ -83,3 +83,31 @@ def test_sliding_residue(distort, window, dtype, far, near):
         m = compare(_subset(gpu_flat(out[form]), sel), _subset(ref, sel), explicit_fit=form.startswith("explicit"))
         assert m["ok"], f"{form} " + " ".join(f"{k}={m[k]:.3g}" for k in (
             "compared", "status_mismatch", "max_normal_rad", "max_residual_rel", "max_curvature_rel"))
+
+
+@pytest.mark.parametrize("window", [5, 15])
+def test_shared_tables_two_streams(window):
+    """One TanAngleMaps shared by two streams fitting concurrently (different batches, the
+    sliding-residue scene in both directions, rows of repeats so the launches overlap): the
+    tables are immutable and the slow pass lives inside each launch, so both streams match
+    the oracle (SURVEY.md 8b "tables shareable across streams")."""
+    cam = Cam(60.0, 60.0, (W - 1) / 2, (H - 1) / 2, W, H)
+    maps = rf.compute_tan_maps(cam.intrinsics())
+    scenes_ = [_scene(6.0, 1e-3).astype(np.float32), _scene(1e-3, 6.0).astype(np.float32)]
+    depths = [torch.from_numpy(np.stack([z] * 48)).cuda() for z in scenes_]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [{f: rf.PixelFits.empty(48, H, W, "cuda") for f in rf.FORMULATIONS} for _ in range(2)]
+    torch.cuda.synchronize()
+    for _ in range(4):
+        for d, s, o in zip(depths, streams, outs):
+            with torch.cuda.stream(s):
+                rf.fit_pixels(d, maps, window, rf.FORMULATIONS, out=o, stream=s)
+    torch.cuda.synchronize()
+    for z, o, far in zip(scenes_, outs, (6.0, 1e-3)):
+        sel = _single_class(z, window, far)
+        for form in rf.FORMULATIONS:
+            ref = oracle_frame(torch.from_numpy(z), cam, window, form)
+            for frame in (0, 47):
+                m = compare(_subset(gpu_flat(o[form], frame), sel), _subset(ref, sel),
+                            explicit_fit=form.startswith("explicit"))
+                assert m["ok"], (form, frame, m)
