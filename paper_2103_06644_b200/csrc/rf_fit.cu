@@ -28,6 +28,7 @@
 #include <stdarg.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "../../include/rangefit_b200.h"
 #include "rf_internal.h"
@@ -96,7 +97,10 @@ __device__ __forceinline__ void tma_load_tile(void* dst, const CUtensorMap* tmap
 
 // slow-pass queue of one tile (row pass -> slow_pixel): tile-local pixel index, with
 // Q_DIRECT when the window must be re-summed directly (sliding-sum guard)
-constexpr int QCAP = 128;
+constexpr int NWARPS = NTHREADS / 32;
+constexpr int RPW = TH / NWARPS;  // output rows per warp (the row pass: TW / KSEG threads per row)
+static_assert(RPW * NWARPS == TH && (TW / KSEG) * RPW == 32, "a warp owns whole output rows");
+constexpr int QCAP = 64;          // per warp
 constexpr int Q_DIRECT = 0x8000;
 
 // depth element -> Z (metres) and validity (DepthImage, synth.py:84, 111-114)
@@ -339,8 +343,11 @@ __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) 
     constexpr int HWc = TW + 2 * RT;
     constexpr int K = 2 * RT + 1;
     const double* prim = VAR == VAR_DF ? T.pw : T.pz;
-    for (int e = tid; e < TH * HWc; e += NTHREADS) {
-      const int o = e / HWc, col = e - o * HWc;
+    // warp-local: each warp sums the rows its own row pass reads (no CTA barrier between)
+    const int o0 = (tid >> 5) * RPW;
+    for (int e = tid & 31; e < RPW * HWc; e += 32) {
+      const int oo = e / HWc, col = e - oo * HWc;
+      const int o = o0 + oo;
       double p[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) p[k] = prim[(o + k) * HWc + col];
@@ -765,15 +772,16 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
 }
 
 // ---- 4. the robust path for the windows the fast solve declined (and the guard's
-// segments, with direct sums), one queued pixel per thread; an overflowing queue (more than
-// QCAP such windows in one tile: hostile inputs) redoes the whole tile that way.  The queue
-// count is read after the barrier that closes the row pass.
+// segments, with direct sums): each warp takes its own queue right after its row pass, one
+// queued pixel per lane (the column sums it reads are the warp's own rows); an overflowing
+// queue (more than QCAP such windows in the warp's rows: hostile inputs) redoes all of them.
 template <int VAR, int RT, bool EXP, bool NOPRIM>
-__device__ __forceinline__ void slow_pass(const TileCtx& T, const KParams& P, const unsigned short* s_q, int nq) {
+__device__ __forceinline__ void slow_pass(const TileCtx& T, const KParams& P, const unsigned short* q, int nq) {
   if (nq <= 0) return;
   const bool all = nq > QCAP;
-  for (int q = T.tid; q < (all ? TW * TH : nq); q += NTHREADS)
-    slow_pixel<VAR, RT, EXP, NOPRIM>(T, P, all ? (Q_DIRECT | q) : s_q[q]);
+  const int lane = T.tid & 31, pix0 = (T.tid >> 5) * RPW * TW;
+  for (int i = lane; i < (all ? RPW * TW : nq); i += 32)
+    slow_pixel<VAR, RT, EXP, NOPRIM>(T, P, all ? (Q_DIRECT | (pix0 + i)) : q[i]);
 }
 
 // Persistent tile kernel.  SP: spaces (bit 0 standard, bit 1 disparity form); USE_TMA;
@@ -810,15 +818,24 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   // NOPRIM (large compile-time radius): no converted halo tile in shared memory -- the
   // column pass converts raw elements as it reads them, so two CTAs fit per SM
   constexpr bool NOPRIM = noprim_radius(RT) && USE_TMA;
+  // small compile-time radii: warp-local column and row passes; the converted halo is
+  // double-buffered so that the tile's one CTA barrier (after the conversion) also orders the
+  // next conversion after every warp's last read of the buffer it overwrites
+  constexpr bool CENTRED = RT > 0 && RT <= 3;
+  // one space per launch: the double buffer fits two CTAs per SM; both spaces (small
+  // batches) keep one buffer and close the tile with a barrier instead
+  constexpr bool DBUF = CENTRED && SP != 3;
   const int nprim = NOPRIM ? 0 : HH_ * HW_;
-  T.pw = reinterpret_cast<double*>(smem_raw + 2 * raw_bytes);  // [HH_][HW_]
-  T.pz = T.pw + ((SP & 2) ? nprim : 0);                         // [HH_][HW_]
+  const int nsp = ((SP & 2) ? 1 : 0) + ((SP & 1) ? 1 : 0);
+  double* prim_base = reinterpret_cast<double*>(smem_raw + 2 * raw_bytes);  // [CENTRED ? 2 : 1][nsp][HH_][HW_]
+  T.pw = prim_base;                              // [HH_][HW_]
+  T.pz = T.pw + ((SP & 2) ? nprim : 0);          // [HH_][HW_]
   // column sums are stored residue-major: column c at (c % 4) * VQ + c / 4, so the row
   // pass (threads 4 columns apart) reads consecutive addresses -- no bank conflicts.
   T.VQ = NOPRIM ? (HW_ + 3) / 4 : vq_of(HW_);
   T.VRS = 4 * T.VQ;
   const int VRS = T.VRS;
-  T.vd = T.pz + ((SP & 1) ? nprim : 0);                              // [NVD][TH][VRS]
+  T.vd = prim_base + (DBUF ? 2 : 1) * nsp * nprim;                   // [NVD][TH][VRS]
   T.vi = reinterpret_cast<int2*>(T.vd + NVD * TH * VRS);             // [TH][VRS]
   uint64_t* bars = reinterpret_cast<uint64_t*>(T.vi + TH * VRS);
   // explicit fits stage their 4 pixels' outputs in shared memory (7 float4 per thread: the
@@ -835,9 +852,12 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   // tile parity; the sliding-sum guard's departed-mass bound at the end of the row pass
   __shared__ unsigned s_dmax[2][2];
   // slow-pass queue (QCAP tile-local pixel indices) and its fill count
-  __shared__ unsigned short s_q[QCAP];
-  __shared__ int s_qn;
-  if (tid == 0) s_dmax[0][0] = s_dmax[0][1] = s_dmax[1][0] = s_dmax[1][1] = 0u, s_qn = 0;
+  // per-warp slow-pass queues (QCAP pixel indices of the warp's rows) and their fill counts
+  __shared__ unsigned short s_q[NWARPS][QCAP];
+  __shared__ int s_qn[NWARPS];
+  const int warp = tid >> 5;
+  if (tid == 0) s_dmax[0][0] = s_dmax[0][1] = s_dmax[1][0] = s_dmax[1][1] = 0u;
+  if (tid < NWARPS) s_qn[tid] = 0;
   __syncthreads();
 
   if (USE_TMA) {
@@ -864,6 +884,10 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     const int64_t frame = g.frame;
     const int x0 = g.x0, y0 = g.y0;
     T.raw = (it & 1) ? raw1 : raw0;
+    if (DBUF) {
+      T.pw = prim_base + (it & 1) * nsp * nprim;
+      T.pz = T.pw + ((SP & 2) ? nprim : 0);
+    }
     T.sx = (x0 - r) - box_x(x0 - r, al);  // raw index shift
     T.sy = (y0 - r) - max(y0 - r, 0);
 
@@ -914,31 +938,29 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       __syncthreads();
     }
 
-    // ---- 2-4 per space: disparity form first, then standard (one column-sum buffer)
-    if constexpr ((SP & 2) != 0) {
+    // ---- 2-4 per space: disparity form first, then standard (one column-sum buffer).
+    // Small radii: all warp-local after the conversion's barrier.  Running column sums are
+    // CTA-wide (a column segment spans many warps' rows): barriers around them.
+    auto space = [&](auto var_tag, const KParams& Pv, bool counts) {
+      constexpr int VAR = decltype(var_tag)::value;
 #if RF_ABLATE < 4
-      column_pass<VAR_DF, RT, NOPRIM, true>(T, s_dmax[VAR_DF]);
+      if (counts) column_pass<VAR, RT, NOPRIM, true>(T, s_dmax[VAR]);
+      else column_pass<VAR, RT, NOPRIM, false>(T, s_dmax[VAR]);
 #endif
-      __syncthreads();
-      row_pass<VAR_DF, RT, EXP, NOPRIM>(T, Pd, s_dmax[VAR_DF], s_q, &s_qn);
-      __syncthreads();  // queue complete
-      slow_pass<VAR_DF, RT, EXP, NOPRIM>(T, Pd, s_q, s_qn);
-      if constexpr ((SP & 1) != 0) {
-        __syncthreads();  // column sums and queue are reused by the standard space
-        if (tid == 0) s_qn = 0;
-      }
-    }
-    if constexpr ((SP & 1) != 0) {
-#if RF_ABLATE < 4
-      column_pass<VAR_STD, RT, NOPRIM, (SP & 2) == 0>(T, s_dmax[VAR_STD]);
-#endif
-      __syncthreads();
-      row_pass<VAR_STD, RT, EXP, NOPRIM>(T, Ps, s_dmax[VAR_STD], s_q, &s_qn);
-      __syncthreads();  // queue complete
-      slow_pass<VAR_STD, RT, EXP, NOPRIM>(T, Ps, s_q, s_qn);
-    }
-    __syncthreads();  // primaries / column sums are rewritten by the next tile
-    if (tid == 0) s_qn = 0;
+      if (CENTRED) __syncwarp();
+      else __syncthreads();
+      row_pass<VAR, RT, EXP, NOPRIM>(T, Pv, s_dmax[VAR], s_q[warp], &s_qn[warp]);
+      __syncwarp();  // the warp's queue is complete
+      const int nq = s_qn[warp];
+      slow_pass<VAR, RT, EXP, NOPRIM>(T, Pv, s_q[warp], nq);
+      __syncwarp();  // every lane has read the count
+      if ((tid & 31) == 0) s_qn[warp] = 0;
+      if (!CENTRED) __syncthreads();  // the next column pass rewrites every warp's rows
+    };
+    if constexpr ((SP & 2) != 0) space(std::integral_constant<int, VAR_DF>(), Pd, true);
+    if constexpr ((SP & 1) != 0) space(std::integral_constant<int, VAR_STD>(), Ps, (SP & 2) == 0);
+    if (CENTRED && !DBUF) __syncthreads();  // the single halo buffer is rewritten next
+    else if (CENTRED) __syncwarp();
   }
 }
 
@@ -967,9 +989,10 @@ size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false) {
   const int nvd = (sp & 1) ? 5 : 3;
   const int nsp = (sp & 1) + ((sp >> 1) & 1);
   const bool noprim = tma && noprim_radius(r);  // matches the kernel's NOPRIM (RT == r)
+  const bool centred = tma && r >= 1 && r <= 3 && sp != 3;  // the kernel's DBUF: double-buffered halo
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
   const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
-  return 2 * raw + sizeof(double) * ((noprim ? 0 : (size_t)nsp * hh * hw) + (size_t)nvd * TH * vrs) +
+  return 2 * raw + sizeof(double) * ((noprim ? 0 : (centred ? 2 : 1) * (size_t)nsp * hh * hw) + (size_t)nvd * TH * vrs) +
          sizeof(int2) * (size_t)TH * vrs + 2 * sizeof(uint64_t) + 128 /* base align */ +
          (exp ? (size_t)28 * sizeof(float) * NTHREADS : 0);
 }
