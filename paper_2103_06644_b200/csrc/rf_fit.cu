@@ -144,7 +144,18 @@ __device__ __forceinline__ void convert_halo(double* pw, double* pz, const T* ra
     if (SP & 2) pw[e] = valid ? rcp_fast(z) : 0.0;
     if (SP & 1) pz[e] = valid ? z : 0.0;
   };
-  if (!P.mask && (sx | sy) >= 0) {
+  if (!P.mask && (sx | sy) >= 0 && ((HW_ | HWP | sx) & 1) == 0) {
+    // interior tile, even row geometry: element pairs (one 2-element load, one 16-byte store
+    // per primary), half the index arithmetic
+    for (int e = 2 * tid; e < n; e += 2 * NTHREADS) {
+      const int row = e / HW_, col = e - row * HW_;
+      const T* src = raw + (row + sy) * HWP + col + sx;
+      bool v0, v1;
+      const double z0 = depth_z(src[0], v0), z1 = depth_z(src[1], v1);
+      if (SP & 2) *reinterpret_cast<double2*>(pw + e) = make_double2(v0 ? rcp_fast(z0) : 0.0, v1 ? rcp_fast(z1) : 0.0);
+      if (SP & 1) *reinterpret_cast<double2*>(pz + e) = make_double2(v0 ? z0 : 0.0, v1 ? z1 : 0.0);
+    }
+  } else if (!P.mask && (sx | sy) >= 0) {
 #pragma unroll 2
     for (int e = tid; e < n; e += NTHREADS) {
       const int row = e / HW_, col = e - row * HW_;
@@ -332,7 +343,9 @@ __device__ __forceinline__ double primary_at(const TileCtx& T, int row, int col)
 // its 2r+1 rows directly (short independent chains, all threads busy), dy centred on the
 // output row.  Otherwise each halo column is split into `parts` row segments that warm up on
 // their 2r leading rows and then slide down, dy relative to the tile's first output row.
-template <int VAR, int RT, bool NOPRIM, bool COUNTS>
+// COUNTS: 0 none (the other space already summed them), 1 the valid count only (a
+// standard-form launch), 2 the count and its dy, dy^2 moments (the disparity form needs them)
+template <int VAR, int RT, bool NOPRIM, int COUNTS>
 __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) {
   constexpr int NVD = VAR == VAR_DF ? 3 : 5;
   constexpr bool CENTRED = RT > 0 && RT <= 3;
@@ -391,11 +404,13 @@ __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) 
         int m = 0, my = 0, myy = 0;
 #pragma unroll
         for (int k = 0; k < K; ++k) m += p[k] > 0.0 ? 1 : 0;
+        if (COUNTS == 2) {
 #pragma unroll
-        for (int d = 1; d <= RT; ++d) {
-          const int vp = p[RT + d] > 0.0 ? 1 : 0, vm = p[RT - d] > 0.0 ? 1 : 0;
-          my += d * (vp - vm);
-          myy += d * d * (vp + vm);
+          for (int d = 1; d <= RT; ++d) {
+            const int vp = p[RT + d] > 0.0 ? 1 : 0, vm = p[RT - d] > 0.0 ? 1 : 0;
+            my += d * (vp - vm);
+            myy += d * d * (vp + vm);
+          }
         }
         T.vi[o * VRS + cpos] = pack_counts(m, my, myy);
       }
@@ -432,8 +447,10 @@ __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) 
         if (COUNTS) {
           const int v = p > 0.0 ? (sg > 0.0 ? 1 : -1) : 0;
           m += v;
-          my += v * dy;
-          myy += v * dy * dy;
+          if (COUNTS == 2) {
+            my += v * dy;
+            myy += v * dy * dy;
+          }
         }
       };
       // window of output row o covers input rows [o, o + 2r]
@@ -875,8 +892,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   }
 
   int it = 0;
-  for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-    const TileGeom g = tile_of(t, ntx, nty);
+  TileIter ti(blockIdx.x, gridDim.x, ntx, nty);
+  for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it, ti.advance()) {
+    const TileGeom g = ti.geom();
     T.frame = g.frame;
     T.x0 = g.x0;
     T.y0 = g.y0;
@@ -910,7 +928,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       // the other buffer was consumed by the previous tile (its last reads precede the
       // end-of-tile barrier): prefetch the next tile into it now
       if (tid == 0 && t + gridDim.x < total) {
-        const TileGeom gn = tile_of(t + gridDim.x, ntx, nty);
+        TileIter tn = ti;
+        tn.advance();
+        const TileGeom gn = tn.geom();
         unsigned char* dst = b ? raw0 : raw1;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&bars[b ^ 1], box_bytes);
@@ -941,11 +961,10 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     // ---- 2-4 per space: disparity form first, then standard (one column-sum buffer).
     // Small radii: all warp-local after the conversion's barrier.  Running column sums are
     // CTA-wide (a column segment spans many warps' rows): barriers around them.
-    auto space = [&](auto var_tag, const KParams& Pv, bool counts) {
+    auto space = [&](auto var_tag, auto counts_tag, const KParams& Pv) {
       constexpr int VAR = decltype(var_tag)::value;
 #if RF_ABLATE < 4
-      if (counts) column_pass<VAR, RT, NOPRIM, true>(T, s_dmax[VAR]);
-      else column_pass<VAR, RT, NOPRIM, false>(T, s_dmax[VAR]);
+      column_pass<VAR, RT, NOPRIM, decltype(counts_tag)::value>(T, s_dmax[VAR]);
 #endif
       if (CENTRED) __syncwarp();
       else __syncthreads();
@@ -957,8 +976,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       if ((tid & 31) == 0) s_qn[warp] = 0;
       if (!CENTRED) __syncthreads();  // the next column pass rewrites every warp's rows
     };
-    if constexpr ((SP & 2) != 0) space(std::integral_constant<int, VAR_DF>(), Pd, true);
-    if constexpr ((SP & 1) != 0) space(std::integral_constant<int, VAR_STD>(), Ps, (SP & 2) == 0);
+    if constexpr ((SP & 2) != 0) space(std::integral_constant<int, VAR_DF>(), std::integral_constant<int, 2>(), Pd);
+    if constexpr ((SP & 1) != 0)
+      space(std::integral_constant<int, VAR_STD>(), std::integral_constant<int, (SP & 2) ? 0 : 1>(), Ps);
     if (CENTRED && !DBUF) __syncthreads();  // the single halo buffer is rewritten next
     else if (CENTRED) __syncwarp();
   }

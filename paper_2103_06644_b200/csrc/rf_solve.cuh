@@ -651,13 +651,18 @@ __device__ __forceinline__ void finish_plane(double a, double b, double c, doubl
   const double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023 - e)
   const float fa = (float)(a * sc), fb = (float)(b * sc), fc = (float)(c * sc),
               fd = (float)(d * sc);
-  // |u_k| / |u| > 1e-9 on the unit 4-vector, squared (no reciprocal square root)
-  const float e4 = 1e-18f * (fa * fa + fb * fb + fc * fc + fd * fd);
-  float sign = 1.0f;
-  if (fc * fc > e4) sign = fc > 0.0f ? 1.0f : -1.0f;
-  else if (fb * fb > e4) sign = fb > 0.0f ? 1.0f : -1.0f;
-  else if (fa * fa > e4) sign = fa > 0.0f ? 1.0f : -1.0f;
-  else if (fd < 0.0f) sign = -1.0f;
+  // |u_k| / |u| > 1e-9 on the unit 4-vector.  After the rescale the largest component lies
+  // in [1, 2), so 1 <= |u| < 4: |c| >= 4e-9 settles it on c (nearly every window); otherwise
+  // the exact test in order c, b, a, d, squared (no reciprocal square root)
+  float sign = fc > 0.0f ? 1.0f : -1.0f;
+  if (!(fabsf(fc) >= 4e-9f)) {
+    const float e4 = 1e-18f * (fa * fa + fb * fb + fc * fc + fd * fd);
+    sign = 1.0f;
+    if (fc * fc > e4) sign = fc > 0.0f ? 1.0f : -1.0f;
+    else if (fb * fb > e4) sign = fb > 0.0f ? 1.0f : -1.0f;
+    else if (fa * fa > e4) sign = fa > 0.0f ? 1.0f : -1.0f;
+    else if (fd < 0.0f) sign = -1.0f;
+  }
   const float in3 = sign * frsqrt(fa * fa + fb * fb + fc * fc);
   nx = fa * in3;
   ny = fb * in3;

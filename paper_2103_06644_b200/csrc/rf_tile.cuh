@@ -89,6 +89,29 @@ __device__ __forceinline__ TileGeom tile_of(int64_t t, int ntx, int nty) {
   return g;
 }
 
+// The tiles a persistent CTA visits, t = t0, t0 + step, ...: the (frame, tile row, tile
+// column) decomposition is advanced by the step's own decomposition with one carry per
+// digit, so no division runs per tile (two divisions once per CTA)
+struct TileIter {
+  int64_t frame, dframe;
+  int tx, ty, dtx, dty, ntx, nty;
+  __device__ __forceinline__ TileIter(int64_t t0, int64_t step, int ntx_, int nty_) : ntx(ntx_), nty(nty_) {
+    const TileGeom a = tile_of(t0, ntx, nty), d = tile_of(step, ntx, nty);
+    frame = a.frame, ty = a.y0 / TH, tx = a.x0 / TW;
+    dframe = d.frame, dty = d.y0 / TH, dtx = d.x0 / TW;
+  }
+  __device__ __forceinline__ TileGeom geom() const { return TileGeom{frame, tx * TW, ty * TH}; }
+  __device__ __forceinline__ void advance() {
+    tx += dtx;
+    int cy = dty;
+    if (tx >= ntx) tx -= ntx, ++cy;
+    ty += cy;
+    int64_t cf = dframe;
+    if (ty >= nty) ty -= nty, ++cf;
+    frame += cf;
+  }
+};
+
 // launch the per-pixel fits of one space on cameras with distortion lattices (rf_lattice.cu)
 cudaError_t launch_lattice(int var, const KParams& P, const double* lat_x, const double* lat_y,
                            cudaStream_t s);
