@@ -35,6 +35,7 @@
 
 #include "rf_tile.cuh"
 #include "rf_solve.cuh"
+#include "rf_invn.cuh"
 #include "rf_general.cuh"
 #include "rf_direct.cuh"
 
@@ -180,21 +181,37 @@ template <int VAR> struct HSums {
   static constexpr int NHI = VAR == VAR_DF ? 6 : 1;
 };
 
-// valid-count geometry of one column sum: x = count | (sum dy) << 16, y = sum dy^2
-__device__ __forceinline__ int2 pack_counts(int m, int my, int myy) { return make_int2((m & 0xffff) | (my << 16), myy); }
+// valid-count geometry of one column sum (count, sum dy, sum dy^2).  Compile-time radii
+// (r <= 15: count < 32, |sum dy| < 1024, sum dy^2 < 65536) pack it into one int; the generic
+// radius (r <= 32) into an int2.
+__device__ __forceinline__ void pack_counts(int& v, int m, int my, int myy) { v = m | ((my + 1024) << 5) | (myy << 16); }
+__device__ __forceinline__ void pack_counts(int2& v, int m, int my, int myy) { v = make_int2((m & 0xffff) | (my << 16), myy); }
+__device__ __forceinline__ int count_of(int v) { return v & 31; }
+__device__ __forceinline__ int count_of(int2 v) { return v.x & 0xffff; }
+__device__ __forceinline__ void unpack_counts(int v, int& m, int& my, int& myy) {
+  m = v & 31;
+  my = ((v >> 5) & 2047) - 1024;
+  myy = (int)((unsigned)v >> 16);
+}
+__device__ __forceinline__ void unpack_counts(int2 v, int& m, int& my, int& myy) {
+  m = v.x & 0xffff;
+  my = v.x >> 16;
+  myy = v.y;
+}
+template <int RT> using CountT = typename std::conditional<(RT > 0), int, int2>::type;
 
 // add (sgn = +1) or remove (sgn = -1) one column's vertical sums at offset dx from the
 // horizontal origin: disparity form w, w^2, dy w (fp64) and the valid count, dy, dy^2
 // (int); standard form Z, Z^2, dy Z, dy Z^2, dy^2 Z^2 (fp64) and the valid count
-template <int VAR>
-__device__ __forceinline__ void accum_column(double* h, int* hi, const double* vrow, const int2* irow, int vstride,
+template <int VAR, typename VI>
+__device__ __forceinline__ void accum_column(double* h, int* hi, const double* vrow, const VI* irow, int vstride,
                                              int c, int dx, double sgn) {
   const double fdx = (double)dx * sgn;
-  const int2 g = irow[c];
-  const int m = g.x & 0xffff;
+  const VI g = irow[c];
   if (VAR == VAR_DF) {
     const double w = vrow[c], ww = vrow[vstride + c], yw = vrow[2 * vstride + c];
-    const int my = g.x >> 16, myy = g.y;
+    int m, my, myy;
+    unpack_counts(g, m, my, myy);
     h[0] = fma(sgn, w, h[0]);    // sum w
     h[1] = fma(sgn, ww, h[1]);   // sum w^2
     h[2] = fma(sgn, yw, h[2]);   // sum dy w
@@ -219,6 +236,7 @@ __device__ __forceinline__ void accum_column(double* h, int* hi, const double* v
     h[6] = fma(fdx, z2, h[6]);    // S13 = sum dx Z^2
     h[7] = fma(fdx, yz2, h[7]);   // S12 = sum dx dy Z^2
     h[8] = fma(fdx2, z2, h[8]);   // S11 = sum dx^2 Z^2
+    const int m = count_of(g);
     hi[0] += sgn > 0 ? m : -m;
   }
 }
@@ -316,7 +334,7 @@ struct TileCtx {
   double* pw;   // [HH_][HW_] 1/Z (disparity form)
   double* pz;   // [HH_][HW_] Z (standard)
   double* vd;   // [NVD][TH][VRS] column sums of the current space
-  int2* vi;     // [TH][VRS] valid-count geometry (both spaces)
+  void* vi;     // [TH][VRS] valid-count geometry (both spaces), CountT<RT>
   float* xstage;
 };
 
@@ -412,7 +430,7 @@ __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) 
             myy += d * d * (vp + vm);
           }
         }
-        T.vi[o * VRS + cpos] = pack_counts(m, my, myy);
+        pack_counts(static_cast<CountT<RT>*>(T.vi)[o * VRS + cpos], m, my, myy);
       }
     }
   } else {
@@ -462,7 +480,7 @@ __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) 
         add(o + 2 * r, fdy, o + r, 1.0);
 #pragma unroll
         for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * VRS + cpos] = a[k];
-        if (COUNTS) T.vi[o * VRS + cpos] = pack_counts(m, my, myy);
+        if (COUNTS) pack_counts(static_cast<CountT<RT>*>(T.vi)[o * VRS + cpos], m, my, myy);
         add(o, fdy_lo, o - r, -1.0);
       }
     }
@@ -501,7 +519,7 @@ __device__ __forceinline__ void slow_pixel(const TileCtx& T, const KParams& P, i
   } else {
     tyo = __ldg(P.tan_y + (CENTRED ? gy : T.y0));
     const double* vrow = T.vd + orow * T.VRS;
-    const int2* irow = T.vi + orow * T.VRS;
+    const CountT<RT>* irow = static_cast<const CountT<RT>*>(T.vi) + orow * T.VRS;
     for (int k = 0; k <= 2 * r; ++k) {
       const int col = xl + k;
       accum_column<VAR>(h, hi, vrow, irow, TH * T.VRS, (col & 3) * T.VQ + (col >> 2), k - r, 1.0);
@@ -563,7 +581,7 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
   const double tyo = __ldg(P.tan_y + (CENTRED ? gy : T.y0));  // origin row of dy
   const double ifx = P.ifx, ify = P.ify;
   const double* vrow = T.vd + orow * VRS;
-  const int2* irow = T.vi + orow * VRS;
+  const CountT<RT>* irow = static_cast<const CountT<RT>*>(T.vi) + orow * VRS;
   const int vstride = TH * VRS;
   if (!CENTRED && tid == 0) s_dmax[(T.it + 1) & 1] = 0u;  // read by the previous tile, written by the next
   // running horizontal sums (origin: segment start xs, tile row y0)
@@ -610,7 +628,7 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
     uint8_t stx = st;  // explicit-fit status (MIN_SAMPLES 3 instead of 4)
     if (st && nwin >= (EXP ? 3 : 4) && gx < P.W) {
       const double nd = (double)nwin;
-      const double invn = rcp_fast(nd);
+      const double invn = inv_count(nwin);
       Sym3 C;
       double mu0, mu1, mu2;
       assemble<VAR>(h, hi, txo, tyo, ifx, ify, invn, C, mu0, mu1, mu2);
@@ -622,7 +640,7 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
         f.kappa = 0.1f; f.degenerate = false;
         const bool fast = true;
 #else
-        const bool fast = solve_fast(C, mu0, mu1, mu2, nd, __int2float_rn(nwin), f);
+        const bool fast = solve_fast(C, mu0, mu1, mu2, nd, pos_d2f(invn), f);
 #endif
         // windows the fast path declines are solved again by the robust path after the row
         // pass (slow_pixel), whose outputs overwrite these
@@ -761,9 +779,9 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
     // runs after the unrolled loop (no register held through the solve), in whole exponent
     // steps on the high words of the non-negative doubles (they order like the values).
     const int* vhi = reinterpret_cast<const int*>(T.vd + (TH + orow) * VRS + vbase) + 1;  // channel 1
-    const int2* cnt = irow + vbase;
+    const CountT<RT>* cnt = irow + vbase;
     auto col_hi = [&](int k) { return vhi[2 * ((k & 3) * VQ + (k >> 2))]; };
-    auto col_n = [&](int k) { return cnt[(k & 3) * VQ + (k >> 2)].x & 0xffff; };
+    auto col_n = [&](int k) { return count_of(cnt[(k & 3) * VQ + (k >> 2)]); };
     // log2 of the departed mass, rounded up: 3 x the largest departed column sum ...
     int te = (max(col_hi(0), max(col_hi(1), col_hi(2))) >> 20) - 1023 + 2;
     if (!CENTRED) {  // ... and the (o - o0) x (2r + 4) samples that left the column sums
@@ -830,8 +848,11 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   T.HWP = (HW_ + al - 1 + 7) & ~7;  // TMA box width (covers the alignment shift)
   const int HWP = T.HWP;
   const int raw_bytes = USE_TMA ? ((HH_ * HWP * esz + 127) & ~127) : 0;
+  // NOPRIM reads the raw box through the whole tile: two buffers; otherwise the conversion
+  // consumes it before the tile's barrier and the next tile's TMA reuses the one buffer
+  constexpr int NRAW = noprim_radius(RT) && USE_TMA ? 2 : 1;
   unsigned char* raw0 = smem_raw;
-  unsigned char* raw1 = smem_raw + raw_bytes;
+  unsigned char* raw1 = smem_raw + (NRAW - 1) * raw_bytes;
   // NOPRIM (large compile-time radius): no converted halo tile in shared memory -- the
   // column pass converts raw elements as it reads them, so two CTAs fit per SM
   constexpr bool NOPRIM = noprim_radius(RT) && USE_TMA;
@@ -841,10 +862,10 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   constexpr bool CENTRED = RT > 0 && RT <= 3;
   // one space per launch: the double buffer fits two CTAs per SM; both spaces (small
   // batches) keep one buffer and close the tile with a barrier instead
-  constexpr bool DBUF = CENTRED && SP != 3;
+  constexpr bool DBUF = CENTRED && SP != 3 && RF_MIN_BLOCKS < 3;
   const int nprim = NOPRIM ? 0 : HH_ * HW_;
   const int nsp = ((SP & 2) ? 1 : 0) + ((SP & 1) ? 1 : 0);
-  double* prim_base = reinterpret_cast<double*>(smem_raw + 2 * raw_bytes);  // [CENTRED ? 2 : 1][nsp][HH_][HW_]
+  double* prim_base = reinterpret_cast<double*>(smem_raw + NRAW * raw_bytes);  // [DBUF ? 2 : 1][nsp][HH_][HW_]
   T.pw = prim_base;                              // [HH_][HW_]
   T.pz = T.pw + ((SP & 2) ? nprim : 0);          // [HH_][HW_]
   // column sums are stored residue-major: column c at (c % 4) * VQ + c / 4, so the row
@@ -853,8 +874,9 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   T.VRS = 4 * T.VQ;
   const int VRS = T.VRS;
   T.vd = prim_base + (DBUF ? 2 : 1) * nsp * nprim;                   // [NVD][TH][VRS]
-  T.vi = reinterpret_cast<int2*>(T.vd + NVD * TH * VRS);             // [TH][VRS]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(T.vi + TH * VRS);
+  T.vi = T.vd + NVD * TH * VRS;                                        // [TH][VRS] CountT<RT>
+  uint64_t* bars = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(T.vi) +
+                                               ((sizeof(CountT<RT>) * TH * VRS + 7) & ~(size_t)7));
   // explicit fits stage their 4 pixels' outputs in shared memory (7 float4 per thread: the
   // implicit outputs already hold the register budget) and store them as vectors
   T.xstage = reinterpret_cast<float*>(bars + 2);
@@ -1004,17 +1026,20 @@ __attribute__((format(printf, 2, 3))) rf_status fail(rf_status s, const char* fm
 }
 
 // dynamic shared memory of fit_tile_kernel<SP, tma, r> (the kernel's own layout)
+bool compiled_radius(int r) { return r == 1 || r == 2 || r == 3 || r == 4 || r == 5 || r == 7 || r == 15; }
 size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false) {
   const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
   const int nvd = (sp & 1) ? 5 : 3;
   const int nsp = (sp & 1) + ((sp >> 1) & 1);
-  const bool noprim = tma && noprim_radius(r);  // matches the kernel's NOPRIM (RT == r)
-  const bool centred = tma && r >= 1 && r <= 3 && sp != 3;  // the kernel's DBUF: double-buffered halo
+  const bool rt = tma && compiled_radius(r);           // the kernel's RT > 0
+  const bool noprim = tma && noprim_radius(r);         // the kernel's NOPRIM (RT == r)
+  const bool dbuf = rt && r <= 3 && sp != 3 && RF_MIN_BLOCKS < 3;  // the kernel's DBUF
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
   const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
-  return 2 * raw + sizeof(double) * ((noprim ? 0 : (centred ? 2 : 1) * (size_t)nsp * hh * hw) + (size_t)nvd * TH * vrs) +
-         sizeof(int2) * (size_t)TH * vrs + 2 * sizeof(uint64_t) + 128 /* base align */ +
-         (exp ? (size_t)28 * sizeof(float) * NTHREADS : 0);
+  const size_t counts = ((rt ? sizeof(int) : sizeof(int2)) * (size_t)TH * vrs + 7) & ~(size_t)7;
+  return (noprim ? 2 : 1) * raw +
+         sizeof(double) * ((noprim ? 0 : (dbuf ? 2 : 1) * (size_t)nsp * hh * hw) + (size_t)nvd * TH * vrs) + counts +
+         2 * sizeof(uint64_t) + 128 /* base align */ + (exp ? (size_t)28 * sizeof(float) * NTHREADS : 0);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)

@@ -519,7 +519,7 @@ __device__ __forceinline__ void solve_window(const Sym3& C, double m0, double m1
 // a curvature spectrum with both pairs close, lam/n above 1e-2, an adjugate of rank 0, a
 // non-positive upper spectrum, or a gap small enough to ask the degenerate test
 // (fitting.py:552-554).  `out` is then unspecified.
-__device__ __forceinline__ bool solve_fast(const Sym3& C, double m0, double m1, double m2, double n, float fn,
+__device__ __forceinline__ bool solve_fast(const Sym3& C, double m0, double m1, double m2, double n, float finvn,
                                            WindowFit& out) {
   const double c00 = C.c00, c01 = C.c01, c02 = C.c02, c11 = C.c11, c12 = C.c12, c22 = C.c22;
   const double A00 = c11 * c22 - c12 * c12;
@@ -558,7 +558,7 @@ __device__ __forceinline__ bool solve_fast(const Sym3& C, double m0, double m1, 
     trig_cubic2(A2, A1, A0, r1, r2, r3);
     g1 = r1.x, g2 = r2.x, g3 = r3.x, k1 = r1.y, k2 = r2.y, k3 = r3.y;
   }
-  const float grel = g1 * frcp(fn);
+  const float grel = g1 * finvn;
   // curvature: Newton on lam_min from just below k1, or on lam_max from k3 when the bottom
   // pair is close (then lam_1 from lam_1 + lam_2 = t - lam_max, lam_1 lam_2 = det / lam_max)
   const bool top = !((k2 - k1) >= 0.05f * k2);
