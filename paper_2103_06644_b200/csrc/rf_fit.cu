@@ -848,14 +848,16 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   T.HWP = (HW_ + al - 1 + 7) & ~7;  // TMA box width (covers the alignment shift)
   const int HWP = T.HWP;
   const int raw_bytes = USE_TMA ? ((HH_ * HWP * esz + 127) & ~127) : 0;
-  // NOPRIM reads the raw box through the whole tile: two buffers; otherwise the conversion
+  // NOPRIM (the standard space at the largest compile-time radius): no converted Z tile in
+  // shared memory -- its column pass reads the raw box (Z is the stored element), so two
+  // CTAs still fit per SM; the disparity form always converts (1/Z once per element).
+  constexpr bool NOPRIM = noprim_radius(RT) && USE_TMA;  // standard space
+  constexpr int PSP = ((SP & 2) ? 2 : 0) | ((SP & 1) && !NOPRIM ? 1 : 0);  // spaces with converted tiles
+  // a raw box read through the whole tile needs two buffers; otherwise the conversion
   // consumes it before the tile's barrier and the next tile's TMA reuses the one buffer
-  constexpr int NRAW = noprim_radius(RT) && USE_TMA ? 2 : 1;
+  constexpr int NRAW = (SP & 1) && NOPRIM ? 2 : 1;
   unsigned char* raw0 = smem_raw;
   unsigned char* raw1 = smem_raw + (NRAW - 1) * raw_bytes;
-  // NOPRIM (large compile-time radius): no converted halo tile in shared memory -- the
-  // column pass converts raw elements as it reads them, so two CTAs fit per SM
-  constexpr bool NOPRIM = noprim_radius(RT) && USE_TMA;
   // small compile-time radii: warp-local column and row passes; the converted halo is
   // double-buffered so that the tile's one CTA barrier (after the conversion) also orders the
   // next conversion after every warp's last read of the buffer it overwrites
@@ -863,11 +865,11 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   // one space per launch: the double buffer fits two CTAs per SM; both spaces (small
   // batches) keep one buffer and close the tile with a barrier instead
   constexpr bool DBUF = CENTRED && SP != 3 && RF_MIN_BLOCKS < 3;
-  const int nprim = NOPRIM ? 0 : HH_ * HW_;
-  const int nsp = ((SP & 2) ? 1 : 0) + ((SP & 1) ? 1 : 0);
+  const int nprim = HH_ * HW_;
+  const int nsp = ((PSP & 2) ? 1 : 0) + ((PSP & 1) ? 1 : 0);
   double* prim_base = reinterpret_cast<double*>(smem_raw + NRAW * raw_bytes);  // [DBUF ? 2 : 1][nsp][HH_][HW_]
   T.pw = prim_base;                              // [HH_][HW_]
-  T.pz = T.pw + ((SP & 2) ? nprim : 0);          // [HH_][HW_]
+  T.pz = T.pw + ((PSP & 2) ? nprim : 0);         // [HH_][HW_]
   // column sums are stored residue-major: column c at (c % 4) * VQ + c / 4, so the row
   // pass (threads 4 columns apart) reads consecutive addresses -- no bank conflicts.
   T.VQ = NOPRIM ? (HW_ + 3) / 4 : vq_of(HW_);
@@ -926,7 +928,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     T.raw = (it & 1) ? raw1 : raw0;
     if (DBUF) {
       T.pw = prim_base + (it & 1) * nsp * nprim;
-      T.pz = T.pw + ((SP & 2) ? nprim : 0);
+      T.pz = T.pw + ((PSP & 2) ? nprim : 0);
     }
     T.sx = (x0 - r) - box_x(x0 - r, al);  // raw index shift
     T.sy = (y0 - r) - max(y0 - r, 0);
@@ -935,15 +937,15 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     if (USE_TMA) {
       const int b = it & 1;
       mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
-      if (!NOPRIM) {
+      if (PSP != 0) {
         if (esz == 2)
-          convert_halo<SP>(T.pw, T.pz, reinterpret_cast<const unsigned short*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P,
+          convert_halo<PSP>(T.pw, T.pz, reinterpret_cast<const unsigned short*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P,
                            frame, x0, y0, r, tid);
         else if (esz == 8)
-          convert_halo<SP>(T.pw, T.pz, reinterpret_cast<const double*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
+          convert_halo<PSP>(T.pw, T.pz, reinterpret_cast<const double*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
                            x0, y0, r, tid);
         else
-          convert_halo<SP>(T.pw, T.pz, reinterpret_cast<const float*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
+          convert_halo<PSP>(T.pw, T.pz, reinterpret_cast<const float*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
                            x0, y0, r, tid);
         __syncthreads();
       }
@@ -985,15 +987,16 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
     // CTA-wide (a column segment spans many warps' rows): barriers around them.
     auto space = [&](auto var_tag, auto counts_tag, const KParams& Pv) {
       constexpr int VAR = decltype(var_tag)::value;
+      constexpr bool NP = VAR == VAR_STD && NOPRIM;
 #if RF_ABLATE < 4
-      column_pass<VAR, RT, NOPRIM, decltype(counts_tag)::value>(T, s_dmax[VAR]);
+      column_pass<VAR, RT, NP, decltype(counts_tag)::value>(T, s_dmax[VAR]);
 #endif
       if (CENTRED) __syncwarp();
       else __syncthreads();
-      row_pass<VAR, RT, EXP, NOPRIM>(T, Pv, s_dmax[VAR], s_q[warp], &s_qn[warp]);
+      row_pass<VAR, RT, EXP, NP>(T, Pv, s_dmax[VAR], s_q[warp], &s_qn[warp]);
       __syncwarp();  // the warp's queue is complete
       const int nq = s_qn[warp];
-      slow_pass<VAR, RT, EXP, NOPRIM>(T, Pv, s_q[warp], nq);
+      slow_pass<VAR, RT, EXP, NP>(T, Pv, s_q[warp], nq);
       __syncwarp();  // every lane has read the count
       if ((tid & 31) == 0) s_qn[warp] = 0;
       if (!CENTRED) __syncthreads();  // the next column pass rewrites every warp's rows
@@ -1032,13 +1035,14 @@ size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false) {
   const int nvd = (sp & 1) ? 5 : 3;
   const int nsp = (sp & 1) + ((sp >> 1) & 1);
   const bool rt = tma && compiled_radius(r);           // the kernel's RT > 0
-  const bool noprim = tma && noprim_radius(r);         // the kernel's NOPRIM (RT == r)
+  const bool noprim = tma && noprim_radius(r);         // the kernel's NOPRIM (RT == r; standard space)
+  const int psp = nsp - ((sp & 1) && noprim ? 1 : 0);  // spaces with a converted tile
   const bool dbuf = rt && r <= 3 && sp != 3 && RF_MIN_BLOCKS < 3;  // the kernel's DBUF
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
   const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
   const size_t counts = ((rt ? sizeof(int) : sizeof(int2)) * (size_t)TH * vrs + 7) & ~(size_t)7;
-  return (noprim ? 2 : 1) * raw +
-         sizeof(double) * ((noprim ? 0 : (dbuf ? 2 : 1) * (size_t)nsp * hh * hw) + (size_t)nvd * TH * vrs) + counts +
+  return ((sp & 1) && noprim ? 2 : 1) * raw +
+         sizeof(double) * ((dbuf ? 2 : 1) * (size_t)psp * hh * hw + (size_t)nvd * TH * vrs) + counts +
          2 * sizeof(uint64_t) + 128 /* base align */ + (exp ? (size_t)28 * sizeof(float) * NTHREADS : 0);
 }
 
