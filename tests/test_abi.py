@@ -48,8 +48,9 @@ def test_launch_count_fused():
     lib = N.load()
     f32, u16 = N.RF_DEPTH_F32_M, N.RF_DEPTH_U16_MM
     both = N.RF_IMPLICIT_STANDARD | N.RF_IMPLICIT_RGBD
-    for window in (3, 5, 7, 9, 11, 31):
+    for window in (3, 5, 7, 9, 11):
         assert lib.rf_launches_per_call(both, window, f32, 1, 480, 640) == 1, window
+    for window in (3, 5, 7, 9, 11, 15, 31):
         assert lib.rf_launches_per_call(both, window, f32, 64, 480, 640) == 2, window
     assert lib.rf_launches_per_call(both, 15, u16, 1, 480, 640) == 1
 
