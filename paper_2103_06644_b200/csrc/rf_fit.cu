@@ -374,63 +374,84 @@ __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) 
     constexpr int HWc = TW + 2 * RT;
     constexpr int K = 2 * RT + 1;
     const double* prim = VAR == VAR_DF ? T.pw : T.pz;
-    // warp-local: each warp sums the rows its own row pass reads (no CTA barrier between)
+    // warp-local: each warp sums the RPW rows its own row pass reads (no CTA barrier
+    // between); a lane takes whole columns, so its RPW output rows share K + RPW - 1 loads
+    // and, for the plain sums, the K - 1 rows common to neighbouring windows
+    static_assert(RPW == 2, "column-major centred pass written for two rows per warp");
     const int o0 = (tid >> 5) * RPW;
-    for (int e = tid & 31; e < RPW * HWc; e += 32) {
-      const int oo = e / HWc, col = e - oo * HWc;
-      const int o = o0 + oo;
-      double p[K];
+    for (int col = tid & 31; col < HWc; col += 32) {
+      double p[K + 1];
 #pragma unroll
-      for (int k = 0; k < K; ++k) p[k] = prim[(o + k) * HWc + col];
-      double a[NVD];
-      double s0 = p[0];
+      for (int k = 0; k <= K; ++k) p[k] = prim[(o0 + k) * HWc + col];
+      const int cpos = (col & 3) * VQ + (col >> 2);
+      // rows o0 (window p[0..K-1]) and o0 + 1 (p[1..K]); dy centred: symmetric differences
+      double t0 = p[1];
 #pragma unroll
-      for (int k = 1; k < K; ++k) s0 += p[k];
-      double s2 = p[RT + 1] - p[RT - 1];
+      for (int k = 2; k < K; ++k) t0 += p[k];
+      double d0 = p[RT + 1] - p[RT - 1], d1 = p[RT + 2] - p[RT];
 #pragma unroll
-      for (int d = 2; d <= RT; ++d) s2 = fma((double)d, p[RT + d] - p[RT - d], s2);
+      for (int d = 2; d <= RT; ++d) {
+        d0 = fma((double)d, p[RT + d] - p[RT - d], d0);
+        d1 = fma((double)d, p[RT + 1 + d] - p[RT + 1 - d], d1);
+      }
+      double a0[NVD], a1[NVD];
+      a0[0] = p[0] + t0;
+      a1[0] = t0 + p[K];
+      a0[2] = d0;
+      a1[2] = d1;
       if (VAR == VAR_DF) {
-        double s1 = p[0] * p[0];
+        double t1 = p[1] * p[1];
 #pragma unroll
-        for (int k = 1; k < K; ++k) s1 = fma(p[k], p[k], s1);
-        a[0] = s0;
-        a[1] = s1;
-        a[2] = s2;
+        for (int k = 2; k < K; ++k) t1 = fma(p[k], p[k], t1);
+        a0[1] = fma(p[0], p[0], t1);
+        a1[1] = fma(p[K], p[K], t1);
       } else {
-        double q[K];
+        double q[K + 1];
 #pragma unroll
-        for (int k = 0; k < K; ++k) q[k] = p[k] * p[k];
-        double s1 = q[0];
+        for (int k = 0; k <= K; ++k) q[k] = p[k] * p[k];
+        double t1 = q[1];
 #pragma unroll
-        for (int k = 1; k < K; ++k) s1 += q[k];
-        double s3 = q[RT + 1] - q[RT - 1], s4 = q[RT + 1] + q[RT - 1];
+        for (int k = 2; k < K; ++k) t1 += q[k];
+        a0[1] = q[0] + t1;
+        a1[1] = t1 + q[K];
+        double e0 = q[RT + 1] - q[RT - 1], e1 = q[RT + 2] - q[RT];
+        double f0 = q[RT + 1] + q[RT - 1], f1 = q[RT + 2] + q[RT];
 #pragma unroll
         for (int d = 2; d <= RT; ++d) {
-          s3 = fma((double)d, q[RT + d] - q[RT - d], s3);
-          s4 = fma((double)(d * d), q[RT + d] + q[RT - d], s4);
+          e0 = fma((double)d, q[RT + d] - q[RT - d], e0);
+          e1 = fma((double)d, q[RT + 1 + d] - q[RT + 1 - d], e1);
+          f0 = fma((double)(d * d), q[RT + d] + q[RT - d], f0);
+          f1 = fma((double)(d * d), q[RT + 1 + d] + q[RT + 1 - d], f1);
         }
-        a[0] = s0;
-        a[1] = s1;
-        a[2] = s2;
-        a[3] = s3;
-        a[4] = s4;
+        a0[3] = e0;
+        a1[3] = e1;
+        a0[4] = f0;
+        a1[4] = f1;
       }
-      const int cpos = (col & 3) * VQ + (col >> 2);
 #pragma unroll
-      for (int k = 0; k < NVD; ++k) vd[(k * TH + o) * VRS + cpos] = a[k];
+      for (int k = 0; k < NVD; ++k) {
+        vd[(k * TH + o0) * VRS + cpos] = a0[k];
+        vd[(k * TH + o0 + 1) * VRS + cpos] = a1[k];
+      }
       if (COUNTS) {
-        int m = 0, my = 0, myy = 0;
+        int v[K + 1];
 #pragma unroll
-        for (int k = 0; k < K; ++k) m += p[k] > 0.0 ? 1 : 0;
+        for (int k = 0; k <= K; ++k) v[k] = p[k] > 0.0 ? 1 : 0;
+        int mt = 0;
+#pragma unroll
+        for (int k = 1; k < K; ++k) mt += v[k];
+        int my0 = 0, myy0 = 0, my1 = 0, myy1 = 0;
         if (COUNTS == 2) {
 #pragma unroll
           for (int d = 1; d <= RT; ++d) {
-            const int vp = p[RT + d] > 0.0 ? 1 : 0, vm = p[RT - d] > 0.0 ? 1 : 0;
-            my += d * (vp - vm);
-            myy += d * d * (vp + vm);
+            my0 += d * (v[RT + d] - v[RT - d]);
+            myy0 += d * d * (v[RT + d] + v[RT - d]);
+            my1 += d * (v[RT + 1 + d] - v[RT + 1 - d]);
+            myy1 += d * d * (v[RT + 1 + d] + v[RT + 1 - d]);
           }
         }
-        pack_counts(static_cast<CountT<RT>*>(T.vi)[o * VRS + cpos], m, my, myy);
+        pack_counts(static_cast<CountT<RT>*>(T.vi)[o0 * VRS + cpos], mt + v[0], my0, myy0);
+        pack_counts(static_cast<CountT<RT>*>(T.vi)[(o0 + 1) * VRS + cpos], mt + v[K], my1, myy1);
       }
     }
   } else {
