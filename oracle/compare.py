@@ -37,7 +37,7 @@ def normal_angles(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.arctan2(cross, dot)
 
 
-def compare(gpu: dict, ref: dict, explicit_fit: bool = False) -> dict:
+def compare(gpu: dict, ref: dict, explicit_fit: bool = False, include_degenerate: bool = False) -> dict:
     """gpu/ref: dicts of flat arrays normal (P,3), offset, residual, curvature, status (P,);
     ref also carries ``scale`` = ||S||_F/n.  Returns metrics and a pass flag.  Explicit fits
     compute their residual from aggregated sums, sum(b^2) - alpha.rhs, whose cancellation
@@ -48,7 +48,9 @@ def compare(gpu: dict, ref: dict, explicit_fit: bool = False) -> dict:
     status_mismatch = int(((gs & mask_bits) != (rs & mask_bits)).sum())
     fit = ((rs & 2) != 0) & ((gs & 2) != 0)
     degen = ((rs & 4) != 0)
-    sel = fit & ~degen
+    # degenerate implicit windows (eigenvalue near-ties) have no well-defined normal; explicit
+    # ones (failed Cholesky pivots) are the reference's minimum-norm solution and compare too
+    sel = fit if include_degenerate else fit & ~degen
     gn = np.asarray(gpu["normal"], np.float64).reshape(-1, 3)
     rn = np.asarray(ref["normal"], np.float64).reshape(-1, 3)
     ang = normal_angles(gn[sel], rn[sel]) if sel.any() else np.zeros(0)

@@ -17,7 +17,7 @@ SOURCES = [PKG / "csrc" / "rf_fit.cu", PKG / "csrc" / "rf_rects.cu", PKG / "csrc
            PKG / "csrc" / "rf_render.cu", PKG / "csrc" / "rf_lattice.cu"]
 HEADERS = [ROOT / "include" / "rangefit_b200.h", PKG / "csrc" / "rf_solve.cuh", PKG / "csrc" / "rf_internal.h",
            PKG / "csrc" / "rf_tile.cuh", PKG / "csrc" / "rf_general.cuh",
-           PKG / "csrc" / "rf_direct.cuh", PKG / "csrc" / "rf_invn.cuh"]
+           PKG / "csrc" / "rf_direct.cuh", PKG / "csrc" / "rf_invn.cuh", PKG / "csrc" / "rf_jacobi.cuh"]
 OUT = PKG / "librangefit_b200.so"
 
 NVCC_FLAGS = [

@@ -36,6 +36,7 @@
 #include "rf_tile.cuh"
 #include "rf_solve.cuh"
 #include "rf_invn.cuh"
+#include "rf_jacobi.cuh"
 #include "rf_general.cuh"
 #include "rf_direct.cuh"
 
@@ -102,7 +103,9 @@ constexpr int NWARPS = NTHREADS / 32;
 constexpr int RPW = TH / NWARPS;  // output rows per warp (the row pass: TW / KSEG threads per row)
 static_assert(RPW * NWARPS == TH && (TW / KSEG) * RPW == 32, "a warp owns whole output rows");
 constexpr int QCAP = 64;          // per warp
-constexpr int Q_DIRECT = 0x8000;
+constexpr int Q_DIRECT = 0x8000;  // re-sum the window directly (sliding-sum guard)
+constexpr int Q_EXPL = 0x4000;    // only the explicit fit: its Cholesky pivot test failed
+constexpr int Q_PIX = 0x3fff;     // tile-local pixel index
 
 // depth element -> Z (metres) and validity (DepthImage, synth.py:84, 111-114)
 __device__ __forceinline__ double depth_z(float zf, bool& valid) {
@@ -519,8 +522,9 @@ template <int VAR, int RT, bool EXP, bool NOPRIM>
 __device__ __forceinline__ void slow_pixel(const TileCtx& T, const KParams& P, int e) {
   constexpr bool CENTRED = RT > 0 && RT <= 3;
   const int r = T.r;
-  const int pix = e & (Q_DIRECT - 1);
+  const int pix = e & Q_PIX;
   const bool direct = (e & Q_DIRECT) != 0;
+  const bool expl_only = (e & Q_EXPL) != 0 && !direct;
   const int orow = pix / TW, xl = pix % TW;
   const int gy = T.y0 + orow, gx = T.x0 + xl;
   if (gy >= P.H || gx >= P.W) return;
@@ -557,7 +561,7 @@ __device__ __forceinline__ void slow_pixel(const TileCtx& T, const KParams& P, i
   const int64_t p = T.frame * P.out_frame + (int64_t)gy * P.W + gx;
   float kap = 0.0f;
   bool have_kap = false;
-  if (P.do_imp && nwin >= 4) {
+  if (P.do_imp && nwin >= 4 && !expl_only) {
     WindowFit f;
     solve_window<true>(C, mu0, mu1, mu2, nd, f);
     float nx, ny, nz, off;
@@ -570,9 +574,9 @@ __device__ __forceinline__ void slow_pixel(const TileCtx& T, const KParams& P, i
   }
   if (EXP && P.do_exp) {
     if (!have_kap) kap = curvature_only(C);
-    if (direct) {
+    if (direct || expl_only) {
       ExplicitFit ex;
-      explicit_solve(C, mu0, mu1, mu2, nd, ex);
+      explicit_fit_robust(C, mu0, mu1, mu2, nd, ex);
       float a, b, c, d;
       if (VAR == VAR_DF) finish_plane(ex.a, ex.b, ex.c, -1.0, a, b, c, d);
       else finish_plane(ex.a, ex.b, -1.0, ex.c, a, b, c, d);
@@ -688,6 +692,10 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
         if (!(P.do_imp && nwin >= 4)) kap = curvature_only(C);
         ExplicitFit e;
         explicit_solve(C, mu0, mu1, mu2, nd, e);
+        if (e.degenerate) {  // rank-deficient: the minimum-norm solution in the slow pass
+          const int qi = atomicAdd(s_qn, 1);
+          if (qi < QCAP) s_q[qi] = (unsigned short)(Q_EXPL | (orow * TW + xs + j));
+        }
         float ex, ey, ez, eo;
         // explicit_to_implicit (fitting.py:729-739): standard (a, b, -1, c), rgbd (a, b, c, -1)
         if (VAR == VAR_DF) finish_plane(e.a, e.b, e.c, -1.0, ex, ey, ez, eo);

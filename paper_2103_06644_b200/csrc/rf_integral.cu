@@ -26,6 +26,7 @@
 #include "../../include/rangefit_b200.h"
 #include "rf_internal.h"
 #include "rf_solve.cuh"
+#include "rf_jacobi.cuh"
 
 namespace {
 using namespace rf_dev;
@@ -187,65 +188,6 @@ __global__ void box_sums_kernel(const BoxParams P) {
   const double a = t[(int64_t)R.y1 * W1 + R.x1], b = t[(int64_t)R.y0 * W1 + R.x1];
   const double cc = t[(int64_t)R.y1 * W1 + R.x0], d = t[(int64_t)R.y0 * W1 + R.x0];
   P.out[i] = a - b - cc + d;  // evaluated left to right, as the reference
-}
-
-// ---- cyclic Jacobi (jacobi_eigh, fitting.py:193-253): same threshold (1e-13 ||A||_F),
-// same sweep order and rotation formulas, no fused multiply-adds (the reference runs in
-// Python floats); eigenvectors in the columns of v.
-template <int N>
-__device__ bool jacobi(double (&a)[N][N], double (&v)[N][N], double fro) {
-  for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) v[i][j] = i == j ? 1.0 : 0.0;
-  if (fro == 0.0) {
-    for (int i = 0; i < N; ++i) a[i][i] = 0.0;
-    return true;
-  }
-  const double threshold = 1e-13 * fro;
-  auto off_norm = [&]() {
-    double s = 0.0;
-    for (int p = 0; p < N - 1; ++p)
-      for (int q = p + 1; q < N; ++q) s += a[p][q] * a[p][q];
-    return sqrt(2.0 * s);
-  };
-  for (int sweep = 0; sweep < 50; ++sweep) {
-    if (off_norm() <= threshold) return true;
-    for (int p = 0; p < N - 1; ++p) {
-      for (int q = p + 1; q < N; ++q) {
-        const double apq = a[p][q];
-        if (apq == 0.0) continue;
-        const double theta = __ddiv_rn(__dmul_rn(0.5, __dsub_rn(a[q][q], a[p][p])), apq);
-        double t;
-        if (fabs(theta) > 1e8) t = __ddiv_rn(0.5, theta);
-        else if (theta >= 0.0) t = __ddiv_rn(1.0, __dadd_rn(theta, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(theta, theta)))));
-        else t = __ddiv_rn(-1.0, __dadd_rn(-theta, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(theta, theta)))));
-        const double c = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, __dmul_rn(t, t)))), s = __dmul_rn(t, c);
-        const double app = a[p][p], aqq = a[q][q];
-        a[p][p] = __dsub_rn(app, __dmul_rn(t, apq));
-        a[q][q] = __dadd_rn(aqq, __dmul_rn(t, apq));
-        a[p][q] = a[q][p] = 0.0;
-        for (int k = 0; k < N; ++k) {
-          if (k == p || k == q) continue;
-          const double akp = a[k][p], akq = a[k][q];
-          a[k][p] = a[p][k] = __dsub_rn(__dmul_rn(c, akp), __dmul_rn(s, akq));
-          a[k][q] = a[q][k] = __dadd_rn(__dmul_rn(s, akp), __dmul_rn(c, akq));
-        }
-        for (int k = 0; k < N; ++k) {
-          const double vkp = v[k][p], vkq = v[k][q];
-          v[k][p] = __dsub_rn(__dmul_rn(c, vkp), __dmul_rn(s, vkq));
-          v[k][q] = __dadd_rn(__dmul_rn(s, vkp), __dmul_rn(c, vkq));
-        }
-      }
-    }
-  }
-  return off_norm() <= threshold;
-}
-
-template <int N>
-__device__ __forceinline__ double frobenius(const double (&a)[N][N]) {
-  double s = 0.0;
-  for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) s += a[i][j] * a[i][j];
-  return sqrt(s);
 }
 
 struct FitParams {

@@ -10,6 +10,7 @@
 #include "rf_internal.h"
 #include "rf_tile.cuh"
 #include "rf_solve.cuh"
+#include "rf_jacobi.cuh"
 #include "rf_general.cuh"
 #include "rf_direct.cuh"
 
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) fit_lattice_tile_kernel(const KPa
             if (EXP && P.do_exp) {
               if (!(P.do_imp && hc >= 4)) kap = curvature_only(C);
               ExplicitFit e;
-              explicit_solve(C, mu0, mu1, mu2, nd, e);
+              explicit_fit_robust(C, mu0, mu1, mu2, nd, e);
               if (std_space) finish_plane(e.a, e.b, -1.0, e.c, ex, ey, ez, eo);
               else finish_plane(e.a, e.b, e.c, -1.0, ex, ey, ez, eo);
               eres = fsqrt(fmaxf((float)(e.ss / nd), 0.0f));

@@ -17,6 +17,7 @@
 #include "../../include/rangefit_b200.h"
 #include "rf_internal.h"
 #include "rf_solve.cuh"
+#include "rf_jacobi.cuh"
 #include "rf_general.cuh"
 
 namespace {
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(RT_THREADS) fit_rects_kernel(const RectParams 
       res.status = RF_RECT_FIT | (f.degenerate ? RF_RECT_DEGENERATE : 0);
     } else {
       ExplicitFit e;
-      explicit_solve(C, mu0, mu1, mu2, nd, e);
+      explicit_fit_robust(C, mu0, mu1, mu2, nd, e);
       res.explicit_coef[0] = e.a;
       res.explicit_coef[1] = e.b;
       res.explicit_coef[2] = e.c;

@@ -183,3 +183,26 @@ def test_sweep_three_sample_explicit_windows(seed):
         ref = oracle_frame(torch.from_numpy(z), cam, window, form, mask=None if mask is None else mask.cpu())
         m = compare(gpu_flat(out[form]), ref, explicit_fit=form.startswith("explicit"))
         assert m["ok"], (seed, form, m["max_residual_rel"])
+
+
+@pytest.mark.parametrize("kind,window", [("stripes", 3), ("stripes", 5), ("checker", 3)])
+def test_degenerate_explicit_windows(kind, window):
+    """Rank-deficient explicit systems (every valid sample of a window in one row: collinear in
+    tan_y): the reference's Cholesky fails and _pinv_solve returns the minimum-norm plane and
+    its true residual (fitting.py:313-322, 584-597).  The per-pixel kernel queues such windows
+    for the slow pass, which solves them that way; degenerate pixels are compared too."""
+    z, cam = _adversarial(kind)
+    H, W = z.shape
+    maps = rf.compute_tan_maps(rf.CameraIntrinsics(cam.fx, cam.fy, cam.cx, cam.cy, W, H))
+    out = rf.fit_pixels(torch.from_numpy(z).cuda(), maps, window, rf.FORMULATIONS)
+    torch.cuda.synchronize()
+    for form in (rf.EXPLICIT_STANDARD, rf.EXPLICIT_RGBD):
+        ref = oracle_frame(torch.from_numpy(z), cam, window, form)
+        got = gpu_flat(out[form])
+        rdeg = (ref["status"] & 6) == 6
+        if kind == "stripes" and window == 3:
+            assert rdeg.sum() > 100  # the case exercises the minimum-norm path
+        assert np.array_equal((got["status"] & 6) == 6, rdeg), form
+        m = compare(got, ref, explicit_fit=True, include_degenerate=True)
+        assert m["ok"], (kind, window, form, {k: m[k] for k in ("compared", "status_mismatch", "max_normal_rad",
+                                                                 "max_residual_rel", "max_curvature_rel")})
