@@ -299,23 +299,24 @@ class HostPipeline:
         self._dev_out = None
         self._host_out = None
 
-    def _buffers(self, B: int, dtype: torch.dtype):
+    def _buffers(self, B: int, dtype: torch.dtype, host: bool = True):
         H, W, c = self.maps.height, self.maps.width, self.chunk
         if self._dev_in is None or self._dev_in.dtype != dtype:
             self._dev_in = torch.empty((self.slots, c, H, W), dtype=dtype, device=self.device)
             self._dev_out = [{f: PixelFits.empty(c, H, W, self.device) for f in self.formulations}
                              for _ in range(self.slots)]
-        if self._host_out is None or self._host_out[self.formulations[0]].status.shape[0] != B:
+        if host and (self._host_out is None or self._host_out[self.formulations[0]].status.shape[0] != B):
             pin = dict(pin_memory=True)
             self._host_out = {f: PixelFits(torch.empty((B, H, W, 3), **pin), torch.empty((B, H, W), **pin),
                                            torch.empty((B, H, W), **pin), torch.empty((B, H, W), **pin),
                                            torch.empty((B, H, W), dtype=torch.uint8, **pin))
                               for f in self.formulations}
 
-    def run(self, depth: torch.Tensor) -> dict:
+    def run(self, depth: torch.Tensor, out: dict | None = None) -> dict:
         """depth: host tensor [B, H, W] (float32/float64 metres or uint16 mm; pinned for
         asynchronous copies).  Returns ``{formulation: PixelFits}`` of pinned host tensors,
-        complete when this returns and reused by the next ``run`` of the same batch size."""
+        complete when this returns and reused by the next ``run`` of the same batch size;
+        ``out`` (host PixelFits per formulation, [B, ...] each) receives them instead."""
         if depth.is_cuda:
             raise ValueError("HostPipeline.run takes host frames; use fit_pixels for device tensors")
         d = depth.unsqueeze(0) if depth.dim() == 2 else depth
@@ -324,7 +325,8 @@ class HostPipeline:
         _depth_dtype(d)  # validates the element type
         d = d.contiguous()
         B = d.shape[0]
-        self._buffers(B, d.dtype)
+        self._buffers(B, d.dtype if out is None else d.dtype, host=out is None)
+        host_out = self._host_out if out is None else out
         slot_free = [None] * self.slots   # D2H done with the slot's outputs (and the fit with its input)
         for i, b0 in enumerate(range(0, B, self.chunk)):
             b1 = min(B, b0 + self.chunk)
@@ -346,12 +348,12 @@ class HostPipeline:
             with torch.cuda.stream(self.d2h):
                 for f in self.formulations:
                     for name in ("normal", "offset", "residual", "curvature", "status"):
-                        getattr(self._host_out[f], name)[b0:b1].copy_(getattr(outs[f], name), non_blocking=True)
+                        getattr(host_out[f], name)[b0:b1].copy_(getattr(outs[f], name), non_blocking=True)
                 ev_out = torch.cuda.Event()
                 ev_out.record(self.d2h)
             slot_free[k] = ev_out
         self.d2h.synchronize()
-        return self._host_out
+        return host_out
 
 
 def launches_per_call(formulations=PIXEL_FORMULATIONS, window: int = 5, dtype=torch.float32,

@@ -37,3 +37,56 @@ def max_over_ranks(value: float, world: int, device: str | torch.device = "cpu")
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def fit_frames_sharded(depth, intrinsics, window: int, formulations=None, devices=None, chunk_frames: int = 8):
+    """Fit a host batch of frames across several GPUs of this process: contiguous frame ranges
+    (frame_range) per device, each streamed through its own HostPipeline (H2D, tile kernels,
+    D2H on its own streams and PCIe link) from its own host thread, straight into one pinned
+    host output per formulation.  No collective: frames are independent.
+
+    depth: host tensor [B, H, W] (float32 / float64 metres or uint16 mm); intrinsics: the
+    camera (CameraIntrinsics); devices: CUDA device indices (default: every visible device; a
+    device may repeat).  Returns {formulation: PixelFits} of pinned host tensors."""
+    import threading
+
+    from .pixels import PIXEL_FORMULATIONS, HostPipeline, PixelFits, compute_tan_maps
+
+    formulations = PIXEL_FORMULATIONS if formulations is None else (
+        (formulations,) if isinstance(formulations, str) else tuple(formulations))
+    if depth.is_cuda or depth.dim() != 3:
+        raise ValueError("fit_frames_sharded takes a host batch [B, H, W]")
+    devices = list(range(torch.cuda.device_count())) if devices is None else [int(d) for d in devices]
+    if not devices:
+        raise ValueError("no CUDA device to shard over (the sm_100a path has no CPU fallback)")
+    B, H, W = depth.shape
+    pin = dict(pin_memory=True)
+    out = {f: PixelFits(torch.empty((B, H, W, 3), **pin), torch.empty((B, H, W), **pin),
+                        torch.empty((B, H, W), **pin), torch.empty((B, H, W), **pin),
+                        torch.empty((B, H, W), dtype=torch.uint8, **pin)) for f in formulations}
+    src = depth.contiguous()
+    errors = []
+
+    def work(rank: int, dev: int):
+        try:
+            start, stop = frame_range(B, len(devices), rank)
+            if stop == start:
+                return
+            with torch.cuda.device(dev):
+                maps = compute_tan_maps(intrinsics, dev)
+                pipe = HostPipeline(maps, window, formulations, chunk_frames=chunk_frames)
+                view = {f: PixelFits(*(getattr(out[f], k)[start:stop] for k in
+                                       ("normal", "offset", "residual", "curvature", "status")))
+                        for f in formulations}
+                pipe.run(src[start:stop], out=view)
+        except BaseException as e:  # surfaced in the caller's thread
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k, d)) for k, d in enumerate(devices)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out
