@@ -44,6 +44,7 @@ UNIT = "Mpixel-fits/s"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 BYTES_IN = 4  # float32 depth
 BYTES_OUT = 25  # per pixel per formulation: 12 normal + 4 offset + 4 residual + 4 curvature + 1 status
+FP64_PEAK_TOPS = 17.1  # measured DFMA throughput, T/s (profiles/peak_probe_r1.txt)
 
 
 def hbm_peak():
@@ -68,6 +69,20 @@ def profiled_traffic():
         return None
 
 
+def profiled_fp64(kernel: str, launch_ms: float):
+    """Secondary roofline: the dominant kernel's executed fp64 instructions per
+    launch (committed ncu SASS count) over this run's launch time, against the measured DFMA
+    peak (profiles/peak_probe_r1.txt: 17.1 T/s on this pool's B200s)."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        n = float(json.loads(p.read_text())["kernels"][kernel]["fp64_thread_inst_per_launch"])
+    except Exception:
+        return None
+    achieved = n / (launch_ms * 1e-3) / 1e12
+    return {"achieved": achieved, "peak": FP64_PEAK_TOPS, "unit": "T fp64 inst/s", "frac": achieved / FP64_PEAK_TOPS,
+            "fp64_thread_inst_per_launch": n, "peak_source": "measured: tools/peak_probe.cu, profiles/peak_probe_r1.txt"}
+
+
 def profiled_pipes(kernel: str):
     """What binds the dominant kernel instead of HBM, from the same committed ncu capture:
     issue-slot and pipe utilisation (fractions of peak)."""
@@ -83,7 +98,7 @@ def profiled_pipes(kernel: str):
         except Exception:
             return None
 
-    return {"bound": "instruction issue under fp64 / MUFU dependency latency",
+    return {"bound": "instruction issue under fp64 / MUFU dependency latency (pipes shared in the solve phase)",
             "issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "fp64_pipe": pct("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
             "xu_pipe": pct("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
@@ -427,6 +442,7 @@ def run_ours(args, world, rank, local):
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": alg_bytes,
                 "algorithmic_bytes_per_pixel_fit": (BYTES_IN + BYTES_OUT * len(forms)) / len(forms),
                 "launches_per_step": launches_step, "launch_ms": launch_ms,
+                "fp64": profiled_fp64("per_space", launch_ms),
                 "binding": profiled_pipes("per_space")}
 
     # ---- end to end through the public API with host buffers (pinned): HostPipeline
