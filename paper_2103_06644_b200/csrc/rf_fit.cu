@@ -859,6 +859,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
                     const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   const KParams& P = (SP & 1) ? Ps : Pd;  // input and geometry (identical in both)
+  if (P.pdl_trigger == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // TMA destinations must be 128-byte aligned: align the dynamic base explicitly
   // (pointer arithmetic on the __shared__ array, not integer casts, so every derived
   // pointer stays in the shared window and compiles to LDS/STS rather than generic LD/ST)
@@ -947,6 +948,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   int it = 0;
   TileIter ti(blockIdx.x, gridDim.x, ntx, nty);
   for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it, ti.advance()) {
+    if (P.pdl_trigger == 2 && t + gridDim.x >= total) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const TileGeom g = ti.geom();
     T.frame = g.frame;
     T.x0 = g.x0;
@@ -1126,7 +1128,7 @@ struct KernelCache {
 
 template <int SP, bool TMA, int RT, bool EXP>
 cudaError_t launch_sp(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, size_t sm, int64_t tiles,
-                      int sms, cudaStream_t s) {
+                      int sms, cudaStream_t s, bool pdl) {
   auto kern = fit_tile_kernel<SP, TMA, RT, EXP>;
   static KernelCache kc;
   int per_sm;
@@ -1148,32 +1150,48 @@ cudaError_t launch_sp(const KParams& Ps, const KParams& Pd, const CUtensorMap& t
     }
   }
   const int64_t grid = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
-  kern<<<(unsigned)grid, NTHREADS, sm, s>>>(Ps, Pd, tmap);
-  return cudaGetLastError();
+  if (!pdl) {
+    kern<<<(unsigned)grid, NTHREADS, sm, s>>>(Ps, Pd, tmap);
+    return cudaGetLastError();
+  }
+  // the second space's launch of a call: programmatic dependent launch -- it shares no data
+  // with the first (same input, its own outputs), so its CTAs take SMs as the first
+  // kernel's CTAs retire (every CTA of fit_tile_kernel releases its dependents at entry)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, Ps, Pd, tmap);
 }
 
 template <int SP, bool TMA, int RT>
 cudaError_t launch_var(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, size_t sm, int64_t tiles,
-                       int sms, cudaStream_t s) {
+                       int sms, cudaStream_t s, bool pdl = false) {
   const bool exp = ((SP & 1) && Ps.do_exp) || ((SP & 2) && Pd.do_exp);
-  return exp ? launch_sp<SP, TMA, RT, true>(Ps, Pd, tmap, sm, tiles, sms, s)
-             : launch_sp<SP, TMA, RT, false>(Ps, Pd, tmap, sm, tiles, sms, s);
+  return exp ? launch_sp<SP, TMA, RT, true>(Ps, Pd, tmap, sm, tiles, sms, s, pdl)
+             : launch_sp<SP, TMA, RT, false>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
 }
 
 // compile-time radii for the BASELINE windows 3, 5, 7, 9, 11, 15, 31; others run generic
 template <int SP>
 cudaError_t launch_radius(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, bool tma, size_t sm,
-                          int64_t tiles, int sms, cudaStream_t s) {
-  if (!tma) return launch_var<SP, false, 0>(Ps, Pd, tmap, sm, tiles, sms, s);
+                          int64_t tiles, int sms, cudaStream_t s, bool pdl = false) {
+  if (!tma) return launch_var<SP, false, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
   switch (Ps.r) {
-    case 1: return launch_var<SP, true, 1>(Ps, Pd, tmap, sm, tiles, sms, s);
-    case 2: return launch_var<SP, true, 2>(Ps, Pd, tmap, sm, tiles, sms, s);
-    case 3: return launch_var<SP, true, 3>(Ps, Pd, tmap, sm, tiles, sms, s);
-    case 4: return launch_var<SP, true, 4>(Ps, Pd, tmap, sm, tiles, sms, s);
-    case 5: return launch_var<SP, true, 5>(Ps, Pd, tmap, sm, tiles, sms, s);
-    case 7: return launch_var<SP, true, 7>(Ps, Pd, tmap, sm, tiles, sms, s);
-    case 15: return launch_var<SP, true, 15>(Ps, Pd, tmap, sm, tiles, sms, s);
-    default: return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s);
+    case 1: return launch_var<SP, true, 1>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    case 2: return launch_var<SP, true, 2>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    case 3: return launch_var<SP, true, 3>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    case 4: return launch_var<SP, true, 4>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    case 5: return launch_var<SP, true, 5>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    case 7: return launch_var<SP, true, 7>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    case 15: return launch_var<SP, true, 15>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    default: return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
   }
 }
 
@@ -1408,12 +1426,18 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   if (fused) {
     e = launch_radius<3>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, sm_both, tiles, di.sms, s);
   } else {
+    // Two launches (one per space): the second is a programmatic dependent launch -- it shares
+    // nothing with the first (same input, its own outputs), so its CTAs take the SMs the first
+    // frees as its CTAs retire (the first releases its dependents at entry).  The next call's
+    // first launch is ordered normally after both.
+    const bool pdl = want_df && want_std && getenv("RF_NO_PDL") == nullptr;
+    if (pdl) Pv[VAR_DF].pdl_trigger = 1;
     if (want_df)
       e = launch_radius<2>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, smem_bytes(2, r, tma, esz, Pv[VAR_DF].do_exp), tiles,
                            di.sms, s);
     if (e == cudaSuccess && want_std)
       e = launch_radius<1>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, smem_bytes(1, r, tma, esz, Pv[VAR_STD].do_exp), tiles,
-                           di.sms, s);
+                           di.sms, s, pdl);
   }
   if (e != cudaSuccess) return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return RF_OK;
