@@ -48,7 +48,8 @@ using namespace rf_tile;
 __device__ unsigned long long g_slow_count[256];
 #endif
 
-// compile-time radii whose halo tile is not staged as fp64 in shared memory (see NOPRIM)
+// compile-time radii whose standard-space halo (Z) is staged as float, not fp64 (see ZF): the
+// only way two CTAs fit per SM at r = 15; Z of a float32 input is exact in float
 __host__ __device__ constexpr bool noprim_radius(int rt) { return rt == 15; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -136,17 +137,18 @@ __device__ __forceinline__ double primary_of(T v, bool mask_ok) {
 // primaries of the requested spaces, [row * HW_ + col].  The plain loop covers interior
 // tiles without a mask; image edges (negative shift: rows/columns left of or above the
 // image) and masks take the checked loop.
-template <int SP, typename T>
-__device__ __forceinline__ void convert_halo(double* pw, double* pz, const T* raw, int HW_, int HH_, int HWP, int sx,
-                                             int sy, const KParams& P, int64_t frame, int x0, int y0, int r,
-                                             int tid) {
+template <int SP, bool ZF, typename T>
+__device__ __forceinline__ void convert_halo(double* pw, double* pz, float* pzf, const T* raw, int HW_, int HH_,
+                                             int HWP, int sx, int sy, const KParams& P, int64_t frame, int x0,
+                                             int y0, int r, int tid) {
   const int n = HH_ * HW_;
   auto put = [&](int e, T v, bool ok) {
     bool valid;
     const double z = depth_z(v, valid);
     valid = valid && ok;
     if (SP & 2) pw[e] = valid ? rcp_fast(z) : 0.0;
-    if (SP & 1) pz[e] = valid ? z : 0.0;
+    if ((SP & 1) && ZF) pzf[e] = valid ? (float)z : 0.0f;
+    if ((SP & 1) && !ZF) pz[e] = valid ? z : 0.0;
   };
   if (!P.mask && (sx | sy) >= 0 && ((HW_ | HWP | sx) & 1) == 0) {
     // interior tile, even row geometry: element pairs (one 2-element load, one 16-byte store
@@ -157,7 +159,8 @@ __device__ __forceinline__ void convert_halo(double* pw, double* pz, const T* ra
       bool v0, v1;
       const double z0 = depth_z(src[0], v0), z1 = depth_z(src[1], v1);
       if (SP & 2) *reinterpret_cast<double2*>(pw + e) = make_double2(v0 ? rcp_fast(z0) : 0.0, v1 ? rcp_fast(z1) : 0.0);
-      if (SP & 1) *reinterpret_cast<double2*>(pz + e) = make_double2(v0 ? z0 : 0.0, v1 ? z1 : 0.0);
+      if ((SP & 1) && ZF) *reinterpret_cast<float2*>(pzf + e) = make_float2(v0 ? (float)z0 : 0.0f, v1 ? (float)z1 : 0.0f);
+      if ((SP & 1) && !ZF) *reinterpret_cast<double2*>(pz + e) = make_double2(v0 ? z0 : 0.0, v1 ? z1 : 0.0);
     }
   } else if (!P.mask && (sx | sy) >= 0) {
 #pragma unroll 2
@@ -326,8 +329,7 @@ __device__ __forceinline__ void assemble(const double* h, const int* hi, double 
   }
 }
 
-// Per-tile context shared by the space passes: geometry, shared-memory views, the raw
-// halo (NOPRIM reads primaries straight from it).
+// Per-tile context shared by the space passes: geometry, shared-memory views.
 struct TileCtx {
   const KParams* P;
   int r, HW_, HH_, HWP, VQ, VRS, sx, sy, esz, it, tid;
@@ -336,27 +338,18 @@ struct TileCtx {
   const unsigned char* raw;
   double* pw;   // [HH_][HW_] 1/Z (disparity form)
   double* pz;   // [HH_][HW_] Z (standard)
+  float* pzf;   // [HH_][HW_] Z (standard, ZF kernels: float32 input only)
   double* vd;   // [NVD][TH][VRS] column sums of the current space
   void* vi;     // [TH][VRS] valid-count geometry (both spaces), CountT<RT>
   float* xstage;
 };
 
-// primary of halo element (row, col) of the tile for space VAR: from the converted tile, or
-// (NOPRIM) converted from the raw TMA box on the fly
-template <int VAR, bool NOPRIM>
+// primary of halo element (row, col) of the tile for space VAR (ZF: the standard space's Z
+// tile is float)
+template <int VAR, bool ZF>
 __device__ __forceinline__ double primary_at(const TileCtx& T, int row, int col) {
-  if (!NOPRIM) return (VAR == VAR_DF ? T.pw : T.pz)[row * T.HW_ + col];
-  if (row + T.sy < 0 || col + T.sx < 0) return 0.0;  // left / top of the image
-  const KParams& P = *T.P;
-  bool mask_ok = true;
-  if (P.mask) {
-    const int y = T.y0 - T.r + row, x = T.x0 - T.r + col;
-    mask_ok = y < P.H && x < P.W && __ldg(P.mask + T.frame * P.out_frame + (int64_t)y * P.W + x) != 0;
-  }
-  const int ri = (row + T.sy) * T.HWP + col + T.sx;
-  return T.esz == 2   ? primary_of<VAR>(reinterpret_cast<const unsigned short*>(T.raw)[ri], mask_ok)
-         : T.esz == 8 ? primary_of<VAR>(reinterpret_cast<const double*>(T.raw)[ri], mask_ok)
-                      : primary_of<VAR>(reinterpret_cast<const float*>(T.raw)[ri], mask_ok);
+  if (VAR == VAR_STD && ZF) return (double)T.pzf[row * T.HW_ + col];
+  return (VAR == VAR_DF ? T.pw : T.pz)[row * T.HW_ + col];
 }
 
 // ---- 2. vertical window sums of space VAR (and, for the tile's first space, the
@@ -878,14 +871,11 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   T.HWP = (HW_ + al - 1 + 7) & ~7;  // TMA box width (covers the alignment shift)
   const int HWP = T.HWP;
   const int raw_bytes = USE_TMA ? ((HH_ * HWP * esz + 127) & ~127) : 0;
-  // NOPRIM (the standard space at the largest compile-time radius): no converted Z tile in
-  // shared memory -- its column pass reads the raw box (Z is the stored element), so two
-  // CTAs still fit per SM; the disparity form always converts (1/Z once per element).
-  constexpr bool NOPRIM = noprim_radius(RT) && USE_TMA;  // standard space
-  constexpr int PSP = ((SP & 2) ? 2 : 0) | ((SP & 1) && !NOPRIM ? 1 : 0);  // spaces with converted tiles
-  // a raw box read through the whole tile needs two buffers; otherwise the conversion
-  // consumes it before the tile's barrier and the next tile's TMA reuses the one buffer
-  constexpr int NRAW = (SP & 1) && NOPRIM ? 2 : 1;
+  // ZF (the largest compile-time radius): the standard space's Z tile is float (float32 input
+  // only: rf_fit_pixels routes other element types to the generic kernel), so two CTAs fit
+  constexpr bool NOPRIM = noprim_radius(RT) && USE_TMA;  // ZF
+  constexpr int PSP = SP;
+  constexpr int NRAW = 1;  // the conversion consumes the raw box before the tile's barrier
   unsigned char* raw0 = smem_raw;
   unsigned char* raw1 = smem_raw + (NRAW - 1) * raw_bytes;
   // small compile-time radii: warp-local column and row passes; the converted halo is
@@ -896,16 +886,18 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   // batches) keep one buffer and close the tile with a barrier instead
   constexpr bool DBUF = CENTRED && SP != 3 && RF_MIN_BLOCKS < 3;
   const int nprim = HH_ * HW_;
-  const int nsp = ((PSP & 2) ? 1 : 0) + ((PSP & 1) ? 1 : 0);
+  const int nsp = ((PSP & 2) ? 1 : 0) + ((PSP & 1) && !NOPRIM ? 1 : 0);  // fp64 tiles
   double* prim_base = reinterpret_cast<double*>(smem_raw + NRAW * raw_bytes);  // [DBUF ? 2 : 1][nsp][HH_][HW_]
   T.pw = prim_base;                              // [HH_][HW_]
   T.pz = T.pw + ((PSP & 2) ? nprim : 0);         // [HH_][HW_]
+  T.pzf = reinterpret_cast<float*>(prim_base + (DBUF ? 2 : 1) * nsp * nprim);  // [HH_][HW_] (ZF)
   // column sums are stored residue-major: column c at (c % 4) * VQ + c / 4, so the row
   // pass (threads 4 columns apart) reads consecutive addresses -- no bank conflicts.
   T.VQ = NOPRIM ? (HW_ + 3) / 4 : vq_of(HW_);
   T.VRS = 4 * T.VQ;
   const int VRS = T.VRS;
-  T.vd = prim_base + (DBUF ? 2 : 1) * nsp * nprim;                   // [NVD][TH][VRS]
+  T.vd = prim_base + (DBUF ? 2 : 1) * nsp * nprim +
+         (((SP & 1) && NOPRIM) ? (nprim + 1) / 2 : 0);                  // [NVD][TH][VRS]
   T.vi = T.vd + NVD * TH * VRS;                                        // [TH][VRS] CountT<RT>
   uint64_t* bars = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(T.vi) +
                                                ((sizeof(CountT<RT>) * TH * VRS + 7) & ~(size_t)7));
@@ -970,13 +962,13 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
       mbar_wait(&bars[b], (uint32_t)((it >> 1) & 1));
       if (PSP != 0) {
         if (esz == 2)
-          convert_halo<PSP>(T.pw, T.pz, reinterpret_cast<const unsigned short*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P,
+          convert_halo<PSP, NOPRIM>(T.pw, T.pz, T.pzf, reinterpret_cast<const unsigned short*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P,
                            frame, x0, y0, r, tid);
         else if (esz == 8)
-          convert_halo<PSP>(T.pw, T.pz, reinterpret_cast<const double*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
+          convert_halo<PSP, NOPRIM>(T.pw, T.pz, T.pzf, reinterpret_cast<const double*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
                            x0, y0, r, tid);
         else
-          convert_halo<PSP>(T.pw, T.pz, reinterpret_cast<const float*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
+          convert_halo<PSP, NOPRIM>(T.pw, T.pz, T.pzf, reinterpret_cast<const float*>(T.raw), HW_, HH_, HWP, T.sx, T.sy, P, frame,
                            x0, y0, r, tid);
         __syncthreads();
       }
@@ -1062,17 +1054,19 @@ __attribute__((format(printf, 2, 3))) rf_status fail(rf_status s, const char* fm
 // dynamic shared memory of fit_tile_kernel<SP, tma, r> (the kernel's own layout)
 bool compiled_radius(int r) { return r == 1 || r == 2 || r == 3 || r == 4 || r == 5 || r == 7 || r == 15; }
 size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false) {
+  // r = 15 with the standard space and a non-float32 input runs the generic-radius kernel
+  const bool generic15 = r == 15 && (sp & 1) && esz != 4;
   const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
   const int nvd = (sp & 1) ? 5 : 3;
   const int nsp = (sp & 1) + ((sp >> 1) & 1);
-  const bool rt = tma && compiled_radius(r);           // the kernel's RT > 0
-  const bool noprim = tma && noprim_radius(r);         // the kernel's NOPRIM (RT == r; standard space)
-  const int psp = nsp - ((sp & 1) && noprim ? 1 : 0);  // spaces with a converted tile
+  const bool rt = tma && compiled_radius(r) && !generic15;  // the kernel's RT > 0
+  const bool noprim = rt && noprim_radius(r);          // the kernel's ZF (RT == r): float Z tile
+  const int psp = nsp - ((sp & 1) && noprim ? 1 : 0);  // spaces with an fp64 tile
   const bool dbuf = rt && r <= 3 && sp != 3 && RF_MIN_BLOCKS < 3;  // the kernel's DBUF
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
   const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
   const size_t counts = ((rt ? sizeof(int) : sizeof(int2)) * (size_t)TH * vrs + 7) & ~(size_t)7;
-  return ((sp & 1) && noprim ? 2 : 1) * raw +
+  return raw + ((sp & 1) && noprim ? (((size_t)hh * hw + 1) / 2) * sizeof(double) : 0) +
          sizeof(double) * ((dbuf ? 2 : 1) * (size_t)psp * hh * hw + (size_t)nvd * TH * vrs) + counts +
          2 * sizeof(uint64_t) + 128 /* base align */ + (exp ? (size_t)28 * sizeof(float) * NTHREADS : 0);
 }
@@ -1190,7 +1184,9 @@ cudaError_t launch_radius(const KParams& Ps, const KParams& Pd, const CUtensorMa
     case 4: return launch_var<SP, true, 4>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
     case 5: return launch_var<SP, true, 5>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
     case 7: return launch_var<SP, true, 7>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
-    case 15: return launch_var<SP, true, 15>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    case 15:  // the float Z tile holds float32 depths exactly; other element types: generic radius
+      if ((SP & 1) && elem_size(Ps.dtype) != 4) return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+      return launch_var<SP, true, 15>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
     default: return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
   }
 }
