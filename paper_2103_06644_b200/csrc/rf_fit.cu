@@ -34,6 +34,11 @@
 #include "rf_internal.h"
 
 #include "rf_tile.cuh"
+// largest compile-time radius whose column pass sums each window directly (dy centred on the
+// output row, warp-local, no running sums): measured r <= 5 (C3 w9 +2%; r = 7 loses 1-3%)
+#ifndef RF_CENTRED_MAX
+#define RF_CENTRED_MAX 5
+#endif
 #include "rf_solve.cuh"
 #include "rf_invn.cuh"
 #include "rf_jacobi.cuh"
@@ -362,7 +367,7 @@ __device__ __forceinline__ double primary_at(const TileCtx& T, int row, int col)
 template <int VAR, int RT, bool NOPRIM, int COUNTS>
 __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) {
   constexpr int NVD = VAR == VAR_DF ? 3 : 5;
-  constexpr bool CENTRED = RT > 0 && RT <= 3;
+  constexpr bool CENTRED = RT > 0 && RT <= RF_CENTRED_MAX;
   const int r = T.r, VRS = T.VRS, VQ = T.VQ, tid = T.tid;
   double* vd = T.vd;
   if constexpr (CENTRED) {
@@ -513,7 +518,7 @@ __device__ __forceinline__ void column_pass(const TileCtx& T, unsigned* s_dmax) 
 // explicit fits as well; other entries only refresh the explicit curvature (it is shared).
 template <int VAR, int RT, bool EXP, bool NOPRIM>
 __device__ __forceinline__ void slow_pixel(const TileCtx& T, const KParams& P, int e) {
-  constexpr bool CENTRED = RT > 0 && RT <= 3;
+  constexpr bool CENTRED = RT > 0 && RT <= RF_CENTRED_MAX;
   const int r = T.r;
   const int pix = e & Q_PIX;
   const bool direct = (e & Q_DIRECT) != 0;
@@ -587,7 +592,7 @@ __device__ __forceinline__ void slow_pixel(const TileCtx& T, const KParams& P, i
 template <int VAR, int RT, bool EXP, bool NOPRIM>
 __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, unsigned* s_dmax,
                                          unsigned short* s_q, int* s_qn) {
-  constexpr bool CENTRED = RT > 0 && RT <= 3;
+  constexpr bool CENTRED = RT > 0 && RT <= RF_CENTRED_MAX;
   constexpr int NH = HSums<VAR>::NH, NHI = HSums<VAR>::NHI;
   const int r = T.r, VQ = T.VQ, VRS = T.VRS, tid = T.tid;
   const int orow = tid / (TW / KSEG);
@@ -881,10 +886,10 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   // small compile-time radii: warp-local column and row passes; the converted halo is
   // double-buffered so that the tile's one CTA barrier (after the conversion) also orders the
   // next conversion after every warp's last read of the buffer it overwrites
-  constexpr bool CENTRED = RT > 0 && RT <= 3;
+  constexpr bool CENTRED = RT > 0 && RT <= RF_CENTRED_MAX;
   // one space per launch: the double buffer fits two CTAs per SM; both spaces (small
   // batches) keep one buffer and close the tile with a barrier instead
-  constexpr bool DBUF = CENTRED && SP != 3 && RF_MIN_BLOCKS < 3;
+  constexpr bool DBUF = CENTRED && RT <= 3 && SP != 3 && RF_MIN_BLOCKS < 3;
   const int nprim = HH_ * HW_;
   const int nsp = ((PSP & 2) ? 1 : 0) + ((PSP & 1) && !NOPRIM ? 1 : 0);  // fp64 tiles
   double* prim_base = reinterpret_cast<double*>(smem_raw + NRAW * raw_bytes);  // [DBUF ? 2 : 1][nsp][HH_][HW_]
