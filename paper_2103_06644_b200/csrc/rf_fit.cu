@@ -851,8 +851,8 @@ __device__ __forceinline__ void slow_pass(const TileCtx& T, const KParams& P, co
 // constants), RT == 0: runtime radius; EXP: explicit fits compiled in.  Ps / Pd: the
 // standard / disparity-form space's parameters (the same input and geometry, their own
 // outputs and requested formulations).
-template <int SP, bool USE_TMA, int RT, bool EXP>
-__global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
+template <int SP, bool USE_TMA, int RT, bool EXP, int MINB = RF_MIN_BLOCKS>
+__global__ void __launch_bounds__(NTHREADS, MINB)
     fit_tile_kernel(const __grid_constant__ KParams Ps, const __grid_constant__ KParams Pd,
                     const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_dyn[];
@@ -889,7 +889,7 @@ __global__ void __launch_bounds__(NTHREADS, RF_MIN_BLOCKS)
   constexpr bool CENTRED = RT > 0 && RT <= RF_CENTRED_MAX;
   // one space per launch: the double buffer fits two CTAs per SM; both spaces (small
   // batches) keep one buffer and close the tile with a barrier instead
-  constexpr bool DBUF = CENTRED && RT <= 3 && SP != 3 && RF_MIN_BLOCKS < 3;
+  constexpr bool DBUF = CENTRED && RT <= 3 && SP != 3 && MINB < 3;
   const int nprim = HH_ * HW_;
   const int nsp = ((PSP & 2) ? 1 : 0) + ((PSP & 1) && !NOPRIM ? 1 : 0);  // fp64 tiles
   double* prim_base = reinterpret_cast<double*>(smem_raw + NRAW * raw_bytes);  // [DBUF ? 2 : 1][nsp][HH_][HW_]
@@ -1058,7 +1058,7 @@ __attribute__((format(printf, 2, 3))) rf_status fail(rf_status s, const char* fm
 
 // dynamic shared memory of fit_tile_kernel<SP, tma, r> (the kernel's own layout)
 bool compiled_radius(int r) { return r == 1 || r == 2 || r == 3 || r == 4 || r == 5 || r == 7 || r == 15; }
-size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false) {
+size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false, int minb = RF_MIN_BLOCKS) {
   // r = 15 with the standard space and a non-float32 input runs the generic-radius kernel
   const bool generic15 = r == 15 && (sp & 1) && esz != 4;
   const int hw = TW + 2 * r, hh = TH + 2 * r, hwp = (hw + 16 / esz - 1 + 7) & ~7;
@@ -1067,7 +1067,7 @@ size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false) {
   const bool rt = tma && compiled_radius(r) && !generic15;  // the kernel's RT > 0
   const bool noprim = rt && noprim_radius(r);          // the kernel's ZF (RT == r): float Z tile
   const int psp = nsp - ((sp & 1) && noprim ? 1 : 0);  // spaces with an fp64 tile
-  const bool dbuf = rt && r <= 3 && sp != 3 && RF_MIN_BLOCKS < 3;  // the kernel's DBUF
+  const bool dbuf = rt && r <= 3 && sp != 3 && minb < 3;  // the kernel's DBUF
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
   const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
   const size_t counts = ((rt ? sizeof(int) : sizeof(int2)) * (size_t)TH * vrs + 7) & ~(size_t)7;
@@ -1125,10 +1125,10 @@ struct KernelCache {
   int per_sm = 0;
 };
 
-template <int SP, bool TMA, int RT, bool EXP>
+template <int SP, bool TMA, int RT, bool EXP, int MINB = RF_MIN_BLOCKS>
 cudaError_t launch_sp(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, size_t sm, int64_t tiles,
                       int sms, cudaStream_t s, bool pdl) {
-  auto kern = fit_tile_kernel<SP, TMA, RT, EXP>;
+  auto kern = fit_tile_kernel<SP, TMA, RT, EXP, MINB>;
   static KernelCache kc;
   int per_sm;
   {
@@ -1171,8 +1171,11 @@ cudaError_t launch_sp(const KParams& Ps, const KParams& Pd, const CUtensorMap& t
 
 template <int SP, bool TMA, int RT>
 cudaError_t launch_var(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, size_t sm, int64_t tiles,
-                       int sms, cudaStream_t s, bool pdl = false) {
+                       int sms, cudaStream_t s, bool pdl = false, bool three = false) {
   const bool exp = ((SP & 1) && Ps.do_exp) || ((SP & 2) && Pd.do_exp);
+  if constexpr (SP != 3 && TMA && RT >= 1 && RT <= 3) {
+    if (three && !exp) return launch_sp<SP, TMA, RT, false, 3>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+  }
   return exp ? launch_sp<SP, TMA, RT, true>(Ps, Pd, tmap, sm, tiles, sms, s, pdl)
              : launch_sp<SP, TMA, RT, false>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
 }
@@ -1180,19 +1183,19 @@ cudaError_t launch_var(const KParams& Ps, const KParams& Pd, const CUtensorMap& 
 // compile-time radii for the BASELINE windows 3, 5, 7, 9, 11, 15, 31; others run generic
 template <int SP>
 cudaError_t launch_radius(const KParams& Ps, const KParams& Pd, const CUtensorMap& tmap, bool tma, size_t sm,
-                          int64_t tiles, int sms, cudaStream_t s, bool pdl = false) {
-  if (!tma) return launch_var<SP, false, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+                          int64_t tiles, int sms, cudaStream_t s, bool pdl = false, bool three = false) {
+  if (!tma) return launch_var<SP, false, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
   switch (Ps.r) {
-    case 1: return launch_var<SP, true, 1>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
-    case 2: return launch_var<SP, true, 2>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
-    case 3: return launch_var<SP, true, 3>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
-    case 4: return launch_var<SP, true, 4>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
-    case 5: return launch_var<SP, true, 5>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
-    case 7: return launch_var<SP, true, 7>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+    case 1: return launch_var<SP, true, 1>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
+    case 2: return launch_var<SP, true, 2>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
+    case 3: return launch_var<SP, true, 3>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
+    case 4: return launch_var<SP, true, 4>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
+    case 5: return launch_var<SP, true, 5>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
+    case 7: return launch_var<SP, true, 7>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
     case 15:  // the float Z tile holds float32 depths exactly; other element types: generic radius
-      if ((SP & 1) && elem_size(Ps.dtype) != 4) return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
-      return launch_var<SP, true, 15>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
-    default: return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl);
+      if ((SP & 1) && elem_size(Ps.dtype) != 4) return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
+      return launch_var<SP, true, 15>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
+    default: return launch_var<SP, true, 0>(Ps, Pd, tmap, sm, tiles, sms, s, pdl, three);
   }
 }
 
@@ -1218,6 +1221,27 @@ DeviceInfo device_info(int dev) {
     cudaDeviceGetAttribute(&d.smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   }
   return d;
+}
+
+// How rf_fit_pixels launches (both rf_fit_pixels and rf_launches_per_call use it).
+struct LaunchPlan {
+  bool fused;  // both spaces in one SP = 3 launch
+  bool three;  // one launch per space at three CTAs per SM (small radii, one wave of tiles)
+};
+LaunchPlan plan_launches(int sp_all, int r, bool tma, int esz, bool want_exp, int64_t tiles, const DeviceInfo& di) {
+  LaunchPlan lp{false, false};
+  if (sp_all != 3) return lp;
+  lp.three = tma && r >= 1 && r <= 3 && !want_exp && tiles <= (int64_t)3 * di.sms &&
+             3 * (smem_bytes(1, r, true, esz, false, 3) + 1024) <= (size_t)di.smem_sm && getenv("RF_NO_THREE") == nullptr;
+  // Both spaces in one launch (one read and conversion of the input, one launch) for small
+  // batches -- at most four waves of tiles, where the launch count and tail waves dominate --
+  // when two such CTAs still fit per SM.  Large batches run one launch per space (disparity
+  // form first): measured on C2 (64 frames, w5) the fused kernel's doubled instruction
+  // footprint costs more in instruction-fetch stalls (11.6% vs 3.5% of warp samples) than the
+  // shared halo saves (1.20-1.23 vs 1.15 ms per step).
+  lp.fused = !lp.three && 2 * (smem_bytes(3, r, tma, esz, want_exp) + 1024) <= (size_t)di.smem_sm &&
+             (tiles <= (int64_t)4 * 2 * di.sms || getenv("RF_FUSE") != nullptr) && getenv("RF_NO_FUSE") == nullptr;
+  return lp;
 }
 
 }  // namespace
@@ -1247,8 +1271,7 @@ const char* rf_last_error(void) { return g_err; }
 
 int32_t rf_launches_per_call(int32_t formulation_mask, int32_t window, int32_t dtype, int64_t batch,
                              int32_t height, int32_t width) {
-  // one tile kernel for both spaces on small batches when two such CTAs fit per SM (TMA
-  // path, current device; rf_fit_pixels), else one per space
+  // rf_fit_pixels' launch plan for separable tables on the current device (TMA path)
   const bool want_std = (formulation_mask & (RF_IMPLICIT_STANDARD | RF_EXPLICIT_STANDARD)) != 0;
   const bool want_df = (formulation_mask & (RF_IMPLICIT_RGBD | RF_EXPLICIT_RGBD)) != 0;
   if (!(want_std && want_df)) return (want_std || want_df) ? 1 : 0;
@@ -1256,12 +1279,8 @@ int32_t rf_launches_per_call(int32_t formulation_mask, int32_t window, int32_t d
   cudaGetDevice(&dev);
   const DeviceInfo di = device_info(dev);
   const bool want_exp = (formulation_mask & (RF_EXPLICIT_STANDARD | RF_EXPLICIT_RGBD)) != 0;
-  const size_t sm = smem_bytes(3, window / 2, true, elem_size(dtype), want_exp);
   const int64_t tiles = (int64_t)((width + TW - 1) / TW) * ((height + TH - 1) / TH) * batch;
-  const bool fused = 2 * (sm + 1024) <= (size_t)di.smem_sm &&
-                     (tiles <= (int64_t)4 * 2 * di.sms || getenv("RF_FUSE") != nullptr) &&
-                     getenv("RF_NO_FUSE") == nullptr;
-  return fused ? 1 : 2;
+  return plan_launches(3, window / 2, true, elem_size(dtype), want_exp, tiles, di).fused ? 1 : 2;
 }
 
 rf_status rf_tables_create(const rf_intrinsics* in, const double* delta_x, const double* delta_y,
@@ -1420,10 +1439,12 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
   // per space (disparity form first): measured on C2 (64 frames, w5) the fused kernel's
   // doubled instruction footprint costs more in instruction-fetch stalls (11.6% vs 3.5% of
   // warp samples) than the shared halo saves (1.20-1.23 vs 1.15 ms per step).
+  // One wave of tiles at small radii (a single frame): one launch per space at three CTAs per
+  // SM (their smaller per-space footprint fits) so every tile has its own CTA slot.
+  const LaunchPlan lp = plan_launches(sp_all, r, tma, esz, want_exp, tiles, di);
+  const bool fused = lp.fused;
+  const bool three = lp.three;
   const size_t sm_both = smem_bytes(3, r, tma, esz, want_exp);
-  const bool fused = sp_all == 3 && 2 * (sm_both + 1024) <= (size_t)di.smem_sm &&
-                     (tiles <= (int64_t)4 * 2 * di.sms || getenv("RF_FUSE") != nullptr) &&
-                     getenv("RF_NO_FUSE") == nullptr;
   if (fused) {
     e = launch_radius<3>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, sm_both, tiles, di.sms, s);
   } else {
@@ -1433,12 +1454,13 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     // first launch is ordered normally after both.
     const bool pdl = want_df && want_std && getenv("RF_NO_PDL") == nullptr;
     if (pdl) Pv[VAR_DF].pdl_trigger = 1;
+    const int minb = three ? 3 : RF_MIN_BLOCKS;
     if (want_df)
-      e = launch_radius<2>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, smem_bytes(2, r, tma, esz, Pv[VAR_DF].do_exp), tiles,
-                           di.sms, s);
+      e = launch_radius<2>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, smem_bytes(2, r, tma, esz, Pv[VAR_DF].do_exp, minb),
+                           tiles, di.sms, s, false, three);
     if (e == cudaSuccess && want_std)
-      e = launch_radius<1>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, smem_bytes(1, r, tma, esz, Pv[VAR_STD].do_exp), tiles,
-                           di.sms, s, pdl);
+      e = launch_radius<1>(Pv[VAR_STD], Pv[VAR_DF], tmap, tma, smem_bytes(1, r, tma, esz, Pv[VAR_STD].do_exp, minb),
+                           tiles, di.sms, s, pdl, three);
   }
   if (e != cudaSuccess) return fail(RF_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return RF_OK;

@@ -48,11 +48,13 @@ def test_launch_count_fused():
     lib = N.load()
     f32, u16 = N.RF_DEPTH_F32_M, N.RF_DEPTH_U16_MM
     both = N.RF_IMPLICIT_STANDARD | N.RF_IMPLICIT_RGBD
-    for window in (3, 5, 7, 9, 11):
+    for window in (9, 11):  # fused at one frame
         assert lib.rf_launches_per_call(both, window, f32, 1, 480, 640) == 1, window
+    for window in (3, 5, 7):  # one wave of tiles at small radii: a launch per space at three CTAs per SM
+        assert lib.rf_launches_per_call(both, window, f32, 1, 480, 640) == 2, window
     for window in (3, 5, 7, 9, 11, 15, 31):
         assert lib.rf_launches_per_call(both, window, f32, 64, 480, 640) == 2, window
-    assert lib.rf_launches_per_call(both, 15, u16, 1, 480, 640) == 1
+    assert lib.rf_launches_per_call(both, 15, u16, 1, 480, 640) == 1  # fused
 
 
 @pytest.mark.parametrize("fx,fy,cx,cy,w,h,msg", [
