@@ -276,7 +276,8 @@ def run_reference(args, world, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Voronoi planes, BASELINE config 2)",
         "config": {"workload": "C2: 64x640x480 f32 depth, window 5, implicit-rgbd + implicit-standard",
                    "note": "each step fits a bounded sample of the workload (whole C2 frames, both "
-                           "formulations, for ~2 s of wall time); value = pixel-fits/s of those samples "
+                           f"formulations, for ~{budget:.2f} s of wall time, at least one frame); value = "
+                           "pixel-fits/s of those samples "
                            "(median over steps); a whole 64-frame step would take "
                            f"{step_fits / (value * 1e6):.1f} s at this rate",
                    "sample_seconds_per_step": total / max(args.steps, 1)},
