@@ -344,6 +344,9 @@ rf_status rf_fit_pixels(const rf_tables* t, const void* depth, int dtype, int64_
     P.tan_y = t->tan_y;
     P.ifx = 1.0 / t->intr.fx;
     P.ify = 1.0 / t->intr.fy;
+    P.ifx2 = P.ifx * P.ifx;
+    P.ify2 = P.ify * P.ify;
+    P.ifxy = P.ifx * P.ify;
     P.row_pitch = row_pitch;
     P.frame_stride = row_pitch * H;
     P.out_frame = (int64_t)H * W;

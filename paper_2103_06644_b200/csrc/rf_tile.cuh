@@ -43,6 +43,7 @@ struct KParams {
   const double* tan_x;  // [W]
   const double* tan_y;  // [H]
   double ifx, ify;
+  double ifx2, ify2, ifxy;  // ifx^2, ify^2, ifx ify (host-computed, IEEE identical)
   int64_t row_pitch;
   int64_t frame_stride;
   int64_t out_frame;    // H*W

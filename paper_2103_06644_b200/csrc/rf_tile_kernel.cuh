@@ -270,25 +270,23 @@ __device__ __forceinline__ void accum_sample(double* h, int* hi, double p, int d
 // window moments -> centred scatter C (3x3) and mean mu of the space's monomials
 // (scatter_from_integrals / accumulate_scatter_naive, fitting.py:339-533, centred); txo, tyo:
 // tan of the dx / dy origin
-template <int VAR>
-__device__ __forceinline__ void assemble(const double* h, const int* hi, double txo, double tyo, double ifx,
-                                         double ify, double invn, Sym3& C, double& mu0, double& mu1, double& mu2) {
+template <int VAR, bool WIDE>
+__device__ __forceinline__ void assemble(const double* h, const int* hi, double txo, double tyo, const KParams& P,
+                                         double invn, Sym3& C, double& mu0, double& mu1, double& mu2) {
+  const double ifx = P.ifx, ify = P.ify;
   if (VAR == VAR_DF) {
-    const long long n = hi[0], sx = hi[1], sy = hi[2], sxx = hi[3], sxy = hi[4], syy = hi[5];
-    const double cq00 = (double)(n * sxx - sx * sx) * invn;
-    const double cq01 = (double)(n * sxy - sx * sy) * invn;
-    const double cq11 = (double)(n * syy - sy * sy) * invn;
+    // exact integer geometry: compile-time radii (r <= 15) keep n sum dx^2 - (sum dx)^2 and
+    // the other two in 32 bits; the generic radius (r <= 32) needs 64
+    using I = typename std::conditional<WIDE, long long, int>::type;
+    const I n = hi[0], sx = hi[1], sy = hi[2], sxx = hi[3], sxy = hi[4], syy = hi[5];
     const double mw = h[0] * invn;
     const double fsx = (double)sx, fsy = (double)sy;
-    const double cq02 = fma(-fsx, mw, h[3]);
-    const double cq12 = fma(-fsy, mw, h[2]);
-    const double cq22 = fma(-h[0], mw, h[1]);
-    C.c00 = cq00 * (ifx * ifx);
-    C.c01 = cq01 * (ifx * ify);
-    C.c11 = cq11 * (ify * ify);
-    C.c02 = cq02 * ifx;
-    C.c12 = cq12 * ify;
-    C.c22 = cq22;
+    C.c00 = (double)(n * sxx - sx * sx) * (invn * P.ifx2);
+    C.c01 = (double)(n * sxy - sx * sy) * (invn * P.ifxy);
+    C.c11 = (double)(n * syy - sy * sy) * (invn * P.ify2);
+    C.c02 = fma(-fsx, mw, h[3]) * ifx;
+    C.c12 = fma(-fsy, mw, h[2]) * ify;
+    C.c22 = fma(-h[0], mw, h[1]);
     mu0 = fma(fsx * invn, ifx, txo);
     mu1 = fma(fsy * invn, ify, tyo);
     mu2 = mw;
@@ -539,7 +537,7 @@ __device__ __forceinline__ void slow_pixel(const TileCtx& T, const KParams& P, i
   const double invn = 1.0 / nd;
   Sym3 C;
   double mu0, mu1, mu2;
-  assemble<VAR>(h, hi, txo, tyo, P.ifx, P.ify, invn, C, mu0, mu1, mu2);
+  assemble<VAR, RT == 0>(h, hi, txo, tyo, P, invn, C, mu0, mu1, mu2);
   const int64_t p = T.frame * P.out_frame + (int64_t)gy * P.W + gx;
   float kap = 0.0f;
   bool have_kap = false;
@@ -586,7 +584,6 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
   if (gy >= P.H || gxs >= P.W) return;
   const double txo = __ldg(P.tan_x + gxs);
   const double tyo = __ldg(P.tan_y + (CENTRED ? gy : T.y0));  // origin row of dy
-  const double ifx = P.ifx, ify = P.ify;
   const double* vrow = T.vd + orow * VRS;
   const CountT<RT>* irow = static_cast<const CountT<RT>*>(T.vi) + orow * VRS;
   const int vstride = TH * VRS;
@@ -638,7 +635,7 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
       const double invn = inv_count(nwin);
       Sym3 C;
       double mu0, mu1, mu2;
-      assemble<VAR>(h, hi, txo, tyo, ifx, ify, invn, C, mu0, mu1, mu2);
+      assemble<VAR, RT == 0>(h, hi, txo, tyo, P, invn, C, mu0, mu1, mu2);
       float kap = 0.0f;
       if (P.do_imp && nwin >= 4) {
         WindowFit f;
