@@ -608,13 +608,16 @@ __device__ __forceinline__ bool solve_fast(const Sym3& C, double m0, double m1, 
   const double B01 = E02 * E12 - E01 * E22;
   const double B02 = E01 * E12 - E02 * E11;
   const double B12 = E01 * E02 - E00 * E12;
-  const double a0 = fabs(B00), a1 = fabs(B11), a2 = fabs(B22);
+  // the column is chosen on the high words of |B_kk| (integer pipe; any column within 2^-20
+  // of the largest diagonal is as good); all three below 2^-1022 go to the robust path
+  const int a0 = __double2hiint(B00) & 0x7fffffff, a1 = __double2hiint(B11) & 0x7fffffff,
+            a2 = __double2hiint(B22) & 0x7fffffff;
   const bool s0 = a0 >= a1 && a0 >= a2;
   const bool s1 = !s0 && a1 >= a2;
   const double u0 = s0 ? B00 : s1 ? B01 : B02;
   const double u1 = s0 ? B01 : s1 ? B11 : B12;
   const double u2 = s0 ? B02 : s1 ? B12 : B22;
-  ok &= (s0 ? a0 : s1 ? a1 : a2) > 0.0;
+  ok &= (a0 | a1 | a2) >= 0x00100000;
   out.u0 = u0;
   out.u1 = u1;
   out.u2 = u2;

@@ -52,8 +52,7 @@ struct KParams {
   int do_imp, do_exp;  // implicit / explicit fit of this kernel's space requested
   OutPlanes imp, exp;  // implicit-* / explicit-* output planes of the space
   // programmatic dependent launch of the next kernel in the stream: 0 at exit, 1 at entry (the
-  // first space's launch of a two-launch call: the second space shares nothing with it), 2 when
-  // the CTA starts its last tile (unused)
+  // first space's launch of a two-launch call: the second space shares nothing with it)
   int pdl_trigger;
 };
 

@@ -926,7 +926,6 @@ __global__ void __launch_bounds__(NTHREADS, MINB)
   int it = 0;
   TileIter ti(blockIdx.x, gridDim.x, ntx, nty);
   for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it, ti.advance()) {
-    if (P.pdl_trigger == 2 && t + gridDim.x >= total) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const TileGeom g = ti.geom();
     T.frame = g.frame;
     T.x0 = g.x0;
