@@ -326,10 +326,12 @@ def parity_check(depth, out, cam, forms, rng_seed: int = 7) -> dict:
             m = compare(gpu_flat(out[f], frame, sel), ref, explicit_fit=f.startswith("explicit"))
             res["checks"].append({"frame": frame, "form": f, "pixels": m["pixels"], "compared": m["compared"],
                                   "status_mismatch": m["status_mismatch"],
+                                  "degenerate_ref": m["degenerate_ref"], "degenerate_mismatch": m["degenerate_mismatch"],
                                   "max_normal_rad": m["max_normal_rad"], "max_residual_rel": m["max_residual_rel"],
                                   "max_curvature_rel": m["max_curvature_rel"], "ok": m["ok"]})
             res["ok"] = res["ok"] and m["ok"]
-    res["tolerances"] = {"normal_rad": 1e-4, "residual_rel": 1e-4, "curvature_rel": 1e-4, "status_bits": "exact"}
+    res["tolerances"] = {"normal_rad": 1e-4, "residual_rel": 1e-4, "curvature_rel": 1e-4, "status_bits": "exact",
+                         "degenerate_bit": "reported (a float threshold, fitting.py:552-554; SURVEY A18)"}
     return res
 
 
