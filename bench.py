@@ -45,6 +45,7 @@ FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 BYTES_IN = 4  # float32 depth
 BYTES_OUT = 25  # per pixel per formulation: 12 normal + 4 offset + 4 residual + 4 curvature + 1 status
 FP64_PEAK_TOPS = 17.1  # measured DFMA throughput, T/s (profiles/peak_probe_r1.txt)
+NOMINAL_HBM_GBS = 8000.0  # B200 HBM3e nominal (the roofline itself uses the measured copy bandwidth)
 
 
 def hbm_peak():
@@ -453,6 +454,9 @@ def run_ours(args, world, rank, local):
                 "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak,
                 "step_bytes_note": "whole step at 27 B per pixel-fit (input read once for both forms, V=2)",
                 "launches_per_step": launches_step, "launch_ms": launch_ms,
+                # also against the nominal HBM3e bandwidth (~8 TB/s)
+                "nominal": {"peak": NOMINAL_HBM_GBS, "frac": achieved / NOMINAL_HBM_GBS,
+                            "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / NOMINAL_HBM_GBS},
                 "fp64": profiled_fp64("per_space", launch_ms),
                 "binding": profiled_pipes("per_space")}
 
