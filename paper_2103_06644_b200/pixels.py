@@ -170,8 +170,20 @@ class PixelFits:
             status=torch.empty((batch, height, width), dtype=torch.uint8, device=device),
         )
 
-    def _c(self) -> N.RfPixelOut:
-        for t in (self.normal, self.offset, self.residual, self.curvature, self.status):
+    def _c(self, batch: int, height: int, width: int, device: torch.device) -> N.RfPixelOut:
+        """C view of caller-provided output planes, after checking that the kernels can write a
+        [batch, height, width] result into them (shape, element type, device, contiguity)."""
+        shape = (batch, height, width)
+        for name, t, dt, sh in (("normal", self.normal, torch.float32, shape + (3,)),
+                                ("offset", self.offset, torch.float32, shape),
+                                ("residual", self.residual, torch.float32, shape),
+                                ("curvature", self.curvature, torch.float32, shape),
+                                ("status", self.status, torch.uint8, shape)):
+            ok_shape = tuple(t.shape) == sh or (batch == 1 and tuple(t.shape) == sh[1:])  # [H, W] frame
+            if not ok_shape or t.dtype != dt:
+                raise ValueError(f"output {name} must be {dt} of shape {sh}, got {t.dtype} {tuple(t.shape)}")
+            if t.device != device:
+                raise ValueError(f"output {name} on {t.device}, depth on {device}")
             if not t.is_contiguous():
                 raise ValueError("output tensors must be contiguous")
         return N.RfPixelOut(self.normal.data_ptr(), self.offset.data_ptr(), self.residual.data_ptr(),
@@ -251,7 +263,7 @@ def fit_pixels(
     outs = (N.RfPixelOut * N.RF_NUM_FORMULATIONS)()
     for f in formulations:
         fmask |= 1 << _FORM_ID[f]
-        outs[_FORM_ID[f]] = out[f]._c()
+        outs[_FORM_ID[f]] = out[f]._c(B, H, W, d.device)
     cur = torch.cuda.current_stream(d.device)
     if stream is None:
         stream = cur

@@ -188,3 +188,24 @@ def test_naive_helpers_and_small_solvers():
     assert sx.target_sq == pytest.approx(12 * 0.25) and sx.rhs[2] == pytest.approx(6.0)
     with pytest.raises(rf.InsufficientSamplesError):
         rf.accumulate_scatter_naive(smp[:3], "implicit-rgbd")
+
+
+def test_output_planes_are_checked_before_the_launch():
+    """Caller-provided outputs must hold a [B, H, W] result (fit_pixels writes through raw
+    pointers): wrong shapes, element types or devices raise instead of corrupting memory."""
+    import torch
+
+    from paper_2103_06644_b200.pixels import PixelFits
+
+    cpu = torch.device("cpu")
+    o = PixelFits.empty(2, 4, 5, cpu)
+    o._c(2, 4, 5, cpu)
+    with pytest.raises(ValueError):
+        o._c(3, 4, 5, cpu)
+    with pytest.raises(ValueError):
+        PixelFits(o.normal, o.offset.double(), o.residual, o.curvature, o.status)._c(2, 4, 5, cpu)
+    with pytest.raises(ValueError):
+        PixelFits(o.normal[:, :, :, :2], o.offset, o.residual, o.curvature, o.status)._c(2, 4, 5, cpu)
+    # a single frame may come without its batch dimension
+    one = PixelFits.empty(1, 4, 5, cpu)
+    PixelFits(*(getattr(one, k)[0] for k in ("normal", "offset", "residual", "curvature", "status")))._c(1, 4, 5, cpu)
