@@ -92,7 +92,7 @@ size_t smem_bytes(int sp, int r, bool tma, int esz, bool exp = false, int minb =
   const bool rt = tma && compiled_radius(r) && !generic15;  // the kernel's RT > 0
   const bool noprim = rt && noprim_radius(r);          // the kernel's ZF (RT == r): float Z tile
   const int psp = nsp - ((sp & 1) && noprim ? 1 : 0);  // spaces with an fp64 tile
-  const bool dbuf = rt && r <= 3 && sp != 3 && minb < 3;  // the kernel's DBUF
+  const bool dbuf = rt && r <= 3 && sp != 3 && (minb < 3 || TH <= 8);  // the kernel's DBUF
   const size_t raw = tma ? (((size_t)hh * hwp * esz + 127) & ~(size_t)127) : 0;
   const size_t vrs = 4 * (size_t)(noprim ? (hw + 3) / 4 : vq_of(hw));
   const size_t counts = ((rt ? sizeof(int) : sizeof(int2)) * (size_t)TH * vrs + 7) & ~(size_t)7;

@@ -329,6 +329,9 @@ struct TileCtx {
   double* vd;   // [NVD][TH][VRS] column sums of the current space
   void* vi;     // [TH][VRS] valid-count geometry (both spaces), CountT<RT>
   float* xstage;
+  // tan of this thread's row-pass origin (segment start column, dy origin row), loaded at the
+  // start of the tile so the global-load latency hides behind the TMA wait and the conversion
+  double txo, tyo;
 };
 
 // primary of halo element (row, col) of the tile for space VAR (ZF: the standard space's Z
@@ -582,8 +585,8 @@ __device__ __forceinline__ void row_pass(const TileCtx& T, const KParams& P, uns
   const int gy = T.y0 + orow;
   const int gxs = T.x0 + xs;
   if (gy >= P.H || gxs >= P.W) return;
-  const double txo = __ldg(P.tan_x + gxs);
-  const double tyo = __ldg(P.tan_y + (CENTRED ? gy : T.y0));  // origin row of dy
+  const double txo = T.txo;
+  const double tyo = T.tyo;  // origin row of dy
   const double* vrow = T.vd + orow * VRS;
   const CountT<RT>* irow = static_cast<const CountT<RT>*>(T.vi) + orow * VRS;
   const int vstride = TH * VRS;
@@ -870,7 +873,7 @@ __global__ void __launch_bounds__(NTHREADS, MINB)
   constexpr bool CENTRED = RT > 0 && RT <= RF_CENTRED_MAX;
   // one space per launch: the double buffer fits two CTAs per SM; both spaces (small
   // batches) keep one buffer and close the tile with a barrier instead
-  constexpr bool DBUF = CENTRED && RT <= 3 && SP != 3 && MINB < 3;
+  constexpr bool DBUF = CENTRED && RT <= 3 && SP != 3 && (MINB < 3 || TH <= 8);
   const int nprim = HH_ * HW_;
   const int nsp = ((PSP & 2) ? 1 : 0) + ((PSP & 1) && !NOPRIM ? 1 : 0);  // fp64 tiles
   double* prim_base = reinterpret_cast<double*>(smem_raw + NRAW * raw_bytes);  // [DBUF ? 2 : 1][nsp][HH_][HW_]
@@ -937,6 +940,12 @@ __global__ void __launch_bounds__(NTHREADS, MINB)
     if (DBUF) {
       T.pw = prim_base + (it & 1) * nsp * nprim;
       T.pz = T.pw + ((PSP & 2) ? nprim : 0);
+    }
+    {
+      // the row pass's tan origins (clamped: threads past the frame edge return before use)
+      const int orow = tid / (TW / KSEG), xs = (tid % (TW / KSEG)) * KSEG;
+      T.txo = __ldg(P.tan_x + min(x0 + xs, P.W - 1));
+      T.tyo = __ldg(P.tan_y + (CENTRED ? min(y0 + orow, P.H - 1) : y0));
     }
     T.sx = (x0 - r) - box_x(x0 - r, al);  // raw index shift
     T.sy = (y0 - r) - max(y0 - r, 0);
